@@ -1,0 +1,123 @@
+/* C ABI of the B200-native GaNi cell-problem solver (libfftcell_b200.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `fftcell`
+ * (/root/reference/pkg/src/fftcell).  The reference has no FFI; its boundary is
+ * the Python call signature of fftcell.solver / fftcell.homogenize, so every
+ * entry point below names the reference function it replaces.  The Python
+ * package paper_1311_0089_b200 binds these through ctypes and keeps the
+ * reference signatures.
+ *
+ * Conventions (all entry points):
+ *  - plain pointers and sizes; host arrays use the reference layouts exactly:
+ *    fields (R, d, *N) row-major, FFT-shifted storage (grid.py:9-20), fp64;
+ *    coefficients isotropic (*N) or packed symmetric (d(d+1)/2, *N)
+ *    (material.py:30-49);
+ *  - host pointers are borrowed for the duration of the call only;
+ *  - calls are synchronous; a context is not thread-safe;
+ *  - return FC_OK (0) or an FC_E* code; fc_last_error() describes the failure
+ *    (thread-local).  Invalid arguments map to the reference's ValueError.
+ *  - no CPU fallback: without a usable sm_100 device every call fails with
+ *    FC_ECUDA.
+ */
+#ifndef FFTCELL_B200_H
+#define FFTCELL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FC_OK 0
+#define FC_EINVAL 1   /* bad argument (reference: ValueError) */
+#define FC_ENOMEM 2   /* device allocation failed */
+#define FC_ECUDA 3    /* CUDA runtime error / no device */
+#define FC_ENOTSUP 4  /* shape outside the supported envelope */
+
+#define FC_MAX_RHS 8
+
+/* Coefficient kinds (material.py:147-158 isotropic, material.py:90-145 packed). */
+#define FC_COEF_ISOTROPIC 0
+#define FC_COEF_PACKED 1
+
+/* Projector selection for fc_project (solver.py:112-122). */
+#define FC_PROJ_ORTHOGONAL 0   /* _Projector.apply_orthogonal  */
+#define FC_PROJ_GAMMA_REF 1    /* _Projector.apply_gamma_ref   */
+
+/* Solve outcome codes in fc_report.status. */
+#define FC_ST_OK 0          /* converged (or stopped with converged flag) */
+#define FC_ST_MAXITER 1     /* max_iter exhausted, converged = 0 (solver.py:227-230) */
+#define FC_ST_BREAKDOWN 2   /* pAp <= 0 (solver.py:203-212); detail = pAp */
+#define FC_ST_DIVERGENT 3   /* fixed-point growth streak (solver.py:275-288) */
+
+typedef struct fc_ctx fc_ctx;
+
+/* Per right-hand-side outcome: mirrors SolveReport (solver.py:77-87). */
+typedef struct fc_report {
+  int32_t iterations;
+  int32_t converged;
+  int32_t status;
+  int32_t hist_len;   /* entries written to the history row */
+  double detail;      /* pAp at breakdown */
+} fc_report;
+
+int32_t fc_version(void);
+const char* fc_last_error(void);
+int32_t fc_device_count(int32_t* count);
+
+/* GridSpec + device binding (grid.py:30-83): odd positive shape, Y > 0. */
+int32_t fc_create(fc_ctx** out, int32_t dim, const int64_t* shape, const double* half_periods,
+                  int32_t device);
+void fc_destroy(fc_ctx* ctx);
+
+/* CoefficientField upload (material.py:90-158): count = N (isotropic) or nsym*N (packed). */
+int32_t fc_set_coefficients(fc_ctx* ctx, int32_t kind, const double* host, int64_t count);
+
+/* apply_A (material.py:182-187): out = A u for nfields fields of shape (d, *N). */
+int32_t fc_apply_A(fc_ctx* ctx, const double* u, double* out, int32_t nfields);
+
+/* _Projector(spec, ref).apply_orthogonal / apply_gamma_ref (solver.py:90-122).
+ * ref_matrix (d x d, row-major) is required for FC_PROJ_GAMMA_REF. */
+int32_t fc_project(fc_ctx* ctx, int32_t which, const double* ref_matrix, const double* u, double* out,
+                   int32_t nfields);
+
+/* apply_system (solver.py:125-129): out = G A u with the orthogonal G. */
+int32_t fc_apply_system(fc_ctx* ctx, const double* u, double* out, int32_t nfields);
+
+/* solve_cg (solver.py:142-230) for nrhs independent load cases E[nrhs][d].
+ *  lam      : scalar reference lambda (> 0) or <= 0 for none (solver.py:162-171)
+ *  init     : NULL or warm starts (nrhs, d, *N)
+ *  x_out    : NULL (solution stays resident on the device) or (nrhs, d, *N)
+ *  rep      : nrhs reports
+ *  hist     : NULL or nrhs rows of (max_iter + 1) residual norms
+ *  iterates : NULL or room for iterates_cap snapshots of (nrhs, d, *N); returns the
+ *             number written in *n_iterates (record_iterates, solver.py:188-189,219-220) */
+int32_t fc_solve_cg(fc_ctx* ctx, int32_t nrhs, const double* E, double tol, int32_t max_iter, double lam,
+                    const double* init, double* x_out, fc_report* rep, double* hist, double* iterates,
+                    int64_t iterates_cap, int64_t* n_iterates);
+
+/* solve_neumann (solver.py:238-295): e <- E - Gamma0 (A - A0) e.
+ *  ref_matrix : A0 (d x d)    scale : per-RHS stopping scale max(|E_N|, tiny) (solver.py:258)
+ *  x_out      : NULL or the fluctuation e - E, (nrhs, d, *N)
+ *  hist       : NULL or nrhs rows of max_iter update norms */
+int32_t fc_solve_fixed_point(fc_ctx* ctx, int32_t nrhs, const double* E, double tol, int32_t max_iter,
+                             const double* ref_matrix, const double* scale, double* x_out, fc_report* rep,
+                             double* hist);
+
+/* Energy matrix of the last solve (homogenize.py:59-67, transforms.py:168-176):
+ * out[a][b] = < A (E_a + x_a), E_b + x_b >, a, b < nrhs.  x = NULL uses the
+ * solution resident on the device; otherwise x is (nrhs, d, *N) on the host. */
+int32_t fc_energy(fc_ctx* ctx, int32_t nrhs, const double* E, const double* x, double* out);
+
+/* Instrumentation used by bench.py: per-kernel CUDA-event timing and a launch counter. */
+int32_t fc_set_profiling(fc_ctx* ctx, int32_t on);
+int32_t fc_profile_count(fc_ctx* ctx);
+int32_t fc_profile_get(fc_ctx* ctx, int32_t i, char* name, int32_t name_cap, int64_t* launches, double* total_ms);
+int32_t fc_profile_reset(fc_ctx* ctx);
+int64_t fc_launch_count(fc_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FFTCELL_B200_H */

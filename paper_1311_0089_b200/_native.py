@@ -1,0 +1,254 @@
+"""ctypes binding of ``libfftcell_b200.so`` (C ABI: ``include/fftcell_b200.h``).
+
+The shared library is built in-tree by ``__graft_entry__.build()``.  There is
+no CPU fallback: if the library or a CUDA device is missing every call raises
+``RuntimeError`` (north_star "no CPU fallback").
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libfftcell_b200.so"
+MAX_RHS = 8
+
+FC_OK, FC_EINVAL, FC_ENOMEM, FC_ECUDA, FC_ENOTSUP = 0, 1, 2, 3, 4
+ST_OK, ST_MAXITER, ST_BREAKDOWN, ST_DIVERGENT = 0, 1, 2, 3
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+class Report(ctypes.Structure):
+    _fields_ = [
+        ("iterations", ctypes.c_int32),
+        ("converged", ctypes.c_int32),
+        ("status", ctypes.c_int32),
+        ("hist_len", ctypes.c_int32),
+        ("detail", ctypes.c_double),
+    ]
+
+
+_lib = None
+
+# (name, restype, argtypes) for every symbol declared in include/fftcell_b200.h
+SIGNATURES = [
+    ("fc_version", ctypes.c_int32, []),
+    ("fc_last_error", ctypes.c_char_p, []),
+    ("fc_device_count", ctypes.c_int32, [ctypes.POINTER(ctypes.c_int32)]),
+    ("fc_create", ctypes.c_int32,
+     [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, _i64p, _dp, ctypes.c_int32]),
+    ("fc_destroy", None, [ctypes.c_void_p]),
+    ("fc_set_coefficients", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, _dp, ctypes.c_int64]),
+    ("fc_apply_A", ctypes.c_int32, [ctypes.c_void_p, _dp, _dp, ctypes.c_int32]),
+    ("fc_project", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, _dp, _dp, _dp, ctypes.c_int32]),
+    ("fc_apply_system", ctypes.c_int32, [ctypes.c_void_p, _dp, _dp, ctypes.c_int32]),
+    ("fc_solve_cg", ctypes.c_int32,
+     [ctypes.c_void_p, ctypes.c_int32, _dp, ctypes.c_double, ctypes.c_int32, ctypes.c_double, _dp, _dp,
+      ctypes.POINTER(Report), _dp, _dp, ctypes.c_int64, _i64p]),
+    ("fc_solve_fixed_point", ctypes.c_int32,
+     [ctypes.c_void_p, ctypes.c_int32, _dp, ctypes.c_double, ctypes.c_int32, _dp, _dp, _dp,
+      ctypes.POINTER(Report), _dp]),
+    ("fc_energy", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, _dp, _dp, _dp]),
+    ("fc_set_profiling", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32]),
+    ("fc_profile_count", ctypes.c_int32, [ctypes.c_void_p]),
+    ("fc_profile_get", ctypes.c_int32,
+     [ctypes.c_void_p, ctypes.c_int32, ctypes.c_char_p, ctypes.c_int32, _i64p, _dp]),
+    ("fc_profile_reset", ctypes.c_int32, [ctypes.c_void_p]),
+    ("fc_launch_count", ctypes.c_int64, [ctypes.c_void_p]),
+]
+
+
+def lib():
+    """Load the CUDA library (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"CUDA extension {LIB_PATH.name} is not built; run `python -c "
+                "'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)"
+            )
+        handle = ctypes.CDLL(str(LIB_PATH))
+        for name, res, args in SIGNATURES:
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def _check(rc):
+    if rc == FC_OK:
+        return
+    msg = lib().fc_last_error().decode(errors="replace")
+    if rc == FC_EINVAL:
+        raise ValueError(msg)
+    if rc == FC_ENOTSUP:
+        raise NotImplementedError(msg)
+    if rc == FC_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"CUDA error: {msg}")
+
+
+def _ptr(a):
+    return a.ctypes.data_as(_dp) if a is not None else None
+
+
+def _c64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def device_count():
+    n = ctypes.c_int32(0)
+    rc = lib().fc_device_count(ctypes.byref(n))
+    return int(n.value) if rc == FC_OK else 0
+
+
+class Context:
+    """One GridSpec bound to one GPU: coefficients, FFT plans and workspace in HBM."""
+
+    def __init__(self, spec, device_id: int = 0):
+        self.spec = spec
+        self.device_id = device_id
+        self.d = spec.dim
+        self.shape = tuple(spec.shape)
+        self.total = spec.total
+        self._h = ctypes.c_void_p()
+        shape = np.array(spec.shape, dtype=np.int64)
+        Y = np.array(spec.half_periods, dtype=np.float64)
+        _check(lib().fc_create(ctypes.byref(self._h), spec.dim, shape.ctypes.data_as(_i64p), _ptr(Y), device_id))
+        self.isotropic = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.fc_destroy(h)
+            self._h = ctypes.c_void_p()
+
+    # -- coefficients ------------------------------------------------------
+    def set_coefficients(self, a):
+        if a.isotropic_values is not None:
+            host = _c64(a.isotropic_values)
+            kind = 0
+        else:
+            host = _c64(a.components)
+            kind = 1
+        _check(lib().fc_set_coefficients(self._h, kind, _ptr(host), host.size))
+        self.isotropic = kind == 0
+
+    # -- batched field operators ------------------------------------------
+    def _batched(self, fn, u, *extra):
+        u = _c64(u)
+        fshape = (self.d,) + self.shape
+        single = u.shape == fshape
+        ub = u.reshape((-1,) + fshape)
+        out = np.empty_like(ub)
+        for s in range(0, ub.shape[0], MAX_RHS):
+            chunk = np.ascontiguousarray(ub[s:s + MAX_RHS])
+            o = np.empty_like(chunk)
+            _check(fn(self._h, *extra, _ptr(chunk), _ptr(o), chunk.shape[0]))
+            out[s:s + MAX_RHS] = o
+        return out.reshape(fshape) if single else out.reshape(u.shape)
+
+    def apply_A(self, u):
+        return self._batched(lib().fc_apply_A, u)
+
+    def apply_system(self, u):
+        return self._batched(lib().fc_apply_system, u)
+
+    def project(self, which, ref_matrix, u):
+        ref = None if ref_matrix is None else _c64(ref_matrix)
+        return self._batched(lib().fc_project, u, which, _ptr(ref))
+
+    # -- solvers -----------------------------------------------------------
+    def solve_cg(self, E, tol, max_iter, lam=None, init=None, want_x=True, record_iterates=False):
+        E = _c64(np.atleast_2d(E))
+        R = E.shape[0]
+        fshape = (R, self.d) + self.shape
+        x = np.empty(fshape) if want_x else None
+        init = None if init is None else _c64(init).reshape(fshape)
+        reps = (Report * R)()
+        hist = np.zeros((R, max_iter + 1))
+        its = None
+        n_it = ctypes.c_int64(0)
+        if record_iterates:
+            its = np.empty((max_iter + 1,) + fshape)
+        _check(lib().fc_solve_cg(
+            self._h, R, _ptr(E), float(tol), int(max_iter), float(lam) if lam is not None else -1.0,
+            _ptr(init), _ptr(x), reps, _ptr(hist), _ptr(its), 0 if its is None else its.shape[0],
+            ctypes.byref(n_it)))
+        out = []
+        for r in range(R):
+            rp = reps[r]
+            out.append(dict(iterations=rp.iterations, converged=bool(rp.converged), status=rp.status,
+                            detail=rp.detail, history=hist[r, :rp.hist_len].copy()))
+        iterates = None if its is None else its[: n_it.value]
+        return out, x, iterates
+
+    def solve_fixed_point(self, E, tol, max_iter, ref_matrix, scale, want_x=True):
+        E = _c64(np.atleast_2d(E))
+        R = E.shape[0]
+        x = np.empty((R, self.d) + self.shape) if want_x else None
+        reps = (Report * R)()
+        hist = np.zeros((R, max_iter))
+        sc = _c64(np.broadcast_to(np.asarray(scale, dtype=float), (R,)))
+        _check(lib().fc_solve_fixed_point(self._h, R, _ptr(E), float(tol), int(max_iter), _ptr(_c64(ref_matrix)),
+                                          _ptr(sc), _ptr(x), reps, _ptr(hist)))
+        out = []
+        for r in range(R):
+            rp = reps[r]
+            out.append(dict(iterations=rp.iterations, converged=bool(rp.converged), status=rp.status,
+                            detail=rp.detail, history=hist[r, :rp.hist_len].copy()))
+        return out, x
+
+    def energy(self, E, x=None):
+        """``M[a, b] = <A (E_a + x_a), E_b + x_b>`` over the batch (resident solution if x is None)."""
+        E = _c64(np.atleast_2d(E))
+        R = E.shape[0]
+        out = np.empty((R, R))
+        xx = None if x is None else _c64(x)
+        _check(lib().fc_energy(self._h, R, _ptr(E), _ptr(xx), _ptr(out)))
+        return out
+
+    # -- instrumentation ---------------------------------------------------
+    def set_profiling(self, on: bool):
+        _check(lib().fc_set_profiling(self._h, 1 if on else 0))
+
+    def profile(self):
+        out = {}
+        buf = ctypes.create_string_buffer(64)
+        for i in range(lib().fc_profile_count(self._h)):
+            n = ctypes.c_int64()
+            ms = ctypes.c_double()
+            _check(lib().fc_profile_get(self._h, i, buf, 64, ctypes.byref(n), ctypes.byref(ms)))
+            out[buf.value.decode()] = (int(n.value), float(ms.value))
+        return out
+
+    def profile_reset(self):
+        _check(lib().fc_profile_reset(self._h))
+
+    def launch_count(self):
+        return int(lib().fc_launch_count(self._h))
+
+
+_spec_contexts: dict = {}
+
+
+def context_for_spec(spec, device_id: int = 0) -> Context:
+    """Coefficient-free context per (spec, device), for the bare projectors."""
+    key = (spec, device_id)
+    ctx = _spec_contexts.get(key)
+    if ctx is None:
+        if len(_spec_contexts) >= 16:
+            _spec_contexts.pop(next(iter(_spec_contexts)))
+        ctx = Context(spec, device_id)
+        _spec_contexts[key] = ctx
+    return ctx
+
+
+def default_device() -> int:
+    return int(os.environ.get("LOCAL_RANK", "0")) if device_count() > 1 else 0

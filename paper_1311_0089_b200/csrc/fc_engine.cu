@@ -1,0 +1,861 @@
+// Host engine and C ABI (include/fftcell_b200.h) of the B200 GaNi solver.
+//
+// One context = one GridSpec bound to one GPU: the coefficient field, the
+// per-axis FFT plans and the solver workspace live in HBM for the lifetime of
+// the context; the CG / fixed-point loops run entirely on the device with the
+// per-RHS scalars (alpha, beta, stop flags, histories) in device memory.  The
+// host only enqueues iterations and polls one pinned flag, one iteration
+// behind, so the stream never drains between iterations.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/fftcell_b200.h"
+#include "fc_kernels.cuh"
+
+using namespace fc;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_err(e_ == cudaErrorMemoryAllocation ? FC_ENOMEM : FC_ECUDA, "%s: %s (%s:%d)", #call, \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+  } while (0)
+
+#define TRY(call)              \
+  do {                         \
+    int rc_ = (call);          \
+    if (rc_ != FC_OK) return rc_; \
+  } while (0)
+
+struct DevPlan {
+  FftPlan plan{};
+  double2* roots = nullptr;
+};
+
+// Factor plan for an odd length: radix-9 passes first, then 3, 5, other primes.
+bool make_factors(int L, FftPlan& p) {
+  p.L = L;
+  p.nf = 0;
+  int n = L;
+  auto push = [&](int f) {
+    if (p.nf >= kMaxFactors) return false;
+    p.f[p.nf++] = f;
+    return true;
+  };
+  while (n % 9 == 0) { if (!push(9)) return false; n /= 9; }
+  while (n % 3 == 0) { if (!push(3)) return false; n /= 3; }
+  while (n % 5 == 0) { if (!push(5)) return false; n /= 5; }
+  for (int f = 7; n > 1; f += 2) {
+    while (n % f == 0) { if (!push(f)) return false; n /= f; }
+    if ((long long)f * f > n && n > 1) { if (!push(n)) return false; n = 1; }
+  }
+  return true;
+}
+
+struct Prof {
+  std::string name;
+  int64_t launches = 0;
+  double ms = 0.0;
+};
+
+}  // namespace
+
+struct fc_ctx {
+  int device = 0;
+  int dim = 0;
+  int n[3] = {1, 1, 1};
+  double Y[3] = {1, 1, 1};
+  int64_t N = 0;
+  cudaStream_t stream = nullptr;
+  int smem_optin = 0;
+  int num_sms = 0;
+
+  std::map<int, DevPlan> plans;  // by length
+  double* xi = nullptr;          // concatenated per-axis frequency tables
+  int xi_off[3] = {0, 0, 0};
+
+  double* A = nullptr;
+  int coef_kind = -1;
+  int64_t A_count = 0;
+
+  // workspace
+  int Rcap = 0;
+  int hcap = 0;
+  double *x = nullptr, *r = nullptr, *p[2] = {nullptr, nullptr}, *Ap = nullptr;
+  double2 *W1 = nullptr, *W2 = nullptr;
+  double* part = nullptr;
+  int64_t part_cap = 0;
+  RhsState* st = nullptr;
+  double* hist = nullptr;
+  int* any_active = nullptr;
+  int* h_flag = nullptr;  // pinned, 4 slots
+  cudaEvent_t flag_ev[4] = {};
+  double* d_mat = nullptr;
+
+  // tiling
+  RowGeo rg{};
+  MidGeo mg{};
+  OuterGeo og{};
+  size_t smem_row = 0, smem_mid = 0, smem_outer = 0, smem_line = 0;
+
+  // instrumentation
+  bool prof_on = false;
+  std::vector<Prof> prof;
+  std::map<std::string, int> prof_idx;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> ev_pool;
+  int64_t launches = 0;
+
+  Geo geo() const {
+    Geo g{};
+    g.dim = dim;
+    for (int a = 0; a < 3; ++a) g.n[a] = n[a];
+    g.N = N;
+    g.invN = 1.0 / (double)N;
+    for (int a = 0; a < dim; ++a) g.xi[a] = xi + xi_off[a];
+    return g;
+  }
+  Coef coef() const { return Coef{A, coef_kind}; }
+  const FftPlan& plan(int L) const { return plans.at(L).plan; }
+};
+
+namespace {
+
+cudaEvent_t take_event(fc_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Launch wrapper: counts launches and (when profiling) brackets with events.
+template <typename F>
+int launch(fc_ctx* c, const char* name, F&& f) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->prof_on) {
+    e0 = take_event(c);
+    e1 = take_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  f();
+  c->launches++;
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_err(FC_ECUDA, "launch of %s failed: %s", name, cudaGetErrorString(err));
+  if (c->prof_on) {
+    cudaEventRecord(e1, c->stream);
+    auto it = c->prof_idx.find(name);
+    int idx;
+    if (it == c->prof_idx.end()) {
+      idx = (int)c->prof.size();
+      c->prof_idx[name] = idx;
+      c->prof.push_back(Prof{name, 0, 0.0});
+    } else {
+      idx = it->second;
+    }
+    c->pending.push_back({idx, {e0, e1}});
+  }
+  return FC_OK;
+}
+
+// Accumulate finished profiling intervals (call after a stream sync).
+void drain_profile(fc_ctx* c) {
+  for (auto& pe : c->pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pe.second.first, pe.second.second);
+    c->prof[pe.first].launches += 1;
+    c->prof[pe.first].ms += ms;
+    c->ev_pool.push_back(pe.second.first);
+    c->ev_pool.push_back(pe.second.second);
+  }
+  c->pending.clear();
+}
+
+int ensure_plan(fc_ctx* c, int L) {
+  if (c->plans.count(L)) return FC_OK;
+  DevPlan dp;
+  if (!make_factors(L, dp.plan)) return set_err(FC_ENOTSUP, "cannot factor length %d", L);
+  std::vector<double2> roots(L);
+  for (int t = 0; t < L; ++t) {
+    // exp(-2 pi i t / L) in extended precision, exactly conjugate-symmetric
+    int tt = t <= L / 2 ? t : L - t;
+    long double ang = 2.0L * 3.141592653589793238462643383279502884L * (long double)tt / (long double)L;
+    double cr = (double)cosl(ang), si = (double)sinl(ang);
+    roots[t] = make_double2(cr, t <= L / 2 ? -si : si);
+  }
+  roots[0] = make_double2(1.0, 0.0);
+  CK(cudaMalloc(&dp.roots, sizeof(double2) * L));
+  CK(cudaMemcpy(dp.roots, roots.data(), sizeof(double2) * L, cudaMemcpyHostToDevice));
+  dp.plan.roots = dp.roots;
+  c->plans[L] = dp;
+  return FC_OK;
+}
+
+template <typename K>
+int allow_smem(K kernel, int bytes) {
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  return FC_OK;
+}
+
+// Tile selection: smem per CTA <= soft cap (two CTAs per SM) if possible, else opt-in max.
+int choose_tiles(fc_ctx* c) {
+  const size_t soft = 100 * 1024, hard = (size_t)c->smem_optin;
+  const int d = c->dim;
+  if (d == 1) {
+    c->smem_line = (size_t)32 * c->n[0];
+    if (c->smem_line > hard) return set_err(FC_ENOTSUP, "grid axis of length %d exceeds the shared-memory line limit", c->n[0]);
+    return FC_OK;
+  }
+  RowGeo& rg = c->rg;
+  rg.nl = c->n[d - 1];
+  rg.hl = (rg.nl + 1) / 2;
+  rg.np = c->n[d - 2];
+  rg.no = d == 3 ? c->n[0] : 1;
+  {
+    int best = 0;
+    const int npe = (rg.np + 1) & ~1;
+    for (int B = 16; B >= 2; B -= 2) {
+      if (B > npe && B > 2) continue;
+      size_t bytes = (size_t)16 * B * rg.nl;
+      if (bytes <= soft) { best = B; break; }
+    }
+    if (best == 0 && (size_t)32 * rg.nl <= hard) best = 2;
+    if (best == 0) return set_err(FC_ENOTSUP, "contiguous axis of length %d exceeds the shared-memory limit", rg.nl);
+    rg.B = best;
+    rg.ntiles = (rg.np + rg.B - 1) / rg.B;
+    c->smem_row = (size_t)16 * rg.B * rg.nl;
+  }
+  if (d == 3) {
+    MidGeo& mg = c->mg;
+    mg.n0 = c->n[0];
+    mg.n1 = c->n[1];
+    mg.h2 = (c->n[2] + 1) / 2;
+    int best = 0;
+    for (int B = 16; B >= 1; B /= 2) {
+      if (B > mg.n0 && B > 1) continue;
+      if ((size_t)32 * B * mg.n1 <= soft) { best = B; break; }
+    }
+    if (best == 0 && (size_t)32 * mg.n1 <= hard) best = 1;
+    if (best == 0) return set_err(FC_ENOTSUP, "middle axis of length %d exceeds the shared-memory limit", mg.n1);
+    mg.B = best;
+    mg.nib = (mg.n0 + best - 1) / best;
+    c->smem_mid = (size_t)32 * best * mg.n1;
+  }
+  {
+    OuterGeo& og = c->og;
+    og.n0 = c->n[0];
+    og.n1 = d == 3 ? c->n[1] : 1;
+    og.h_last = (c->n[d - 1] + 1) / 2;
+    og.Q = d == 3 ? og.h_last * c->n[1] : og.h_last;
+    int best = 0;
+    for (int QB = 32; QB >= 1; QB /= 2) {
+      if (QB > og.Q && QB > 1) continue;
+      if ((size_t)32 * d * QB * og.n0 <= soft) { best = QB; break; }
+    }
+    if (best == 0 && (size_t)32 * d * og.n0 <= hard) best = 1;
+    if (best == 0) return set_err(FC_ENOTSUP, "outer axis of length %d exceeds the shared-memory limit for d=%d", og.n0, d);
+    og.QB = best;
+    og.nqb = (og.Q + best - 1) / best;
+    c->smem_outer = (size_t)32 * d * best * og.n0;
+  }
+  return FC_OK;
+}
+
+int ensure_workspace(fc_ctx* c, int R, int hcap) {
+  const int d = c->dim;
+  const int64_t field = (int64_t)d * c->N;
+  if (R > c->Rcap) {
+    for (double* q : {c->x, c->r, c->p[0], c->p[1], c->Ap}) cudaFree(q);
+    cudaFree(c->W1);
+    cudaFree(c->W2);
+    cudaFree(c->st);
+    c->x = c->r = c->p[0] = c->p[1] = c->Ap = nullptr;
+    c->W1 = c->W2 = nullptr;
+    c->st = nullptr;
+    c->Rcap = 0;
+    const size_t fb = sizeof(double) * field * R;
+    CK(cudaMalloc(&c->x, fb));
+    CK(cudaMalloc(&c->r, fb));
+    CK(cudaMalloc(&c->p[0], fb));
+    CK(cudaMalloc(&c->p[1], fb));
+    CK(cudaMalloc(&c->Ap, fb));
+    if (d >= 2) {
+      int64_t spec = (int64_t)R * d * c->N / c->n[d - 1] * ((c->n[d - 1] + 1) / 2);
+      CK(cudaMalloc(&c->W2, sizeof(double2) * spec));
+      if (d == 3) CK(cudaMalloc(&c->W1, sizeof(double2) * spec));
+    }
+    CK(cudaMalloc(&c->st, sizeof(RhsState) * R));
+    c->Rcap = R;
+  }
+  // partial-sum slots: max over row sweeps, vector tiles, energy chunks
+  int64_t nslot_row = d == 1 ? 1 : (int64_t)c->rg.no * c->rg.ntiles * d;
+  int64_t nslot_vec = (field + kVecTile - 1) / kVecTile;
+  int64_t nslot_en = (c->N + 8191) / 8192;
+  int64_t need = std::max<int64_t>(std::max(std::max(nslot_row, nslot_vec), nslot_en), 64) * FC_MAX_RHS * FC_MAX_RHS;
+  if (need > c->part_cap) {
+    cudaFree(c->part);
+    c->part = nullptr;
+    CK(cudaMalloc(&c->part, sizeof(double) * need));
+    c->part_cap = need;
+  }
+  if (hcap > c->hcap) {  // history rows: FC_MAX_RHS rows of hcap entries
+    cudaFree(c->hist);
+    c->hist = nullptr;
+    CK(cudaMalloc(&c->hist, sizeof(double) * (int64_t)hcap * FC_MAX_RHS));
+    c->hcap = hcap;
+  }
+  return FC_OK;
+}
+
+int64_t nslot_row(const fc_ctx* c) { return c->dim == 1 ? 1 : (int64_t)c->rg.no * c->rg.ntiles * c->dim; }
+int64_t nslot_vec(const fc_ctx* c) { return ((int64_t)c->dim * c->N + kVecTile - 1) / kVecTile; }
+
+// One operator application over R fields: first sweep (InArgs) ... last sweep (EpArgs).
+int run_operator(fc_ctx* c, int R, const InArgs& ia, EpArgs ea, int orth, const double M[3][3], const RhsState* st) {
+  const Geo g = c->geo();
+  const Coef C = c->coef();
+  const int d = c->dim;
+  cudaStream_t s = c->stream;
+  if (ea.part != nullptr) ea.nslot = (int)nslot_row(c);
+  if (d == 1) {
+    const FftPlan pl = c->plan(c->n[0]);
+    const size_t sm = c->smem_line;
+    return launch(c, "line", [&] { k_line<<<R, kThreads, sm, s>>>(g, C, ia, ea, st, pl, orth, M[0][0]); });
+  }
+  const RowGeo rg = c->rg;
+  const FftPlan pl_last = c->plan(rg.nl);
+  const int64_t nrow_blocks = (int64_t)R * rg.no * rg.ntiles * d;
+  double2* Wrow = d == 3 ? c->W1 : c->W2;
+  TRY(launch(c, "row_fwd", [&] {
+    k_row_fwd<<<(unsigned)nrow_blocks, kThreads, c->smem_row, s>>>(g, rg, C, ia, st, pl_last, Wrow);
+  }));
+  const MidGeo mg = c->mg;
+  const int64_t nmid = (int64_t)R * d * mg.h2 * mg.nib;
+  if (d == 3) {
+    const FftPlan pl1 = c->plan(c->n[1]);
+    TRY(launch(c, "mid_fwd", [&] {
+      k_mid<false><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, st, pl1, c->W1, c->W2);
+    }));
+  }
+  OuterGeo og = c->og;
+  og.orth = orth;
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) og.M[a][b] = M[a][b];
+  const FftPlan pl0 = c->plan(c->n[0]);
+  TRY(launch(c, "outer", [&] {
+    k_outer<<<(unsigned)(R * og.nqb), kThreads, c->smem_outer, s>>>(g, og, st, pl0, c->W2);
+  }));
+  if (d == 3) {
+    const FftPlan pl1 = c->plan(c->n[1]);
+    TRY(launch(c, "mid_inv", [&] {
+      k_mid<true><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, st, pl1, c->W2, c->W1);
+    }));
+  }
+  return launch(c, "row_inv", [&] {
+    k_row_inv<<<(unsigned)nrow_blocks, kThreads, c->smem_row, s>>>(g, rg, ea, st, pl_last, Wrow);
+  });
+}
+
+int check_ctx(fc_ctx* c, bool need_coef) {
+  if (c == nullptr) return set_err(FC_EINVAL, "null context");
+  if (need_coef && c->A == nullptr) return set_err(FC_EINVAL, "coefficients not set");
+  CK(cudaSetDevice(c->device));
+  return FC_OK;
+}
+
+int check_R(int R) {
+  if (R < 1 || R > FC_MAX_RHS) return set_err(FC_EINVAL, "number of right-hand sides must lie in [1, %d], got %d", FC_MAX_RHS, R);
+  return FC_OK;
+}
+
+const double kIdentity[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+
+int upload_fields(fc_ctx* c, double* dst, const double* host, int R) {
+  CK(cudaMemcpyAsync(dst, host, sizeof(double) * (size_t)R * c->dim * c->N, cudaMemcpyHostToDevice, c->stream));
+  return FC_OK;
+}
+int download_fields(fc_ctx* c, double* host, const double* src, int R) {
+  CK(cudaMemcpyAsync(host, src, sizeof(double) * (size_t)R * c->dim * c->N, cudaMemcpyDeviceToHost, c->stream));
+  return FC_OK;
+}
+
+int sync(fc_ctx* c) {
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->prof_on) drain_profile(c);
+  return FC_OK;
+}
+
+FinArgs fin_args(fc_ctx* c, int R, int nslot, double tol, int max_iter) {
+  FinArgs f{};
+  f.R = R;
+  f.nslot = nslot;
+  f.part = c->part;
+  f.st = c->st;
+  f.hist = c->hist;
+  f.hcap = c->hcap;
+  f.tol = tol;
+  f.max_iter = max_iter;
+  f.invN = 1.0 / (double)c->N;
+  f.any_active = c->any_active;
+  return f;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+extern "C" {
+
+int32_t fc_version(void) { return 1; }
+const char* fc_last_error(void) { return g_err.c_str(); }
+
+int32_t fc_device_count(int32_t* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return set_err(FC_ECUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  *count = n;
+  return FC_OK;
+}
+
+int32_t fc_create(fc_ctx** out, int32_t dim, const int64_t* shape, const double* half_periods, int32_t device) {
+  if (out == nullptr) return set_err(FC_EINVAL, "null output pointer");
+  *out = nullptr;
+  if (dim < 1 || dim > 3) return set_err(FC_ENOTSUP, "dimension %d not supported (1..3)", dim);
+  for (int a = 0; a < dim; ++a) {
+    if (shape[a] <= 0 || shape[a] % 2 == 0)
+      return set_err(FC_EINVAL, "grid shape must consist of positive odd integers");
+    if (!(half_periods[a] > 0)) return set_err(FC_EINVAL, "half_periods must be positive");
+    if (shape[a] > (1 << 20)) return set_err(FC_ENOTSUP, "axis length %lld too large", (long long)shape[a]);
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return set_err(FC_ECUDA, "no CUDA device available");
+  if (device < 0 || device >= ndev) return set_err(FC_EINVAL, "device %d out of range (have %d)", device, ndev);
+  fc_ctx* c = new fc_ctx();
+  c->device = device;
+  c->dim = dim;
+  c->N = 1;
+  for (int a = 0; a < dim; ++a) {
+    c->n[a] = (int)shape[a];
+    c->Y[a] = half_periods[a];
+    c->N *= shape[a];
+  }
+  auto fail = [&](int rc) { fc_destroy(c); return rc; };
+  if (cudaSetDevice(device) != cudaSuccess) return fail(set_err(FC_ECUDA, "cudaSetDevice(%d) failed", device));
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10) return fail(set_err(FC_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor));
+  c->smem_optin = (int)prop.sharedMemPerBlockOptin;
+  c->num_sms = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(set_err(FC_ECUDA, "stream creation failed"));
+  for (int a = 0; a < dim; ++a) {
+    int rc = ensure_plan(c, c->n[a]);
+    if (rc) return fail(rc);
+  }
+  // per-axis frequency tables xi = k / Y (grid.py:131-146)
+  std::vector<double> xi;
+  for (int a = 0; a < dim; ++a) {
+    c->xi_off[a] = (int)xi.size();
+    for (int i = 0; i < c->n[a]; ++i) {
+      long long k = i <= (c->n[a] - 1) / 2 ? i : (long long)i - c->n[a];
+      xi.push_back((double)k / c->Y[a]);
+    }
+  }
+  if (cudaMalloc(&c->xi, sizeof(double) * xi.size()) != cudaSuccess) return fail(set_err(FC_ENOMEM, "xi alloc"));
+  cudaMemcpy(c->xi, xi.data(), sizeof(double) * xi.size(), cudaMemcpyHostToDevice);
+  int rc = choose_tiles(c);
+  if (rc) return fail(rc);
+  const int mx = c->smem_optin;
+  if ((rc = allow_smem(k_row_fwd, mx)) || (rc = allow_smem(k_row_inv, mx)) || (rc = allow_smem(k_mid<false>, mx)) ||
+      (rc = allow_smem(k_mid<true>, mx)) || (rc = allow_smem(k_outer, mx)) || (rc = allow_smem(k_line, mx)))
+    return fail(rc);
+  if (cudaMalloc(&c->any_active, sizeof(int)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "flag alloc"));
+  if (cudaMallocHost(&c->h_flag, 4 * sizeof(int)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "pinned alloc"));
+  for (auto& e : c->flag_ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (cudaMalloc(&c->d_mat, sizeof(double) * FC_MAX_RHS * FC_MAX_RHS) != cudaSuccess)
+    return fail(set_err(FC_ENOMEM, "matrix alloc"));
+  *out = c;
+  return FC_OK;
+}
+
+void fc_destroy(fc_ctx* c) {
+  if (c == nullptr) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->plans) cudaFree(kv.second.roots);
+  for (double* q : {c->xi, c->A, c->x, c->r, c->p[0], c->p[1], c->Ap, c->part, c->hist, c->d_mat}) cudaFree(q);
+  cudaFree(c->W1);
+  cudaFree(c->W2);
+  cudaFree(c->st);
+  cudaFree(c->any_active);
+  if (c->h_flag) cudaFreeHost(c->h_flag);
+  for (auto& e : c->flag_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& pe : c->pending) {
+    cudaEventDestroy(pe.second.first);
+    cudaEventDestroy(pe.second.second);
+  }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int32_t fc_set_coefficients(fc_ctx* c, int32_t kind, const double* host, int64_t count) {
+  TRY(check_ctx(c, false));
+  const int d = c->dim;
+  const int64_t nsym = (int64_t)d * (d + 1) / 2;
+  int64_t expect = kind == FC_COEF_ISOTROPIC ? c->N : (kind == FC_COEF_PACKED ? nsym * c->N : -1);
+  if (expect < 0) return set_err(FC_EINVAL, "unknown coefficient kind %d", kind);
+  if (count != expect) return set_err(FC_EINVAL, "coefficient count %lld != expected %lld", (long long)count, (long long)expect);
+  if (c->A == nullptr || c->A_count != count) {
+    cudaFree(c->A);
+    c->A = nullptr;
+    CK(cudaMalloc(&c->A, sizeof(double) * count));
+    c->A_count = count;
+  }
+  CK(cudaMemcpyAsync(c->A, host, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
+  c->coef_kind = kind;
+  return sync(c);
+}
+
+int32_t fc_apply_A(fc_ctx* c, const double* u, double* out, int32_t nf) {
+  TRY(check_ctx(c, true));
+  TRY(check_R(nf));
+  TRY(ensure_workspace(c, nf, 2));
+  TRY(upload_fields(c, c->p[0], u, nf));
+  const Geo g = c->geo();
+  const Coef C = c->coef();
+  dim3 grid((unsigned)std::min<int64_t>((c->N + kThreads - 1) / kThreads, 148 * 16), nf);
+  TRY(launch(c, "apply_A", [&] { k_apply_A<<<grid, kThreads, 0, c->stream>>>(g, C, c->p[0], c->Ap); }));
+  TRY(download_fields(c, out, c->Ap, nf));
+  return sync(c);
+}
+
+int32_t fc_project(fc_ctx* c, int32_t which, const double* ref, const double* u, double* out, int32_t nf) {
+  TRY(check_ctx(c, false));
+  TRY(check_R(nf));
+  if (which != FC_PROJ_ORTHOGONAL && which != FC_PROJ_GAMMA_REF) return set_err(FC_EINVAL, "unknown projector %d", which);
+  if (which == FC_PROJ_GAMMA_REF && ref == nullptr) return set_err(FC_EINVAL, "gamma_ref needs a reference matrix");
+  TRY(ensure_workspace(c, nf, 2));
+  TRY(upload_fields(c, c->p[0], u, nf));
+  InArgs ia{};
+  ia.mode = IN_RAW;
+  ia.s = 1.0;
+  ia.u = c->p[0];
+  EpArgs ea{};
+  ea.mode = EP_STORE;
+  ea.out = c->Ap;
+  double M[3][3] = {};
+  if (which == FC_PROJ_GAMMA_REF)
+    for (int a = 0; a < c->dim; ++a)
+      for (int b = 0; b < c->dim; ++b) M[a][b] = ref[a * c->dim + b];
+  TRY(run_operator(c, nf, ia, ea, which == FC_PROJ_ORTHOGONAL, which == FC_PROJ_ORTHOGONAL ? kIdentity : M, nullptr));
+  TRY(download_fields(c, out, c->Ap, nf));
+  return sync(c);
+}
+
+int32_t fc_apply_system(fc_ctx* c, const double* u, double* out, int32_t nf) {
+  TRY(check_ctx(c, true));
+  TRY(check_R(nf));
+  TRY(ensure_workspace(c, nf, 2));
+  TRY(upload_fields(c, c->p[0], u, nf));
+  InArgs ia{};
+  ia.mode = IN_FIELD;
+  ia.s = 1.0;
+  ia.u = c->p[0];
+  EpArgs ea{};
+  ea.mode = EP_STORE;
+  ea.out = c->Ap;
+  TRY(run_operator(c, nf, ia, ea, 1, kIdentity, nullptr));
+  TRY(download_fields(c, out, c->Ap, nf));
+  return sync(c);
+}
+
+int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t max_iter, double lam,
+                    const double* init, double* x_out, fc_report* rep, double* hist, double* iterates,
+                    int64_t iterates_cap, int64_t* n_iterates) {
+  TRY(check_ctx(c, true));
+  TRY(check_R(R));
+  if (!(tol > 0 && tol < 1)) return set_err(FC_EINVAL, "tol must lie in (0, 1), got %g", tol);
+  if (max_iter < 1) return set_err(FC_EINVAL, "max_iter must be positive");
+  const int d = c->dim;
+  TRY(ensure_workspace(c, R, max_iter + 1));
+  cudaStream_t s = c->stream;
+  const int64_t fieldR = (int64_t)d * c->N * R;
+  const double sc = lam > 0 ? lam : 1.0;
+  const int orth = lam > 0 ? 0 : 1;
+  double M[3][3] = {};
+  for (int a = 0; a < d; ++a) M[a][a] = sc;
+  CK(cudaMemsetAsync(c->st, 0, sizeof(RhsState) * R, s));
+  CK(cudaMemsetAsync(c->x, 0, sizeof(double) * fieldR, s));
+  const int nrow = (int)nslot_row(c);
+  const int nvec = (int)nslot_vec(c);
+  if (init != nullptr) {
+    // x = G init (solver.py:185)
+    TRY(upload_fields(c, c->p[0], init, R));
+    InArgs ia{};
+    ia.mode = IN_RAW;
+    ia.s = 1.0;
+    ia.u = c->p[0];
+    EpArgs ea{};
+    ea.mode = EP_STORE;
+    ea.out = c->x;
+    TRY(run_operator(c, R, ia, ea, 1, kIdentity, nullptr));
+  }
+  // rhs = -op(E_N) (solver.py:176-178)
+  {
+    InArgs ia{};
+    ia.mode = IN_CONST;
+    ia.s = sc;
+    for (int r = 0; r < R; ++r)
+      for (int a = 0; a < d; ++a) ia.E[r][a] = E[r * d + a];
+    EpArgs ea{};
+    ea.mode = EP_RHS;
+    ea.out = init != nullptr ? c->Ap : c->r;
+    ea.part = c->part;
+    TRY(run_operator(c, R, ia, ea, orth, M, nullptr));
+    FinArgs f = fin_args(c, R, nrow, tol, max_iter);
+    TRY(launch(c, "fin_init", [&] { k_fin_init<<<1, kThreads, 0, s>>>(f, 0, init != nullptr); }));
+  }
+  if (init != nullptr) {
+    // r = rhs - op(x) (solver.py:186)
+    InArgs ia{};
+    ia.mode = IN_FIELD;
+    ia.s = sc;
+    ia.u = c->x;
+    EpArgs ea{};
+    ea.mode = EP_STORE;
+    ea.out = c->p[0];
+    TRY(run_operator(c, R, ia, ea, orth, M, nullptr));
+    dim3 grid(nvec, R);
+    TRY(launch(c, "sub_dot", [&] { k_sub_dot<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->Ap, c->p[0], c->r, c->part, nvec); }));
+    FinArgs f = fin_args(c, R, nvec, tol, max_iter);
+    TRY(launch(c, "fin_init", [&] { k_fin_init<<<1, kThreads, 0, s>>>(f, 1, 1); }));
+  }
+  std::vector<RhsState> hs(R);
+  CK(cudaMemcpyAsync(hs.data(), c->st, sizeof(RhsState) * R, cudaMemcpyDeviceToHost, s));
+  TRY(sync(c));
+  bool any = false;
+  for (auto& q : hs) any |= q.active != 0;
+  int64_t nit = 0;
+  if (iterates != nullptr && iterates_cap > 0) {
+    TRY(download_fields(c, iterates, c->x, R));
+    nit = 1;
+  }
+  const bool record = iterates != nullptr;
+  for (int it = 0; any && it < max_iter; ++it) {
+    double* pcur = c->p[it & 1];
+    double* pold = c->p[(it + 1) & 1];
+    InArgs ia{};
+    ia.mode = IN_PNEW;
+    ia.s = sc;
+    ia.u = c->r;
+    ia.p_old = pold;
+    ia.p_new = pcur;
+    EpArgs ea{};
+    ea.mode = EP_AP;
+    ea.out = c->Ap;
+    ea.p = pcur;
+    ea.part = c->part;
+    TRY(run_operator(c, R, ia, ea, orth, M, c->st));
+    FinArgs fa = fin_args(c, R, nrow, tol, max_iter);
+    TRY(launch(c, "fin_alpha", [&] { k_fin_alpha<<<1, kThreads, 0, s>>>(fa); }));
+    dim3 grid(nvec, R);
+    TRY(launch(c, "cg_update", [&] {
+      k_cg_update<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->st, c->x, c->r, pcur, c->Ap, c->part, nvec);
+    }));
+    FinArgs fb = fin_args(c, R, nvec, tol, max_iter);
+    TRY(launch(c, "fin_beta", [&] { k_fin_beta<<<1, kThreads, 0, s>>>(fb); }));
+    const int slot = it & 3;
+    CK(cudaMemcpyAsync(c->h_flag + slot, c->any_active, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(c->flag_ev[slot], s));
+    if (record) {
+      TRY(sync(c));
+      if (nit < iterates_cap) {
+        TRY(download_fields(c, iterates + nit * (int64_t)R * d * c->N, c->x, R));
+        TRY(sync(c));
+        ++nit;
+      }
+      any = c->h_flag[slot] != 0;
+    } else if (it >= 1) {
+      const int prev = (it - 1) & 3;
+      CK(cudaEventSynchronize(c->flag_ev[prev]));
+      if (c->h_flag[prev] == 0) any = false;
+    }
+  }
+  TRY(sync(c));
+  CK(cudaMemcpy(hs.data(), c->st, sizeof(RhsState) * R, cudaMemcpyDeviceToHost));
+  const int hc = c->hcap;
+  for (int r = 0; r < R; ++r) {
+    rep[r].iterations = hs[r].iterations;
+    rep[r].converged = hs[r].converged;
+    rep[r].status = hs[r].status;
+    rep[r].hist_len = hs[r].hist_len;
+    rep[r].detail = hs[r].detail;
+    if (hist != nullptr)
+      CK(cudaMemcpy(hist + (int64_t)r * (max_iter + 1), c->hist + (int64_t)r * hc, sizeof(double) * hs[r].hist_len,
+                    cudaMemcpyDeviceToHost));
+  }
+  if (n_iterates) *n_iterates = nit;
+  if (x_out != nullptr) {
+    TRY(download_fields(c, x_out, c->x, R));
+    TRY(sync(c));
+  }
+  return FC_OK;
+}
+
+int32_t fc_solve_fixed_point(fc_ctx* c, int32_t R, const double* E, double tol, int32_t max_iter,
+                             const double* ref, const double* scale, double* x_out, fc_report* rep, double* hist) {
+  TRY(check_ctx(c, true));
+  TRY(check_R(R));
+  if (!(tol > 0 && tol < 1)) return set_err(FC_EINVAL, "tol must lie in (0, 1), got %g", tol);
+  if (max_iter < 1) return set_err(FC_EINVAL, "max_iter must be positive");
+  if (ref == nullptr || scale == nullptr) return set_err(FC_EINVAL, "reference matrix and scales are required");
+  const int d = c->dim;
+  TRY(ensure_workspace(c, R, max_iter + 1));
+  cudaStream_t s = c->stream;
+  std::vector<RhsState> hs(R);
+  for (int r = 0; r < R; ++r) {
+    std::memset(&hs[r], 0, sizeof(RhsState));
+    hs[r].active = 1;
+    hs[r].scale = scale[r];
+  }
+  CK(cudaMemcpyAsync(c->st, hs.data(), sizeof(RhsState) * R, cudaMemcpyHostToDevice, s));
+  Loads L{};
+  for (int r = 0; r < R; ++r)
+    for (int a = 0; a < d; ++a) L.E[r][a] = E[r * d + a];
+  const int64_t len = (int64_t)d * c->N;
+  dim3 fgrid((unsigned)std::min<int64_t>((len + kThreads - 1) / kThreads, 148 * 16), R);
+  TRY(launch(c, "fill_loads", [&] { k_fill_loads<<<fgrid, kThreads, 0, s>>>(c->N, d, L, nullptr, c->x); }));
+  double M[3][3] = {};
+  InArgs ia{};
+  ia.mode = IN_FP;
+  ia.s = 1.0;
+  ia.u = c->x;
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) {
+      M[a][b] = ref[a * d + b];
+      ia.A0[a][b] = ref[a * d + b];
+    }
+  EpArgs ea{};
+  ea.mode = EP_FP;
+  ea.out = c->x;
+  ea.part = c->part;
+  for (int r = 0; r < R; ++r)
+    for (int a = 0; a < d; ++a) ea.E[r][a] = E[r * d + a];
+  const int nrow = (int)nslot_row(c);
+  bool any = true;
+  for (int it = 0; any && it < max_iter; ++it) {
+    TRY(run_operator(c, R, ia, ea, 0, M, c->st));
+    FinArgs f = fin_args(c, R, nrow, tol, max_iter);
+    TRY(launch(c, "fin_fp", [&] { k_fin_fp<<<1, kThreads, 0, s>>>(f, 10); }));
+    const int slot = it & 3;
+    CK(cudaMemcpyAsync(c->h_flag + slot, c->any_active, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(c->flag_ev[slot], s));
+    if (it >= 1) {
+      const int prev = (it - 1) & 3;
+      CK(cudaEventSynchronize(c->flag_ev[prev]));
+      if (c->h_flag[prev] == 0) any = false;
+    }
+  }
+  // solution = e - E_N in place (solver.py:293-294)
+  TRY(launch(c, "fill_loads", [&] { k_fill_loads<<<fgrid, kThreads, 0, s>>>(c->N, d, L, c->x, c->x); }));
+  TRY(sync(c));
+  CK(cudaMemcpy(hs.data(), c->st, sizeof(RhsState) * R, cudaMemcpyDeviceToHost));
+  const int hc = c->hcap;
+  for (int r = 0; r < R; ++r) {
+    rep[r].iterations = hs[r].iterations;
+    rep[r].converged = hs[r].converged;
+    rep[r].status = hs[r].status;
+    rep[r].hist_len = hs[r].hist_len;
+    rep[r].detail = 0.0;
+    if (hist != nullptr && hs[r].hist_len > 0)
+      CK(cudaMemcpy(hist + (int64_t)r * max_iter, c->hist + (int64_t)r * hc, sizeof(double) * hs[r].hist_len,
+                    cudaMemcpyDeviceToHost));
+  }
+  if (x_out != nullptr) {
+    TRY(download_fields(c, x_out, c->x, R));
+    TRY(sync(c));
+  }
+  return FC_OK;
+}
+
+int32_t fc_energy(fc_ctx* c, int32_t R, const double* E, const double* x, double* out) {
+  TRY(check_ctx(c, true));
+  TRY(check_R(R));
+  if (c->Rcap < R || c->x == nullptr) {
+    if (x == nullptr) return set_err(FC_EINVAL, "no resident solution for %d right-hand sides", R);
+    TRY(ensure_workspace(c, R, 2));
+  }
+  if (x != nullptr) TRY(upload_fields(c, c->x, x, R));
+  const Geo g = c->geo();
+  const Coef C = c->coef();
+  Loads L{};
+  for (int r = 0; r < R; ++r)
+    for (int a = 0; a < c->dim; ++a) L.E[r][a] = E[r * c->dim + a];
+  const int64_t chunk = 8192;
+  const int nblk = (int)((c->N + chunk - 1) / chunk);
+  if ((int64_t)nblk * R * R > c->part_cap) return set_err(FC_ENOTSUP, "partial buffer too small");
+  TRY(launch(c, "energy", [&] { k_energy<<<nblk, kThreads, 0, c->stream>>>(g, C, L, R, c->x, c->part, chunk); }));
+  TRY(launch(c, "fin_matrix", [&] { k_fin_matrix<<<1, kThreads, 0, c->stream>>>(c->part, nblk, R * R, 1.0 / (double)c->N, c->d_mat); }));
+  CK(cudaMemcpyAsync(out, c->d_mat, sizeof(double) * R * R, cudaMemcpyDeviceToHost, c->stream));
+  return sync(c);
+}
+
+int32_t fc_set_profiling(fc_ctx* c, int32_t on) {
+  if (c == nullptr) return set_err(FC_EINVAL, "null context");
+  if (!on && c->prof_on) {
+    cudaStreamSynchronize(c->stream);
+    drain_profile(c);
+  }
+  c->prof_on = on != 0;
+  return FC_OK;
+}
+int32_t fc_profile_count(fc_ctx* c) { return c ? (int32_t)c->prof.size() : 0; }
+int32_t fc_profile_get(fc_ctx* c, int32_t i, char* name, int32_t cap, int64_t* launches, double* ms) {
+  if (c == nullptr || i < 0 || i >= (int)c->prof.size()) return set_err(FC_EINVAL, "bad profile index");
+  std::snprintf(name, cap, "%s", c->prof[i].name.c_str());
+  *launches = c->prof[i].launches;
+  *ms = c->prof[i].ms;
+  return FC_OK;
+}
+int32_t fc_profile_reset(fc_ctx* c) {
+  if (c == nullptr) return set_err(FC_EINVAL, "null context");
+  cudaStreamSynchronize(c->stream);
+  drain_profile(c);
+  c->prof.clear();
+  c->prof_idx.clear();
+  return FC_OK;
+}
+int64_t fc_launch_count(fc_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

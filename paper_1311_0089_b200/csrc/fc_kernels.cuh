@@ -1,0 +1,716 @@
+// Sweep, vector and reduction kernels of the GaNi operator / CG / fixed point.
+//
+// Operator application (reference solver.py:112-122,173-174,265-267):
+//   y = M(x) u  (pointwise, M = s*A for CG, A - A0 for the fixed point)
+//   -> forward FFT over all axes -> per-mode xi (xi . v) / den, 0 at k = 0
+//   -> inverse FFT (1/|N|) -> epilogue.
+// It is executed as 2d-1 sweeps over HBM (d = 2: 3 sweeps, d = 3: 5 sweeps):
+//   row-forward  : pointwise M(x) u fused with a real->half-complex FFT of the
+//                  contiguous axis (two real rows per complex FFT), written
+//                  transposed so the next axis becomes contiguous;
+//   mid-forward  : (d = 3) C2C along axis 1, written transposed (axis 0 contiguous);
+//   outer        : C2C along axis 0, Gamma_hat multiply, inverse C2C, in place;
+//   mid-inverse  : (d = 3) inverse of mid-forward;
+//   row-inverse  : half-complex->real FFT of the contiguous axis fused with the
+//                  CG / fixed-point epilogue and per-CTA dot partials.
+// Spectral layouts (R right-hand sides, c = d components, h = (n_last+1)/2):
+//   d = 3: W1[R][c][n0][h2][n1], W2[R][c][h2][n1][n0]
+//   d = 2: W2[R][c][h1][n0]
+// Dots are reduced deterministically: per-CTA partials in fixed slots (fixed
+// intra-block tree), summed in fixed order by a single-CTA finalize kernel.
+#pragma once
+#include "fc_fft.cuh"
+
+namespace fc {
+
+constexpr int kThreads = 256;
+constexpr int kMaxDim = 3;
+
+// Input modes of the first sweep.
+enum InMode : int {
+  IN_FIELD = 0,   // y = s * A u
+  IN_PNEW = 1,    // p' = r (first) | r + beta p ; store p'; y = s * A p'
+  IN_CONST = 2,   // y = s * A E          (rhs = -op(E_N), E_N never materialised)
+  IN_FP = 3,      // y = (A - A0) e
+  IN_RAW = 4,     // y = s * u            (bare projector)
+};
+// Epilogues of the last sweep (g = inverse transform / |N| at the voxel).
+enum EpMode : int {
+  EP_STORE = 0,   // out = g
+  EP_RHS = 1,     // out = -g ; partial sum out^2
+  EP_AP = 2,      // out = g ; partial sum p g
+  EP_FP = 3,      // e' = E - g ; partial sum (e' - e)^2 ; e = e'
+};
+
+struct RhsState {
+  double rr, r0, pAp, alpha, beta, prev_update, scale, detail;
+  int active, iterations, converged, status, growth, first, has_prev, hist_len;
+};
+enum Status : int { ST_OK = 0, ST_MAXITER = 1, ST_BREAKDOWN = 2, ST_DIVERGENT = 3 };
+
+struct Geo {
+  int dim;
+  int n[3];       // shape (n[1], n[2] unused below dim)
+  int64_t N;      // voxels
+  double invN;
+  const double* xi[3];  // xi[a][slot] = k(slot) / Y_a
+};
+
+struct Coef {
+  const double* A;   // iso: (N) ; packed: (nsym, N)
+  int kind;          // 0 isotropic scalar, 1 packed symmetric
+};
+
+struct InArgs {
+  int mode;
+  double s;                   // CG reference scale lambda (1 otherwise)
+  const double* u;            // IN_FIELD / IN_RAW source, IN_FP e, IN_PNEW r
+  const double* p_old;        // IN_PNEW
+  double* p_new;              // IN_PNEW
+  double E[8][kMaxDim];       // per-RHS loads (IN_CONST / IN_FP uses A0 below)
+  double A0[kMaxDim][kMaxDim];
+};
+
+struct EpArgs {
+  int mode;
+  double* out;                // EP_STORE/EP_RHS/EP_AP destination, EP_FP: e (in place)
+  const double* p;            // EP_AP
+  double E[8][kMaxDim];       // EP_FP
+  double* part;               // partial sums [R][nslot]
+  int nslot;
+};
+
+__device__ __forceinline__ int pidx(int d, int a, int b) {
+  if (a == b) return a;
+  if (a > b) { int t = a; a = b; b = t; }
+  // (0,1),(0,2),(1,2) after the d diagonal entries (material.py:30-34)
+  return d + (a == 0 ? b - 1 : (d - 1) + (b - 2));
+}
+
+__device__ __forceinline__ double coef(const Coef& C, int d, int a, int b, int64_t v, int64_t N) {
+  if (C.kind == 0) return a == b ? C.A[v] : 0.0;
+  return C.A[(int64_t)pidx(d, a, b) * N + v];
+}
+
+__device__ __forceinline__ bool rhs_active(const RhsState* st, int r) {
+  return st == nullptr || st[r].active;
+}
+
+// Value of component a of the first-sweep input at voxel v of RHS r.
+__device__ __forceinline__ double in_value(const InArgs& ia, const Geo& g, const Coef& C,
+                                           const RhsState* st, int r, int a, int64_t v) {
+  const int d = g.dim;
+  const int64_t N = g.N;
+  const int64_t base = (int64_t)r * d * N;
+  switch (ia.mode) {
+    case IN_RAW:
+      return ia.s == 1.0 ? ia.u[base + a * N + v] : __dmul_rn(ia.s, ia.u[base + a * N + v]);
+    case IN_FIELD:
+    case IN_CONST: {
+      double acc = 0.0;
+      if (C.kind == 0) {
+        double u = ia.mode == IN_CONST ? ia.E[r][a] : ia.u[base + a * N + v];
+        acc = __dmul_rn(C.A[v], u);
+      } else {
+        for (int b = 0; b < d; ++b) {
+          double u = ia.mode == IN_CONST ? ia.E[r][b] : ia.u[base + b * N + v];
+          acc = __dadd_rn(acc, __dmul_rn(coef(C, d, a, b, v, N), u));
+        }
+      }
+      return ia.s == 1.0 ? acc : __dmul_rn(ia.s, acc);
+    }
+    case IN_PNEW: {
+      const bool first = st[r].first;
+      const double beta = st[r].beta;
+      double acc = 0.0;
+      for (int b = 0; b < d; ++b) {
+        if (C.kind == 0 && b != a) continue;
+        const int64_t e = base + b * N + v;
+        double pn = first ? ia.u[e] : __dadd_rn(ia.u[e], __dmul_rn(beta, ia.p_old[e]));
+        if (b == a) ia.p_new[e] = pn;
+        acc = __dadd_rn(acc, __dmul_rn(coef(C, d, a, b, v, N), pn));
+      }
+      return ia.s == 1.0 ? acc : __dmul_rn(ia.s, acc);
+    }
+    default: {  // IN_FP: contrast = A - A0 (solver.py:253-255)
+      double acc = 0.0;
+      for (int b = 0; b < d; ++b) {
+        double cab = __dsub_rn(coef(C, d, a, b, v, N), ia.A0[a][b]);
+        acc = __dadd_rn(acc, __dmul_rn(cab, ia.u[base + b * N + v]));
+      }
+      return acc;
+    }
+  }
+}
+
+// Epilogue at voxel v; returns the contribution to the CTA's partial sum.
+__device__ __forceinline__ double ep_apply(const EpArgs& ea, int d, int64_t N, int r, int a, int64_t v,
+                                           double gval) {
+  const int64_t e = (int64_t)r * d * N + a * N + v;
+  switch (ea.mode) {
+    case EP_STORE: ea.out[e] = gval; return 0.0;
+    case EP_RHS: { double o = -gval; ea.out[e] = o; return __dmul_rn(o, o); }
+    case EP_AP: ea.out[e] = gval; return __dmul_rn(ea.p[e], gval);
+    default: {
+      double en = __dsub_rn(ea.E[r][a], gval);
+      double df = __dsub_rn(en, ea.out[e]);
+      ea.out[e] = en;
+      return __dmul_rn(df, df);
+    }
+  }
+}
+
+// Deterministic block sum (fixed shuffle tree + fixed cross-warp order).
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int i = 0; i < nw; ++i) s += red[i];
+  }
+  return s;  // valid in thread 0
+}
+
+// Row-sweep geometry: rows of length nl along the contiguous axis, grouped in
+// blocks of B consecutive rows of the previous axis (length np), for each
+// outer index o < no (d = 3: o = i0; d = 2: no = 1).
+struct RowGeo {
+  int nl, hl, np, no, B, ntiles;
+};
+
+// ---------------------------------------------------------------------------
+// First sweep: pointwise M(x) u, R2C along the contiguous axis, transposed store.
+__global__ void __launch_bounds__(kThreads) k_row_fwd(Geo g, RowGeo rg, Coef C, InArgs ia, const RhsState* st,
+                                                       FftPlan pl, double2* __restrict__ W) {
+  extern __shared__ double2 sm[];
+  const int c = g.dim;
+  int64_t bid = blockIdx.x;
+  const int a = bid % c; bid /= c;
+  const int tile = bid % rg.ntiles; bid /= rg.ntiles;
+  const int o = bid % rg.no;
+  const int r = (int)(bid / rg.no);
+  if (!rhs_active(st, r)) return;
+  const int row0 = tile * rg.B;
+  const int nrows = min(rg.B, rg.np - row0);
+  const int npairs = (nrows + 1) >> 1;
+  const int ld = rg.nl;
+  double2* buf0 = sm;
+  double2* buf1 = sm + (size_t)npairs * ld;
+  // load: two real rows per complex pencil
+  for (int idx = threadIdx.x; idx < npairs * 2 * rg.nl; idx += blockDim.x) {
+    const int row = idx / rg.nl, i = idx - row * rg.nl;
+    double val = 0.0;
+    if (row < nrows) {
+      const int64_t v = ((int64_t)o * rg.np + row0 + row) * rg.nl + i;
+      val = in_value(ia, g, C, st, r, a, v);
+    }
+    double* dst = reinterpret_cast<double*>(buf0 + (size_t)(row >> 1) * ld + i);
+    dst[row & 1] = val;
+  }
+  __syncthreads();
+  double2* res = smem_fft<false>(buf0, buf1, npairs, ld, pl);
+  // separate Z = Ya + i Yb and store Y(k), k < hl, transposed (rows contiguous)
+  double2* Wb = W + ((int64_t)(r * c + a) * rg.no + o) * rg.hl * rg.np + row0;
+  for (int idx = threadIdx.x; idx < rg.hl * nrows; idx += blockDim.x) {
+    const int k = idx / nrows, row = idx - k * nrows;
+    const double2* z = res + (size_t)(row >> 1) * ld;
+    const double2 zk = z[k];
+    const double2 zm = z[k == 0 ? 0 : rg.nl - k];  // conj taken below
+    double2 y;
+    if ((row & 1) == 0) y = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    else y = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+    Wb[(int64_t)k * rg.np + row] = y;
+  }
+}
+
+// Last sweep: transposed load, C2R along the contiguous axis, epilogue.
+__global__ void __launch_bounds__(kThreads) k_row_inv(Geo g, RowGeo rg, EpArgs ea, const RhsState* st,
+                                                       FftPlan pl, const double2* __restrict__ W) {
+  extern __shared__ double2 sm[];
+  __shared__ double red[kThreads / 32];
+  const int c = g.dim;
+  int64_t bid = blockIdx.x;
+  const int a = bid % c; bid /= c;
+  const int tile = bid % rg.ntiles; bid /= rg.ntiles;
+  const int o = bid % rg.no;
+  const int r = (int)(bid / rg.no);
+  if (!rhs_active(st, r)) return;
+  const int row0 = tile * rg.B;
+  const int nrows = min(rg.B, rg.np - row0);
+  const int npairs = (nrows + 1) >> 1;
+  const int ld = rg.nl;
+  double2* buf0 = sm;
+  double2* buf1 = sm + (size_t)npairs * ld;
+  const double2* Wb = W + ((int64_t)(r * c + a) * rg.no + o) * rg.hl * rg.np + row0;
+  // Z(k) = Ye(k) + i Yo(k), Z(n-k) = conj(Ye(k)) + i conj(Yo(k)); k = 0 uses real parts.
+  for (int idx = threadIdx.x; idx < rg.hl * npairs; idx += blockDim.x) {
+    const int k = idx / npairs, pr = idx - k * npairs;
+    const int re = 2 * pr, ro = 2 * pr + 1;
+    double2 ye = Wb[(int64_t)k * rg.np + re];
+    double2 yo = ro < nrows ? Wb[(int64_t)k * rg.np + ro] : make_double2(0.0, 0.0);
+    double2* z = buf0 + (size_t)pr * ld;
+    if (k == 0) {
+      z[0] = make_double2(ye.x, yo.x);
+    } else {
+      z[k] = make_double2(ye.x - yo.y, ye.y + yo.x);
+      z[rg.nl - k] = make_double2(ye.x + yo.y, yo.x - ye.y);
+    }
+  }
+  __syncthreads();
+  double2* res = smem_fft<true>(buf0, buf1, npairs, ld, pl);
+  double acc = 0.0;
+  for (int idx = threadIdx.x; idx < nrows * rg.nl; idx += blockDim.x) {
+    const int row = idx / rg.nl, i = idx - row * rg.nl;
+    const double2 z = res[(size_t)(row >> 1) * ld + i];
+    const double gv = ((row & 1) ? z.y : z.x) * g.invN;
+    const int64_t v = ((int64_t)o * rg.np + row0 + row) * rg.nl + i;
+    acc += ep_apply(ea, c, g.N, r, a, v, gv);
+  }
+  if (ea.part != nullptr) {
+    double s = block_sum(acc, red);
+    if (threadIdx.x == 0) {
+      const int slot = (o * rg.ntiles + tile) * c + a;
+      ea.part[(int64_t)r * ea.nslot + slot] = s;
+    }
+  }
+}
+
+// Middle sweep (d = 3): W1[r][a][i0][k2][i1] <-> W2[r][a][k2][k1][i0].
+struct MidGeo {
+  int n0, n1, h2, B, nib;
+};
+
+template <bool INV>
+__global__ void __launch_bounds__(kThreads) k_mid(Geo g, MidGeo mg, const RhsState* st, FftPlan pl,
+                                                   const double2* __restrict__ src, double2* __restrict__ dst) {
+  extern __shared__ double2 sm[];
+  const int c = g.dim;
+  int64_t bid = blockIdx.x;
+  const int ib = bid % mg.nib; bid /= mg.nib;
+  const int k2 = bid % mg.h2; bid /= mg.h2;
+  const int a = bid % c;
+  const int r = (int)(bid / c);
+  if (!rhs_active(st, r)) return;
+  const int i00 = ib * mg.B;
+  const int nr = min(mg.B, mg.n0 - i00);
+  const int ld = mg.n1;
+  double2* buf0 = sm;
+  double2* buf1 = sm + (size_t)nr * ld;
+  const int64_t rc = (int64_t)(r * c + a);
+  // W1 offset of (i0, k2, i1): ((rc*n0 + i0)*h2 + k2)*n1 + i1
+  // W2 offset of (k2, k1, i0): ((rc*h2 + k2)*n1 + k1)*n0 + i0
+  if (!INV) {
+    for (int idx = threadIdx.x; idx < nr * mg.n1; idx += blockDim.x) {
+      const int row = idx / mg.n1, i1 = idx - row * mg.n1;
+      buf0[(size_t)row * ld + i1] = src[((rc * mg.n0 + i00 + row) * mg.h2 + k2) * mg.n1 + i1];
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < nr * mg.n1; idx += blockDim.x) {
+      const int k1 = idx / nr, row = idx - k1 * nr;
+      buf0[(size_t)row * ld + k1] = src[((rc * mg.h2 + k2) * mg.n1 + k1) * mg.n0 + i00 + row];
+    }
+  }
+  __syncthreads();
+  double2* res = smem_fft<INV>(buf0, buf1, nr, ld, pl);
+  if (!INV) {
+    for (int idx = threadIdx.x; idx < nr * mg.n1; idx += blockDim.x) {
+      const int k1 = idx / nr, row = idx - k1 * nr;
+      dst[((rc * mg.h2 + k2) * mg.n1 + k1) * mg.n0 + i00 + row] = res[(size_t)row * ld + k1];
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < nr * mg.n1; idx += blockDim.x) {
+      const int row = idx / mg.n1, i1 = idx - row * mg.n1;
+      dst[((rc * mg.n0 + i00 + row) * mg.h2 + k2) * mg.n1 + i1] = res[(size_t)row * ld + i1];
+    }
+  }
+}
+
+// Outer sweep: C2C along axis 0, Gamma_hat, inverse, in place on W2.
+// Gamma_hat(k) v = xi (xi . v) / den, den = |xi|^2 (orth) or xi^T M xi; 0 at k = 0
+// (solver.py:98-110, green.py:81-92).
+struct OuterGeo {
+  int n0, Q, QB, nqb;   // Q pencils per component, QB per CTA
+  int n1, h_last;       // d = 3: q = k2 * n1 + k1 ; d = 2: q = k1
+  int orth;
+  double M[kMaxDim][kMaxDim];
+};
+
+__global__ void __launch_bounds__(kThreads) k_outer(Geo g, OuterGeo og, const RhsState* st, FftPlan pl,
+                                                     double2* __restrict__ W) {
+  extern __shared__ double2 sm[];
+  const int c = g.dim;
+  const int qb = blockIdx.x % og.nqb;
+  const int r = blockIdx.x / og.nqb;
+  if (!rhs_active(st, r)) return;
+  const int q0 = qb * og.QB;
+  const int nq = min(og.QB, og.Q - q0);
+  const int P = c * nq;
+  const int ld = og.n0;
+  double2* buf0 = sm;
+  double2* buf1 = sm + (size_t)P * ld;
+  for (int a = 0; a < c; ++a) {
+    const double2* s = W + (((int64_t)(r * c + a)) * og.Q + q0) * og.n0;
+    double2* d = buf0 + (size_t)a * nq * ld;
+    for (int idx = threadIdx.x; idx < nq * og.n0; idx += blockDim.x) d[idx] = s[idx];
+  }
+  __syncthreads();
+  double2* res = smem_fft<false>(buf0, buf1, P, ld, pl);
+  double2* other = res == buf0 ? buf1 : buf0;
+  for (int idx = threadIdx.x; idx < nq * og.n0; idx += blockDim.x) {
+    const int qq = idx / og.n0, i0 = idx - qq * og.n0;
+    const int q = q0 + qq;
+    double xi[kMaxDim];
+    xi[0] = g.xi[0][i0];
+    bool zero_mode = (i0 == 0);
+    if (c == 2) {
+      xi[1] = g.xi[1][q];
+      zero_mode = zero_mode && q == 0;
+    } else if (c == 3) {
+      const int k2 = q / og.n1, k1 = q - k2 * og.n1;
+      xi[1] = g.xi[1][k1];
+      xi[2] = g.xi[2][k2];
+      zero_mode = zero_mode && q == 0;
+    }
+    double2 v[kMaxDim];
+    for (int a = 0; a < c; ++a) v[a] = res[((size_t)a * nq + qq) * ld + i0];
+    double2 out[kMaxDim];
+    if (zero_mode) {
+      for (int a = 0; a < c; ++a) out[a] = make_double2(0.0, 0.0);
+    } else {
+      double2 dots = make_double2(0.0, 0.0);
+      double den = 0.0;
+      for (int a = 0; a < c; ++a) {
+        dots.x += xi[a] * v[a].x;
+        dots.y += xi[a] * v[a].y;
+      }
+      if (og.orth) {
+        for (int a = 0; a < c; ++a) den += xi[a] * xi[a];
+      } else {
+        for (int a = 0; a < c; ++a)
+          for (int b = 0; b < c; ++b) den += xi[a] * og.M[a][b] * xi[b];
+      }
+      const double2 qv = make_double2(dots.x / den, dots.y / den);
+      for (int a = 0; a < c; ++a) out[a] = make_double2(xi[a] * qv.x, xi[a] * qv.y);
+    }
+    for (int a = 0; a < c; ++a) other[((size_t)a * nq + qq) * ld + i0] = out[a];
+  }
+  __syncthreads();
+  double2* res2 = smem_fft<true>(other, res, P, ld, pl);
+  for (int a = 0; a < c; ++a) {
+    double2* d = W + (((int64_t)(r * c + a)) * og.Q + q0) * og.n0;
+    const double2* s = res2 + (size_t)a * nq * ld;
+    for (int idx = threadIdx.x; idx < nq * og.n0; idx += blockDim.x) d[idx] = s[idx];
+  }
+}
+
+// d = 1: the whole line in one CTA per RHS (full complex FFT, no pairing).
+__global__ void __launch_bounds__(kThreads) k_line(Geo g, Coef C, InArgs ia, EpArgs ea, const RhsState* st,
+                                                    FftPlan pl, int orth, double M00) {
+  extern __shared__ double2 sm[];
+  __shared__ double red[kThreads / 32];
+  const int r = blockIdx.x;
+  if (!rhs_active(st, r)) return;
+  const int n = g.n[0];
+  double2* buf0 = sm;
+  double2* buf1 = sm + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) buf0[i] = make_double2(in_value(ia, g, C, st, r, 0, i), 0.0);
+  __syncthreads();
+  double2* res = smem_fft<false>(buf0, buf1, 1, n, pl);
+  double2* other = res == buf0 ? buf1 : buf0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (i == 0) { other[0] = make_double2(0.0, 0.0); continue; }
+    const double xi = g.xi[0][i];
+    const double den = orth ? xi * xi : xi * M00 * xi;
+    const double2 v = res[i];
+    const double2 qv = make_double2((xi * v.x) / den, (xi * v.y) / den);
+    other[i] = make_double2(xi * qv.x, xi * qv.y);
+  }
+  __syncthreads();
+  double2* res2 = smem_fft<true>(other, res, 1, n, pl);
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += ep_apply(ea, 1, g.N, r, 0, i, res2[i].x * g.invN);
+  if (ea.part != nullptr) {
+    double s = block_sum(acc, red);
+    if (threadIdx.x == 0) ea.part[(int64_t)r * ea.nslot] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Elementwise kernels over one RHS block of c*N values; fixed tiling so the
+// partial-sum slots do not depend on scheduling.
+constexpr int kVecTile = kThreads * 16;
+
+// x += alpha p ; r -= alpha Ap ; partial <r, r>     (solver.py:213-216)
+__global__ void __launch_bounds__(kThreads) k_cg_update(int64_t len, RhsState* st, double* x, double* rr,
+                                                        const double* p, const double* Ap, double* part, int nslot) {
+  __shared__ double red[kThreads / 32];
+  const int r = blockIdx.y;
+  if (!st[r].active) return;
+  const double alpha = st[r].alpha;
+  const int64_t base = (int64_t)r * len;
+  const int64_t t0 = (int64_t)blockIdx.x * kVecTile;
+  const int64_t t1 = min(len, t0 + kVecTile);
+  double acc = 0.0;
+  for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+    const int64_t e = base + i;
+    x[e] = __dadd_rn(x[e], __dmul_rn(alpha, p[e]));
+    const double rn = __dsub_rn(rr[e], __dmul_rn(alpha, Ap[e]));
+    rr[e] = rn;
+    acc += __dmul_rn(rn, rn);
+  }
+  double s = block_sum(acc, red);
+  if (threadIdx.x == 0) part[(int64_t)r * nslot + blockIdx.x] = s;
+}
+
+// out = a - b ; partial <out, out>      (r = rhs - op(x), solver.py:186)
+__global__ void __launch_bounds__(kThreads) k_sub_dot(int64_t len, const double* a, const double* b, double* out,
+                                                      double* part, int nslot) {
+  __shared__ double red[kThreads / 32];
+  const int r = blockIdx.y;
+  const int64_t base = (int64_t)r * len;
+  const int64_t t0 = (int64_t)blockIdx.x * kVecTile;
+  const int64_t t1 = min(len, t0 + kVecTile);
+  double acc = 0.0;
+  for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+    const double o = __dsub_rn(a[base + i], b[base + i]);
+    out[base + i] = o;
+    acc += __dmul_rn(o, o);
+  }
+  double s = block_sum(acc, red);
+  if (threadIdx.x == 0) part[(int64_t)r * nslot + blockIdx.x] = s;
+}
+
+// out[r][a][v] = E[r][a] (x == NULL) or x[r][a][v] - E[r][a]   (e = E_N ; solution = e - E_N)
+struct Loads { double E[8][kMaxDim]; };
+__global__ void k_fill_loads(int64_t N, int d, Loads L, const double* x, double* out) {
+  const int r = blockIdx.y;
+  const int64_t len = (int64_t)d * N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(i / N);
+    const int64_t e = (int64_t)r * len + i;
+    out[e] = x == nullptr ? L.E[r][a] : __dsub_rn(x[e], L.E[r][a]);
+  }
+}
+
+// out = A u pointwise (material.py:182-187)
+__global__ void k_apply_A(Geo g, Coef C, const double* u, double* out) {
+  const int r = blockIdx.y;
+  const int d = g.dim;
+  const int64_t base = (int64_t)r * d * g.N;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < g.N; v += (int64_t)gridDim.x * blockDim.x) {
+    for (int a = 0; a < d; ++a) {
+      double acc = 0.0;
+      for (int b = 0; b < d; ++b) acc = __dadd_rn(acc, __dmul_rn(coef(C, d, a, b, v, g.N), u[base + b * g.N + v]));
+      out[base + a * g.N + v] = acc;
+    }
+  }
+}
+
+// Energy / effective-tensor partials: M[al][be] = sum_v sum_a (A t_al)_a (t_be)_a,
+// t_al = E_al + x_al  (homogenize.py:59-67).  One slot per CTA, R*R values.
+constexpr int kMaxRhs = 8;
+__global__ void __launch_bounds__(kThreads) k_energy(Geo g, Coef C, Loads L, int R, const double* x, double* part,
+                                                     int64_t chunk) {
+  __shared__ double red[kThreads / 32];
+  const int d = g.dim;
+  const int64_t v0 = (int64_t)blockIdx.x * chunk;
+  const int64_t v1 = min(g.N, v0 + chunk);
+  double acc[kMaxRhs * kMaxRhs];
+  for (int i = 0; i < R * R; ++i) acc[i] = 0.0;
+  for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+    double t[kMaxRhs][kMaxDim];
+    double f[kMaxRhs][kMaxDim];
+    for (int al = 0; al < R; ++al)
+      for (int a = 0; a < d; ++a) t[al][a] = __dadd_rn(x[((int64_t)al * d + a) * g.N + v], L.E[al][a]);
+    for (int al = 0; al < R; ++al)
+      for (int a = 0; a < d; ++a) {
+        double s = 0.0;
+        for (int b = 0; b < d; ++b) s = __dadd_rn(s, __dmul_rn(coef(C, d, a, b, v, g.N), t[al][b]));
+        f[al][a] = s;
+      }
+    for (int al = 0; al < R; ++al)
+      for (int be = 0; be < R; ++be) {
+        double s = 0.0;
+        for (int a = 0; a < d; ++a) s = __dadd_rn(s, __dmul_rn(f[al][a], t[be][a]));
+        acc[al * R + be] += s;
+      }
+  }
+  for (int i = 0; i < R * R; ++i) {
+    double s = block_sum(acc[i], red);
+    if (threadIdx.x == 0) part[(int64_t)i * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Finalize kernels: one CTA, RHS handled in turn; partials summed in a fixed order.
+__device__ double reduce_slots(const double* part, int n, double* red) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += part[i];
+  return block_sum(acc, red);  // thread 0
+}
+
+struct FinArgs {
+  int R;
+  int nslot;
+  const double* part;
+  RhsState* st;
+  double* hist;       // [R][hcap]
+  int hcap;
+  double tol;
+  int max_iter;
+  double invN;
+  int* any_active;
+};
+
+// After rhs = -op(E) (and optionally r = rhs - op(x)): r0, rr, history[0], early exit
+// (solver.py:176-194).  stage 0: rhs norm only ; stage 1: r norm (+ early exit).
+__global__ void k_fin_init(FinArgs f, int stage, int with_init) {
+  __shared__ double red[kThreads / 32];
+  for (int r = 0; r < f.R; ++r) {
+    double s = reduce_slots(f.part + (int64_t)r * f.nslot, f.nslot, red);
+    if (threadIdx.x == 0) {
+      RhsState& S = f.st[r];
+      const double q = s * f.invN;  // float(np.sum(x*y) / total)
+      if (stage == 0) {
+        S.r0 = sqrt(q);
+        S.rr = q;
+      }
+      if (stage == 1 || !with_init) {
+        if (stage == 1) S.rr = q;
+        const double h0 = sqrt(S.rr);
+        f.hist[(int64_t)r * f.hcap] = h0;
+        S.hist_len = 1;
+        S.iterations = 0;
+        S.first = 1;
+        S.status = ST_OK;
+        S.beta = 0.0;
+        if (S.r0 == 0.0 || h0 <= f.tol * S.r0) {
+          S.active = 0;
+          S.converged = 1;
+        } else {
+          S.active = 1;
+          S.converged = 0;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// pAp, breakdown, alpha (solver.py:202-213)
+__global__ void k_fin_alpha(FinArgs f) {
+  __shared__ double red[kThreads / 32];
+  for (int r = 0; r < f.R; ++r) {
+    if (!f.st[r].active) continue;
+    double s = reduce_slots(f.part + (int64_t)r * f.nslot, f.nslot, red);
+    if (threadIdx.x == 0) {
+      RhsState& S = f.st[r];
+      const double pAp = s * f.invN;
+      S.pAp = pAp;
+      if (pAp <= 0.0) {
+        S.active = 0;
+        S.converged = 0;
+        S.status = ST_BREAKDOWN;
+        S.detail = pAp;
+      } else {
+        S.alpha = S.rr / pAp;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// rr_new, history, stop test, beta (solver.py:216-225)
+__global__ void k_fin_beta(FinArgs f) {
+  __shared__ double red[kThreads / 32];
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  for (int r = 0; r < f.R; ++r) {
+    if (!f.st[r].active) continue;
+    double s = reduce_slots(f.part + (int64_t)r * f.nslot, f.nslot, red);
+    if (threadIdx.x == 0) {
+      RhsState& S = f.st[r];
+      const double rr_new = s * f.invN;
+      S.iterations += 1;
+      const double h = sqrt(rr_new);
+      f.hist[(int64_t)r * f.hcap + S.iterations] = h;
+      S.hist_len = S.iterations + 1;
+      if (h <= f.tol * S.r0) {
+        S.converged = 1;
+        S.active = 0;
+      } else {
+        S.beta = rr_new / S.rr;
+        S.rr = rr_new;
+        S.first = 0;
+        if (S.iterations >= f.max_iter) {
+          S.active = 0;
+          S.status = ST_MAXITER;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int r = 0; r < f.R; ++r) a |= f.st[r].active;
+    *f.any_active = a;
+  }
+}
+
+// Fixed point: update norm, history, stop, growth streak (solver.py:264-291)
+__global__ void k_fin_fp(FinArgs f, int window) {
+  __shared__ double red[kThreads / 32];
+  for (int r = 0; r < f.R; ++r) {
+    if (!f.st[r].active) continue;
+    double s = reduce_slots(f.part + (int64_t)r * f.nslot, f.nslot, red);
+    if (threadIdx.x == 0) {
+      RhsState& S = f.st[r];
+      const double update = sqrt(s * f.invN);
+      f.hist[(int64_t)r * f.hcap + S.iterations] = update;
+      S.iterations += 1;
+      S.hist_len = S.iterations;
+      if (update <= f.tol * S.scale) {
+        S.converged = 1;
+        S.active = 0;
+      } else {
+        if (S.has_prev && update > S.prev_update) {
+          S.growth += 1;
+          if (S.growth >= window) {
+            S.active = 0;
+            S.status = ST_DIVERGENT;
+          }
+        } else {
+          S.growth = 0;
+        }
+        S.prev_update = update;
+        S.has_prev = 1;
+        if (S.active && S.iterations >= f.max_iter) {
+          S.active = 0;
+          S.status = ST_MAXITER;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int r = 0; r < f.R; ++r) a |= f.st[r].active;
+    *f.any_active = a;
+  }
+}
+
+// Energy matrix finalize: out[i] = (sum of slots) / N in fixed order.
+__global__ void k_fin_matrix(const double* part, int nslot, int nval, double invN, double* out) {
+  __shared__ double red[kThreads / 32];
+  for (int i = 0; i < nval; ++i) {
+    double s = reduce_slots(part + (int64_t)i * nslot, nslot, red);
+    if (threadIdx.x == 0) out[i] = s * invN;
+    __syncthreads();
+  }
+}
+
+}  // namespace fc
