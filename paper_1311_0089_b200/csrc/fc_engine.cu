@@ -219,13 +219,15 @@ int ensure_plan(fc_ctx* c, int L) {
 
 template <typename K>
 int allow_smem(K kernel, int bytes) {
-  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kernel));
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes - (int)fa.sharedSizeBytes));
   return FC_OK;
 }
 
 // Tile selection: smem per CTA <= soft cap (two CTAs per SM) if possible, else opt-in max.
 int choose_tiles(fc_ctx* c) {
-  const size_t soft = 100 * 1024, hard = (size_t)c->smem_optin;
+  const size_t soft = 100 * 1024, hard = (size_t)c->smem_optin - 1024;
   const int d = c->dim;
   if (d == 1) {
     c->smem_line = (size_t)32 * c->n[0];

@@ -77,3 +77,14 @@ def curl_residual(values, Y):
 def rel_l2(a, b):
     nb = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+def log_parity(rec):
+    """Append a parity record (margins vs gates) to $PARITY_LOG when set."""
+    import json
+    import os
+
+    path = os.environ.get("PARITY_LOG")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(json.dumps(rec) + "\n")

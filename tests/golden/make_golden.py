@@ -52,6 +52,39 @@ def sample_idx(n):
     return np.sort(np.random.default_rng(SAMPLE_SEED).choice(n, size=min(NSAMPLE, n), replace=False))
 
 
+class perturbed_fft:
+    """Run the reference with scipy's pocketfft over REVERSED axis order: the same
+    mathematics with different rounding.  The difference to the unperturbed run is
+    the reference's own reproducibility floor, recorded as ``<prefix>floor``."""
+
+    def __enter__(self):
+        import scipy.fft as sf
+
+        self.saved = np.fft.fftn, np.fft.ifftn
+        np.fft.fftn = lambda a, axes=None: sf.fftn(a, axes=None if axes is None else axes[::-1])
+        np.fft.ifftn = lambda a, axes=None: sf.ifftn(a, axes=None if axes is None else axes[::-1])
+
+    def __exit__(self, *exc):
+        np.fft.fftn, np.fft.ifftn = self.saved
+
+
+def with_floor(prefix, run, full=True):
+    """report_dict of run() plus the perturbed-rounding floor (rel. L2 and history)."""
+    rep = run()
+    out = report_dict(prefix, rep, full)
+    with perturbed_fft():
+        alt = run()
+    ref = rep.solution.values
+    nrm = np.linalg.norm(ref)
+    out[f"{prefix}floor"] = float(np.linalg.norm(alt.solution.values - ref) / nrm) if nrm > 0 else 0.0
+    h, ha = np.array(rep.residual_history), np.array(alt.residual_history)
+    m = min(len(h), len(ha))
+    out[f"{prefix}floor_hist"] = (float(np.max(np.abs(h[:m] - ha[:m]) / np.maximum(h[:m], h[0])))
+                                  if m and h[0] > 0 else 0.0)
+    out[f"{prefix}floor_iterations"] = alt.iterations
+    return out
+
+
 def report_dict(prefix, rep, full=True):
     sol = rep.solution.values
     out = {
@@ -93,13 +126,13 @@ def small():
     a = ref_field(gen.cfg1_square_inclusion())
     load = LoadCase((1.0, 0.0))
     kw = {}
-    kw.update(report_dict("cg_", solve_cg(a, load, SolverConfig(tol=1e-8, max_iter=1000))))
+    kw.update(with_floor("cg_", lambda: solve_cg(a, load, SolverConfig(tol=1e-8, max_iter=1000))))
     mean = float(a.components[0].mean())
     kw["fp_mean_lambda"] = mean
-    kw.update(report_dict("fpmean_", solve_neumann(
+    kw.update(with_floor("fpmean_", lambda: solve_neumann(
         a, load, SolverConfig(method="neumann", tol=1e-8, max_iter=1000,
                               reference=ReferenceTensor.scalar(mean, 2)))))
-    kw.update(report_dict("fpdef_", solve_neumann(
+    kw.update(with_floor("fpdef_", lambda: solve_neumann(
         a, load, SolverConfig(method="neumann", tol=1e-8, max_iter=1000))))
     kw["AH"] = effective_tensor(a, SolverConfig(tol=1e-8, max_iter=1000)).matrix
     save("cfg1", **kw)
@@ -109,17 +142,17 @@ def small():
     a = fam.sample(fam.default_spec((255,)))
     eff = effective_tensor(a, SolverConfig(tol=1e-10, max_iter=500))
     kw = {"packed": a.components, "AH": eff.matrix}
-    kw.update(report_dict("cg_", eff.per_case_reports[0]))
-    kw.update(report_dict("fp_", solve_neumann(a, LoadCase((1.0,)),
-                                               SolverConfig(method="neumann", tol=1e-8, max_iter=5000))))
+    kw.update(with_floor("cg_", lambda: solve_cg(a, LoadCase((1.0,)), SolverConfig(tol=1e-10, max_iter=500))))
+    kw.update(with_floor("fp_", lambda: solve_neumann(a, LoadCase((1.0,)),
+                                                      SolverConfig(method="neumann", tol=1e-8, max_iter=5000))))
     save("sine255", **kw)
 
     # Checkerboard 27^2 (1, 50): scalar-reference independence.
     a = rfam.checkerboard_2d(1.0, 50.0).sample(GridSpec((1.0, 1.0), (27, 27)))
     kw = {"packed": a.components}
-    kw.update(report_dict("none_", solve_cg(a, LoadCase((1.0, 0.0)), SolverConfig(tol=1e-8, max_iter=500))))
+    kw.update(with_floor("none_", lambda: solve_cg(a, LoadCase((1.0, 0.0)), SolverConfig(tol=1e-8, max_iter=500))))
     for lam in (0.5, 10.0):
-        kw.update(report_dict(f"lam{lam:g}_", solve_cg(
+        kw.update(with_floor(f"lam{lam:g}_", lambda: solve_cg(
             a, LoadCase((1.0, 0.0)),
             SolverConfig(tol=1e-8, max_iter=500, reference=ReferenceTensor.scalar(lam, 2)))))
     save("checker27", **kw)
@@ -132,12 +165,11 @@ def small():
     for i, (Y, shape, E) in enumerate(cases):
         spec = GridSpec(Y, shape)
         a = CoefficientField(spec, random_spd_packed(shape, rng))
-        rep = solve_cg(a, LoadCase(E), SolverConfig(tol=1e-13, max_iter=2000))
         kw[f"c{i}_Y"] = np.array(Y)
         kw[f"c{i}_shape"] = np.array(shape)
         kw[f"c{i}_E"] = np.array(E)
         kw[f"c{i}_packed"] = a.components
-        kw.update(report_dict(f"c{i}_", rep))
+        kw.update(with_floor(f"c{i}_", lambda: solve_cg(a, LoadCase(E), SolverConfig(tol=1e-13, max_iter=2000))))
         kw[f"c{i}_dense"] = dense_oracle(a, LoadCase(E)).values
     save("dense_small", **kw)
 
@@ -171,9 +203,9 @@ def small():
     # cfg3 generator at 27^3: CG 1e-8 (+A_H), fixed point 1e-6 default reference.
     a = ref_field(gen.cfg3_sphere(27))
     kw = {}
-    kw.update(report_dict("cg_", solve_cg(a, LoadCase((1.0, 0.0, 0.0)), SolverConfig(tol=1e-8, max_iter=1000))))
-    kw.update(report_dict("fp_", solve_neumann(a, LoadCase((1.0, 0.0, 0.0)),
-                                               SolverConfig(method="neumann", tol=1e-6, max_iter=5000))))
+    kw.update(with_floor("cg_", lambda: solve_cg(a, LoadCase((1.0, 0.0, 0.0)), SolverConfig(tol=1e-8, max_iter=1000))))
+    kw.update(with_floor("fp_", lambda: solve_neumann(a, LoadCase((1.0, 0.0, 0.0)),
+                                                      SolverConfig(method="neumann", tol=1e-6, max_iter=5000))))
     kw["AH"] = effective_tensor(a, SolverConfig(tol=1e-8, max_iter=1000)).matrix
     save("sphere27", **kw)
 
@@ -183,7 +215,7 @@ def small():
                                 np.moveaxis(packed[gen.voronoi_labels(27, seeds)], -1, 0).copy())
     a = ref_field(ours)
     kw = {"packed": a.components}
-    kw.update(report_dict("cg_", solve_cg(a, LoadCase((1.0, 0.0, 0.0)), SolverConfig(tol=1e-8, max_iter=2000))))
+    kw.update(with_floor("cg_", lambda: solve_cg(a, LoadCase((1.0, 0.0, 0.0)), SolverConfig(tol=1e-8, max_iter=2000))))
     eff = effective_tensor(a, SolverConfig(tol=1e-8, max_iter=2000))
     kw["AH"] = eff.matrix
     save("poly27", **kw)
@@ -192,8 +224,8 @@ def small():
     a = ref_field(gen.cfg2_random_two_phase(81))
     kw = {}
     for j, E in enumerate(gen.CFG2_LOADS):
+        kw.update(with_floor(f"l{j}_", lambda: solve_cg(a, LoadCase(E), SolverConfig(tol=1e-8, max_iter=2000))))
         rep = solve_cg(a, LoadCase(E), SolverConfig(tol=1e-8, max_iter=2000))
-        kw.update(report_dict(f"l{j}_", rep))
         kw[f"l{j}_energy"] = energy(a, LoadCase(E), rep)
     save("cfg2_81", **kw)
 
@@ -202,8 +234,8 @@ def small():
     spec = GridSpec((1.0, 1.5, 0.75), (11, 21, 65))
     a = CoefficientField(spec, random_spd_packed(spec.shape, rng))
     kw = {"packed": a.components, "Y": np.array(spec.half_periods), "shape": np.array(spec.shape)}
-    kw.update(report_dict("cg_", solve_cg(a, LoadCase((0.3, -1.0, 0.5)), SolverConfig(tol=1e-9, max_iter=2000))))
-    kw.update(report_dict("fp_", solve_neumann(
+    kw.update(with_floor("cg_", lambda: solve_cg(a, LoadCase((0.3, -1.0, 0.5)), SolverConfig(tol=1e-9, max_iter=2000))))
+    kw.update(with_floor("fp_", lambda: solve_neumann(
         a, LoadCase((0.3, -1.0, 0.5)),
         SolverConfig(method="neumann", tol=1e-7, max_iter=5000,
                      reference=ReferenceTensor(np.diag([3.0, 2.0, 2.5]))))))

