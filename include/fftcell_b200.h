@@ -115,6 +115,9 @@ int32_t fc_profile_count(fc_ctx* ctx);
 int32_t fc_profile_get(fc_ctx* ctx, int32_t i, char* name, int32_t name_cap, int64_t* launches, double* total_ms);
 int32_t fc_profile_reset(fc_ctx* ctx);
 int64_t fc_launch_count(fc_ctx* ctx);
+/* CUDA-event timers on the context's stream: mark slot (0..7); elapsed between two marks (syncs on b). */
+int32_t fc_timer_mark(fc_ctx* ctx, int32_t slot);
+int32_t fc_timer_elapsed(fc_ctx* ctx, int32_t a, int32_t b, double* ms);
 
 #ifdef __cplusplus
 }

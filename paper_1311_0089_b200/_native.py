@@ -60,6 +60,8 @@ SIGNATURES = [
      [ctypes.c_void_p, ctypes.c_int32, ctypes.c_char_p, ctypes.c_int32, _i64p, _dp]),
     ("fc_profile_reset", ctypes.c_int32, [ctypes.c_void_p]),
     ("fc_launch_count", ctypes.c_int64, [ctypes.c_void_p]),
+    ("fc_timer_mark", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32]),
+    ("fc_timer_elapsed", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, _dp]),
 ]
 
 
@@ -165,11 +167,16 @@ class Context:
         return self._batched(lib().fc_project, u, which, _ptr(ref))
 
     # -- solvers -----------------------------------------------------------
-    def solve_cg(self, E, tol, max_iter, lam=None, init=None, want_x=True, record_iterates=False):
+    def solve_cg(self, E, tol, max_iter, lam=None, init=None, want_x=True, record_iterates=False, out=None):
         E = _c64(np.atleast_2d(E))
         R = E.shape[0]
         fshape = (R, self.d) + self.shape
-        x = np.empty(fshape) if want_x else None
+        if out is not None:
+            if out.shape != fshape or out.dtype != np.float64 or not out.flags.c_contiguous:
+                raise ValueError(f"out must be a C-contiguous float64 array of shape {fshape}")
+            x = out
+        else:
+            x = np.empty(fshape) if want_x else None
         init = None if init is None else _c64(init).reshape(fshape)
         reps = (Report * R)()
         hist = np.zeros((R, max_iter + 1))
@@ -233,6 +240,14 @@ class Context:
 
     def launch_count(self):
         return int(lib().fc_launch_count(self._h))
+
+    def timer_mark(self, slot):
+        _check(lib().fc_timer_mark(self._h, slot))
+
+    def timer_elapsed(self, a, b):
+        ms = ctypes.c_double()
+        _check(lib().fc_timer_elapsed(self._h, a, b, ctypes.byref(ms)))
+        return float(ms.value)
 
 
 _spec_contexts: dict = {}

@@ -114,6 +114,7 @@ struct fc_ctx {
   int* h_flag = nullptr;  // pinned, 4 slots
   cudaEvent_t flag_ev[4] = {};
   double* d_mat = nullptr;
+  cudaEvent_t timer_ev[8] = {};
 
   // tiling
   RowGeo rg{};
@@ -527,6 +528,8 @@ void fc_destroy(fc_ctx* c) {
     cudaEventDestroy(pe.second.second);
   }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (auto& e : c->timer_ev)
+    if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -859,5 +862,24 @@ int32_t fc_profile_reset(fc_ctx* c) {
   return FC_OK;
 }
 int64_t fc_launch_count(fc_ctx* c) { return c ? c->launches : 0; }
+
+int32_t fc_timer_mark(fc_ctx* c, int32_t slot) {
+  TRY(check_ctx(c, false));
+  if (slot < 0 || slot >= 8) return set_err(FC_EINVAL, "timer slot %d out of range", slot);
+  if (!c->timer_ev[slot]) CK(cudaEventCreate(&c->timer_ev[slot]));
+  CK(cudaEventRecord(c->timer_ev[slot], c->stream));
+  return FC_OK;
+}
+
+int32_t fc_timer_elapsed(fc_ctx* c, int32_t a, int32_t b, double* ms) {
+  TRY(check_ctx(c, false));
+  if (a < 0 || a >= 8 || b < 0 || b >= 8 || !c->timer_ev[a] || !c->timer_ev[b])
+    return set_err(FC_EINVAL, "timer slots not recorded");
+  CK(cudaEventSynchronize(c->timer_ev[b]));
+  float f = 0.f;
+  CK(cudaEventElapsedTime(&f, c->timer_ev[a], c->timer_ev[b]));
+  *ms = f;
+  return FC_OK;
+}
 
 }  // extern "C"
