@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -19,6 +20,7 @@
 
 #include "../../include/fftcell_b200.h"
 #include "fc_kernels.cuh"
+#include "fc_kernels_reg.cuh"
 
 using namespace fc;
 
@@ -53,7 +55,29 @@ int set_err(int code, const char* fmt, ...) {
 struct DevPlan {
   FftPlan plan{};
   double2* roots = nullptr;
+  double2* rtw = nullptr;  // register-FFT twiddle table (L = 3^k only)
 };
+
+bool is_pow3_reg(int L) { return L == 9 || L == 27 || L == 81 || L == 243 || L == 729 || L == 2187; }
+
+// Twiddle table of fc_fft_reg.cuh for L = 3^k: for radix-9 pass S >= 1 (Ns = 9^S)
+// tw[off9(S) + (r-1) Ns + k] = w_L^{k r L/(9 Ns)}, r = 1..8, k < Ns; tail block
+// tw[offT + (r-1) L/3 + b] = w_L^{b r}, r = 1, 2, b < L/3.
+std::vector<double2> reg_twiddles(int L, const std::vector<double2>& roots) {
+  int K = 0;
+  for (int t = L; t > 1; t /= 3) ++K;
+  const int NP9 = K / 2;
+  const bool tail = K % 2;
+  std::vector<double2> tw;
+  for (int S = 1, Ns = 9; S < NP9; ++S, Ns *= 9)
+    for (int r = 1; r < 9; ++r)
+      for (int k = 0; k < Ns; ++k) tw.push_back(roots[(int64_t)k * r * (L / (9 * Ns)) % L]);
+  if (tail)
+    for (int r = 1; r < 3; ++r)
+      for (int b = 0; b < L / 3; ++b) tw.push_back(roots[(int64_t)b * r % L]);
+  if (tw.empty()) tw.push_back(make_double2(1.0, 0.0));
+  return tw;
+}
 
 // Factor plan for an odd length: radix-9 passes first, then 3, 5, other primes.
 bool make_factors(int L, FftPlan& p) {
@@ -92,6 +116,7 @@ struct fc_ctx {
   cudaStream_t stream = nullptr;
   int smem_optin = 0;
   int num_sms = 0;
+  bool force_generic = false;  // FC_FORCE_GENERIC=1: generic smem FFT for every axis
 
   std::map<int, DevPlan> plans;  // by length
   double* xi = nullptr;          // concatenated per-axis frequency tables
@@ -111,6 +136,7 @@ struct fc_ctx {
   RhsState* st = nullptr;
   double* hist = nullptr;
   int* any_active = nullptr;
+  unsigned* counter = nullptr;  // last-CTA arrival counter of the fused finalize
   int* h_flag = nullptr;  // pinned, 4 slots
   cudaEvent_t flag_ev[4] = {};
   double* d_mat = nullptr;
@@ -141,6 +167,10 @@ struct fc_ctx {
   }
   Coef coef() const { return Coef{A, coef_kind}; }
   const FftPlan& plan(int L) const { return plans.at(L).plan; }
+  const double2* rtw(int L) const { return plans.at(L).rtw; }
+  // register-path tiling per sweep (0 = generic path)
+  int row_npen = 0, mid_bp = 0, outer_qb = 0;
+  size_t smem_row_r = 0, smem_mid_r = 0, smem_outer_r = 0;
 };
 
 namespace {
@@ -214,6 +244,11 @@ int ensure_plan(fc_ctx* c, int L) {
   CK(cudaMalloc(&dp.roots, sizeof(double2) * L));
   CK(cudaMemcpy(dp.roots, roots.data(), sizeof(double2) * L, cudaMemcpyHostToDevice));
   dp.plan.roots = dp.roots;
+  if (is_pow3_reg(L) && !c->force_generic) {
+    std::vector<double2> tw = reg_twiddles(L, roots);
+    CK(cudaMalloc(&dp.rtw, sizeof(double2) * tw.size()));
+    CK(cudaMemcpy(dp.rtw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
+  }
   c->plans[L] = dp;
   return FC_OK;
 }
@@ -287,7 +322,70 @@ int choose_tiles(fc_ctx* c) {
     og.nqb = (og.Q + best - 1) / best;
     c->smem_outer = (size_t)32 * d * best * og.n0;
   }
+  // register-resident path for power-of-three axes (fc_kernels_reg.cuh)
+  auto env_int = [](const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+  };
+  if (c->force_generic) return FC_OK;
+  if (is_pow3_reg(rg.nl)) {
+    const int TP = rg.nl / 9;
+    int npen = std::max(1, std::min(16, std::min(env_int("FC_ROW_THREADS", 512), kMaxBlock) / TP));
+    npen = std::min(npen, (rg.np + 1) / 2);
+    rg.B = 2 * npen;
+    rg.ntiles = (rg.np + rg.B - 1) / rg.B;
+    c->row_npen = npen;
+    c->smem_row_r = (size_t)16 * npen * (rg.nl + 1);
+  }
+  if (d == 3 && is_pow3_reg(c->n[1])) {
+    MidGeo& mg = c->mg;
+    const int TP = c->n[1] / 9;
+    int bp = std::max(1, std::min(16, std::min(env_int("FC_MID_THREADS", 512), kMaxBlock) / TP));
+    bp = std::min(bp, c->n[0]);
+    mg.B = bp;
+    mg.nib = (mg.n0 + bp - 1) / bp;
+    c->mid_bp = bp;
+    c->smem_mid_r = (size_t)16 * bp * c->n[1];
+  }
+  if (is_pow3_reg(c->n[0])) {
+    OuterGeo& og = c->og;
+    const int TP = c->n[0] / 9;
+    int qb = std::max(1, std::min(32, std::min(env_int("FC_OUTER_THREADS", 256), kMaxBlockOuter) / TP));
+    qb = std::min(qb, og.Q);
+    og.QB = qb;
+    og.nqb = (og.Q + qb - 1) / qb;
+    c->outer_qb = qb;
+    c->smem_outer_r = (size_t)16 * d * qb * c->n[0];
+  }
   return FC_OK;
+}
+
+// ---- compile-time dispatch of the register kernels on the axis length ----------
+#define FC_POW3_SWITCH(L, BODY)         \
+  switch (L) {                           \
+    case 9: { constexpr int LL = 9; BODY; } break;       \
+    case 27: { constexpr int LL = 27; BODY; } break;     \
+    case 81: { constexpr int LL = 81; BODY; } break;     \
+    case 243: { constexpr int LL = 243; BODY; } break;   \
+    case 729: { constexpr int LL = 729; BODY; } break;   \
+    case 2187: { constexpr int LL = 2187; BODY; } break; \
+    default: break;                      \
+  }
+
+int allow_reg_smem(int mx) {
+  int rc = FC_OK;
+  auto al = [&](auto k) { if (rc == FC_OK) rc = allow_smem(k, mx); };
+  for (int L : {9, 27, 81, 243, 729, 2187}) {
+    FC_POW3_SWITCH(L, {
+      al(k_row_fwd_r<LL>);
+      al(k_row_inv_r<LL>);
+      al(k_mid_r<LL, false>);
+      al(k_mid_r<LL, true>);
+      al(k_outer_r<LL, 2>);
+      al(k_outer_r<LL, 3>);
+    });
+  }
+  return rc;
 }
 
 int ensure_workspace(fc_ctx* c, int R, int hcap) {
@@ -352,34 +450,66 @@ int run_operator(fc_ctx* c, int R, const InArgs& ia, EpArgs ea, int orth, const 
     return launch(c, "line", [&] { k_line<<<R, kThreads, sm, s>>>(g, C, ia, ea, st, pl, orth, M[0][0]); });
   }
   const RowGeo rg = c->rg;
-  const FftPlan pl_last = c->plan(rg.nl);
   const int64_t nrow_blocks = (int64_t)R * rg.no * rg.ntiles * d;
   double2* Wrow = d == 3 ? c->W1 : c->W2;
-  TRY(launch(c, "row_fwd", [&] {
-    k_row_fwd<<<(unsigned)nrow_blocks, kThreads, c->smem_row, s>>>(g, rg, C, ia, st, pl_last, Wrow);
-  }));
-  const MidGeo mg = c->mg;
-  const int64_t nmid = (int64_t)R * d * mg.h2 * mg.nib;
-  if (d == 3) {
-    const FftPlan pl1 = c->plan(c->n[1]);
-    TRY(launch(c, "mid_fwd", [&] {
-      k_mid<false><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, st, pl1, c->W1, c->W2);
+  if (c->row_npen) {
+    const int nt = c->row_npen * (rg.nl / 9);
+    const double2* tw = c->rtw(rg.nl);
+    TRY(launch(c, "row_fwd", [&] {
+      FC_POW3_SWITCH(rg.nl, (k_row_fwd_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, C, ia, st, tw, Wrow)));
+    }));
+  } else {
+    const FftPlan pl_last = c->plan(rg.nl);
+    TRY(launch(c, "row_fwd", [&] {
+      k_row_fwd<<<(unsigned)nrow_blocks, kThreads, c->smem_row, s>>>(g, rg, C, ia, st, pl_last, Wrow);
     }));
   }
+  const MidGeo mg = c->mg;
+  const int64_t nmid = (int64_t)R * d * mg.h2 * mg.nib;
+  auto mid = [&](bool inv) -> int {
+    const double2* src = inv ? c->W2 : c->W1;
+    double2* dst = inv ? c->W1 : c->W2;
+    if (c->mid_bp) {
+      const int nt = c->mid_bp * (c->n[1] / 9);
+      const double2* tw = c->rtw(c->n[1]);
+      return launch(c, inv ? "mid_inv" : "mid_fwd", [&] {
+        if (inv) FC_POW3_SWITCH(c->n[1], (k_mid_r<LL, true><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, st, tw, src, dst)))
+        else FC_POW3_SWITCH(c->n[1], (k_mid_r<LL, false><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, st, tw, src, dst)))
+      });
+    }
+    const FftPlan pl1 = c->plan(c->n[1]);
+    return launch(c, inv ? "mid_inv" : "mid_fwd", [&] {
+      if (inv) k_mid<true><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, st, pl1, src, dst);
+      else k_mid<false><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, st, pl1, src, dst);
+    });
+  };
+  if (d == 3) TRY(mid(false));
   OuterGeo og = c->og;
   og.orth = orth;
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b) og.M[a][b] = M[a][b];
-  const FftPlan pl0 = c->plan(c->n[0]);
-  TRY(launch(c, "outer", [&] {
-    k_outer<<<(unsigned)(R * og.nqb), kThreads, c->smem_outer, s>>>(g, og, st, pl0, c->W2);
-  }));
-  if (d == 3) {
-    const FftPlan pl1 = c->plan(c->n[1]);
-    TRY(launch(c, "mid_inv", [&] {
-      k_mid<true><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, st, pl1, c->W2, c->W1);
+  if (c->outer_qb) {
+    const int nt = c->outer_qb * (c->n[0] / 9);
+    const double2* tw = c->rtw(c->n[0]);
+    TRY(launch(c, "outer", [&] {
+      if (d == 2) FC_POW3_SWITCH(c->n[0], (k_outer_r<LL, 2><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, c->W2)))
+      else FC_POW3_SWITCH(c->n[0], (k_outer_r<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, c->W2)))
+    }));
+  } else {
+    const FftPlan pl0 = c->plan(c->n[0]);
+    TRY(launch(c, "outer", [&] {
+      k_outer<<<(unsigned)(R * og.nqb), kThreads, c->smem_outer, s>>>(g, og, st, pl0, c->W2);
     }));
   }
+  if (d == 3) TRY(mid(true));
+  if (c->row_npen) {
+    const int nt = c->row_npen * (rg.nl / 9);
+    const double2* tw = c->rtw(rg.nl);
+    return launch(c, "row_inv", [&] {
+      FC_POW3_SWITCH(rg.nl, (k_row_inv_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, ea, st, tw, Wrow)));
+    });
+  }
+  const FftPlan pl_last = c->plan(rg.nl);
   return launch(c, "row_inv", [&] {
     k_row_inv<<<(unsigned)nrow_blocks, kThreads, c->smem_row, s>>>(g, rg, ea, st, pl_last, Wrow);
   });
@@ -414,8 +544,9 @@ int sync(fc_ctx* c) {
   return FC_OK;
 }
 
-FinArgs fin_args(fc_ctx* c, int R, int nslot, double tol, int max_iter) {
+FinArgs fin_args(fc_ctx* c, int mode, int R, int nslot, double tol, int max_iter, int with_init = 0) {
   FinArgs f{};
+  f.mode = mode;
   f.R = R;
   f.nslot = nslot;
   f.part = c->part;
@@ -424,8 +555,11 @@ FinArgs fin_args(fc_ctx* c, int R, int nslot, double tol, int max_iter) {
   f.hcap = c->hcap;
   f.tol = tol;
   f.max_iter = max_iter;
+  f.window = 10;  // solver.py:27
+  f.with_init = with_init;
   f.invN = 1.0 / (double)c->N;
   f.any_active = c->any_active;
+  f.counter = c->counter;
   return f;
 }
 
@@ -477,6 +611,7 @@ int32_t fc_create(fc_ctx** out, int32_t dim, const int64_t* shape, const double*
   cudaGetDeviceProperties(&prop, device);
   if (prop.major < 10) return fail(set_err(FC_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor));
   c->smem_optin = (int)prop.sharedMemPerBlockOptin;
+  c->force_generic = getenv("FC_FORCE_GENERIC") != nullptr && atoi(getenv("FC_FORCE_GENERIC")) != 0;
   c->num_sms = prop.multiProcessorCount;
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(set_err(FC_ECUDA, "stream creation failed"));
@@ -499,9 +634,12 @@ int32_t fc_create(fc_ctx** out, int32_t dim, const int64_t* shape, const double*
   if (rc) return fail(rc);
   const int mx = c->smem_optin;
   if ((rc = allow_smem(k_row_fwd, mx)) || (rc = allow_smem(k_row_inv, mx)) || (rc = allow_smem(k_mid<false>, mx)) ||
-      (rc = allow_smem(k_mid<true>, mx)) || (rc = allow_smem(k_outer, mx)) || (rc = allow_smem(k_line, mx)))
+      (rc = allow_smem(k_mid<true>, mx)) || (rc = allow_smem(k_outer, mx)) || (rc = allow_smem(k_line, mx)) ||
+      (rc = allow_reg_smem(mx)))
     return fail(rc);
   if (cudaMalloc(&c->any_active, sizeof(int)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "flag alloc"));
+  if (cudaMalloc(&c->counter, sizeof(unsigned)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "counter alloc"));
+  cudaMemset(c->counter, 0, sizeof(unsigned));
   if (cudaMallocHost(&c->h_flag, 4 * sizeof(int)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "pinned alloc"));
   for (auto& e : c->flag_ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   if (cudaMalloc(&c->d_mat, sizeof(double) * FC_MAX_RHS * FC_MAX_RHS) != cudaSuccess)
@@ -514,12 +652,16 @@ void fc_destroy(fc_ctx* c) {
   if (c == nullptr) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (auto& kv : c->plans) cudaFree(kv.second.roots);
+  for (auto& kv : c->plans) {
+    cudaFree(kv.second.roots);
+    cudaFree(kv.second.rtw);
+  }
   for (double* q : {c->xi, c->A, c->x, c->r, c->p[0], c->p[1], c->Ap, c->part, c->hist, c->d_mat}) cudaFree(q);
   cudaFree(c->W1);
   cudaFree(c->W2);
   cudaFree(c->st);
   cudaFree(c->any_active);
+  cudaFree(c->counter);
   if (c->h_flag) cudaFreeHost(c->h_flag);
   for (auto& e : c->flag_ev)
     if (e) cudaEventDestroy(e);
@@ -636,7 +778,7 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
     ea.out = c->x;
     TRY(run_operator(c, R, ia, ea, 1, kIdentity, nullptr));
   }
-  // rhs = -op(E_N) (solver.py:176-178)
+  // rhs = -op(E_N) (solver.py:176-178); the last CTA sets r0 (and history[0])
   {
     InArgs ia{};
     ia.mode = IN_CONST;
@@ -647,9 +789,8 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
     ea.mode = EP_RHS;
     ea.out = init != nullptr ? c->Ap : c->r;
     ea.part = c->part;
+    ea.fin = fin_args(c, FIN_INIT, R, nrow, tol, max_iter, init != nullptr);
     TRY(run_operator(c, R, ia, ea, orth, M, nullptr));
-    FinArgs f = fin_args(c, R, nrow, tol, max_iter);
-    TRY(launch(c, "fin_init", [&] { k_fin_init<<<1, kThreads, 0, s>>>(f, 0, init != nullptr); }));
   }
   if (init != nullptr) {
     // r = rhs - op(x) (solver.py:186)
@@ -662,9 +803,10 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
     ea.out = c->p[0];
     TRY(run_operator(c, R, ia, ea, orth, M, nullptr));
     dim3 grid(nvec, R);
-    TRY(launch(c, "sub_dot", [&] { k_sub_dot<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->Ap, c->p[0], c->r, c->part, nvec); }));
-    FinArgs f = fin_args(c, R, nvec, tol, max_iter);
-    TRY(launch(c, "fin_init", [&] { k_fin_init<<<1, kThreads, 0, s>>>(f, 1, 1); }));
+    FinArgs f = fin_args(c, FIN_INIT2, R, nvec, tol, max_iter);
+    TRY(launch(c, "sub_dot", [&] {
+      k_sub_dot<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->Ap, c->p[0], c->r, c->part, nvec, f);
+    }));
   }
   std::vector<RhsState> hs(R);
   CK(cudaMemcpyAsync(hs.data(), c->st, sizeof(RhsState) * R, cudaMemcpyDeviceToHost, s));
@@ -691,15 +833,13 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
     ea.out = c->Ap;
     ea.p = pcur;
     ea.part = c->part;
+    ea.fin = fin_args(c, FIN_ALPHA, R, nrow, tol, max_iter);
     TRY(run_operator(c, R, ia, ea, orth, M, c->st));
-    FinArgs fa = fin_args(c, R, nrow, tol, max_iter);
-    TRY(launch(c, "fin_alpha", [&] { k_fin_alpha<<<1, kThreads, 0, s>>>(fa); }));
     dim3 grid(nvec, R);
+    FinArgs fb = fin_args(c, FIN_BETA, R, nvec, tol, max_iter);
     TRY(launch(c, "cg_update", [&] {
-      k_cg_update<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->st, c->x, c->r, pcur, c->Ap, c->part, nvec);
+      k_cg_update<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->st, c->x, c->r, pcur, c->Ap, c->part, nvec, fb);
     }));
-    FinArgs fb = fin_args(c, R, nvec, tol, max_iter);
-    TRY(launch(c, "fin_beta", [&] { k_fin_beta<<<1, kThreads, 0, s>>>(fb); }));
     const int slot = it & 3;
     CK(cudaMemcpyAsync(c->h_flag + slot, c->any_active, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaEventRecord(c->flag_ev[slot], s));
@@ -778,11 +918,10 @@ int32_t fc_solve_fixed_point(fc_ctx* c, int32_t R, const double* E, double tol, 
   for (int r = 0; r < R; ++r)
     for (int a = 0; a < d; ++a) ea.E[r][a] = E[r * d + a];
   const int nrow = (int)nslot_row(c);
+  ea.fin = fin_args(c, FIN_FP, R, nrow, tol, max_iter);
   bool any = true;
   for (int it = 0; any && it < max_iter; ++it) {
     TRY(run_operator(c, R, ia, ea, 0, M, c->st));
-    FinArgs f = fin_args(c, R, nrow, tol, max_iter);
-    TRY(launch(c, "fin_fp", [&] { k_fin_fp<<<1, kThreads, 0, s>>>(f, 10); }));
     const int slot = it & 3;
     CK(cudaMemcpyAsync(c->h_flag + slot, c->any_active, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaEventRecord(c->flag_ev[slot], s));

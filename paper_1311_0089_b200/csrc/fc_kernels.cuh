@@ -71,6 +71,33 @@ struct InArgs {
   double A0[kMaxDim][kMaxDim];
 };
 
+// Finalize stages run by the last CTA of a reducing kernel (see finish_block).
+enum FinMode : int {
+  FIN_NONE = 0,
+  FIN_INIT = 1,    // rhs norm: r0 (and history[0] / early exit unless a warm start follows)
+  FIN_INIT2 = 2,   // warm start: r = rhs - op(x) norm, history[0], early exit
+  FIN_ALPHA = 3,   // pAp, breakdown, alpha
+  FIN_BETA = 4,    // rr_new, history, stop test, beta
+  FIN_FP = 5,      // fixed point update norm, history, stop, divergence streak
+};
+
+struct FinArgs {
+  int mode;
+  int R;
+  int nslot;
+  double* part;       // [R][nslot]
+  RhsState* st;
+  double* hist;       // [R][hcap]
+  int hcap;
+  double tol;
+  int max_iter;
+  int window;         // fixed-point divergence window (solver.py:27)
+  int with_init;      // FIN_INIT: a warm start follows
+  double invN;
+  int* any_active;
+  unsigned* counter;  // arrival counter, reset by the last CTA
+};
+
 struct EpArgs {
   int mode;
   double* out;                // EP_STORE/EP_RHS/EP_AP destination, EP_FP: e (in place)
@@ -78,6 +105,7 @@ struct EpArgs {
   double E[8][kMaxDim];       // EP_FP
   double* part;               // partial sums [R][nslot]
   int nslot;
+  FinArgs fin;
 };
 
 __device__ __forceinline__ int pidx(int d, int a, int b) {
@@ -96,63 +124,148 @@ __device__ __forceinline__ bool rhs_active(const RhsState* st, int r) {
   return st == nullptr || st[r].active;
 }
 
-// Value of component a of the first-sweep input at voxel v of RHS r.
-__device__ __forceinline__ double in_value(const InArgs& ia, const Geo& g, const Coef& C,
-                                           const RhsState* st, int r, int a, int64_t v) {
-  const int d = g.dim;
-  const int64_t N = g.N;
-  const int64_t base = (int64_t)r * d * N;
-  switch (ia.mode) {
-    case IN_RAW:
-      return ia.s == 1.0 ? ia.u[base + a * N + v] : __dmul_rn(ia.s, ia.u[base + a * N + v]);
-    case IN_FIELD:
-    case IN_CONST: {
-      double acc = 0.0;
-      if (C.kind == 0) {
-        double u = ia.mode == IN_CONST ? ia.E[r][a] : ia.u[base + a * N + v];
-        acc = __dmul_rn(C.A[v], u);
-      } else {
-        for (int b = 0; b < d; ++b) {
-          double u = ia.mode == IN_CONST ? ia.E[r][b] : ia.u[base + b * N + v];
-          acc = __dadd_rn(acc, __dmul_rn(coef(C, d, a, b, v, N), u));
+// First-sweep input, prepared once per CTA (RHS scalars hoisted out of the
+// voxel loop).  All reads go through the read-only path (__ldg): nothing the
+// first sweep reads is written by it (p' goes to the other p buffer), so the
+// loads of a thread can be issued back to back.
+struct InEval {
+  int mode, d, a;
+  double s, beta;
+  bool first;
+  int64_t N, base;
+  const double* u;
+  const double* p_old;
+  const double* A;
+  int kind;
+  double E0, E1, E2, Ea;  // load of this RHS (scalars: no local-memory arrays)
+  double R0, R1, R2;      // row a of the reference tensor
+  __device__ __forceinline__ static double sel(int b, double x0, double x1, double x2) {
+    return b == 0 ? x0 : (b == 1 ? x1 : x2);
+  }
+
+  __device__ __forceinline__ double coefv(int b, int64_t v) const {
+    if (kind == 0) return a == b ? __ldg(A + v) : 0.0;
+    return __ldg(A + (int64_t)pidx(d, a, b) * N + v);
+  }
+  // value y_a(v); for IN_PNEW also p'_a(v) in .y (the caller stores it)
+  __device__ __forceinline__ double2 operator()(int64_t v) const {
+    double pn = 0.0;
+    const double y = eval(v, pn);
+    return make_double2(y, pn);
+  }
+  __device__ __forceinline__ double eval(int64_t v, double& pn) const {
+    switch (mode) {
+      case IN_RAW: {
+        const double x = __ldg(u + base + a * N + v);
+        return s == 1.0 ? x : __dmul_rn(s, x);
+      }
+      case IN_FIELD:
+      case IN_CONST: {
+        double acc = 0.0;
+        if (kind == 0) {
+          const double x = mode == IN_CONST ? Ea : __ldg(u + base + a * N + v);
+          acc = __dmul_rn(__ldg(A + v), x);
+        } else {
+#pragma unroll
+          for (int b = 0; b < kMaxDim; ++b) {
+            if (b >= d) break;
+            const double x = mode == IN_CONST ? sel(b, E0, E1, E2) : __ldg(u + base + b * N + v);
+            acc = __dadd_rn(acc, __dmul_rn(coefv(b, v), x));
+          }
         }
+        return s == 1.0 ? acc : __dmul_rn(s, acc);
       }
-      return ia.s == 1.0 ? acc : __dmul_rn(ia.s, acc);
-    }
-    case IN_PNEW: {
-      const bool first = st[r].first;
-      const double beta = st[r].beta;
-      double acc = 0.0;
-      for (int b = 0; b < d; ++b) {
-        if (C.kind == 0 && b != a) continue;
-        const int64_t e = base + b * N + v;
-        double pn = first ? ia.u[e] : __dadd_rn(ia.u[e], __dmul_rn(beta, ia.p_old[e]));
-        if (b == a) ia.p_new[e] = pn;
-        acc = __dadd_rn(acc, __dmul_rn(coef(C, d, a, b, v, N), pn));
+      case IN_PNEW: {
+        double acc = 0.0;
+        if (kind == 0) {
+          const int64_t e = base + a * N + v;
+          const double x = __ldg(u + e);
+          const double q = first ? x : __dadd_rn(x, __dmul_rn(beta, __ldg(p_old + e)));
+          pn = q;
+          acc = __dmul_rn(__ldg(A + v), q);
+        } else {
+#pragma unroll
+          for (int b = 0; b < kMaxDim; ++b) {
+            if (b >= d) break;
+            const int64_t e = base + b * N + v;
+            const double x = __ldg(u + e);
+            const double q = first ? x : __dadd_rn(x, __dmul_rn(beta, __ldg(p_old + e)));
+            if (b == a) pn = q;
+            acc = __dadd_rn(acc, __dmul_rn(coefv(b, v), q));
+          }
+        }
+        return s == 1.0 ? acc : __dmul_rn(s, acc);
       }
-      return ia.s == 1.0 ? acc : __dmul_rn(ia.s, acc);
-    }
-    default: {  // IN_FP: contrast = A - A0 (solver.py:253-255)
-      double acc = 0.0;
-      for (int b = 0; b < d; ++b) {
-        double cab = __dsub_rn(coef(C, d, a, b, v, N), ia.A0[a][b]);
-        acc = __dadd_rn(acc, __dmul_rn(cab, ia.u[base + b * N + v]));
+      default: {  // IN_FP: contrast = A - A0 (solver.py:253-255)
+        double acc = 0.0;
+#pragma unroll
+        for (int b = 0; b < kMaxDim; ++b) {
+          if (b >= d) break;
+          const double cab = __dsub_rn(coefv(b, v), sel(b, R0, R1, R2));
+          acc = __dadd_rn(acc, __dmul_rn(cab, __ldg(u + base + b * N + v)));
+        }
+        return acc;
       }
-      return acc;
     }
   }
+};
+
+// Static-index selection from a kernel-parameter table (dynamic indexing of
+// parameters would force a local-memory copy of the whole argument block).
+__device__ __forceinline__ double pick(const double (&T)[8][kMaxDim], int i, int j) {
+  double v = 0.0;
+#pragma unroll
+  for (int x = 0; x < 8; ++x)
+#pragma unroll
+    for (int y = 0; y < kMaxDim; ++y)
+      if (x == i && y == j) v = T[x][y];
+  return v;
+}
+__device__ __forceinline__ double pick3(const double (&T)[kMaxDim][kMaxDim], int i, int j) {
+  double v = 0.0;
+#pragma unroll
+  for (int x = 0; x < kMaxDim; ++x)
+#pragma unroll
+    for (int y = 0; y < kMaxDim; ++y)
+      if (x == i && y == j) v = T[x][y];
+  return v;
+}
+
+__device__ __forceinline__ InEval make_eval(const InArgs& ia, const Geo& g, const Coef& C, const RhsState* st,
+                                            int r, int a) {
+  InEval ev;
+  ev.mode = ia.mode;
+  ev.d = g.dim;
+  ev.a = a;
+  ev.s = ia.s;
+  ev.N = g.N;
+  ev.base = (int64_t)r * g.dim * g.N;
+  ev.u = ia.u;
+  ev.p_old = ia.p_old;
+  ev.A = C.A;
+  ev.kind = C.kind;
+  ev.first = ia.mode == IN_PNEW ? st[r].first != 0 : true;
+  ev.beta = ia.mode == IN_PNEW ? st[r].beta : 0.0;
+  ev.E0 = pick(ia.E, r, 0);
+  ev.E1 = pick(ia.E, r, 1);
+  ev.E2 = pick(ia.E, r, 2);
+  ev.Ea = pick(ia.E, r, a);
+  ev.R0 = pick3(ia.A0, a, 0);
+  ev.R1 = pick3(ia.A0, a, 1);
+  ev.R2 = pick3(ia.A0, a, 2);
+  return ev;
 }
 
 // Epilogue at voxel v; returns the contribution to the CTA's partial sum.
 __device__ __forceinline__ double ep_apply(const EpArgs& ea, int d, int64_t N, int r, int a, int64_t v,
-                                           double gval) {
+                                           double gval, double Ea) {
   const int64_t e = (int64_t)r * d * N + a * N + v;
   switch (ea.mode) {
     case EP_STORE: ea.out[e] = gval; return 0.0;
     case EP_RHS: { double o = -gval; ea.out[e] = o; return __dmul_rn(o, o); }
     case EP_AP: ea.out[e] = gval; return __dmul_rn(ea.p[e], gval);
     default: {
-      double en = __dsub_rn(ea.E[r][a], gval);
+      double en = __dsub_rn(Ea, gval);
       double df = __dsub_rn(en, ea.out[e]);
       ea.out[e] = en;
       return __dmul_rn(df, df);
@@ -175,6 +288,137 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;  // valid in thread 0
 }
 
+// Sum of n partial slots in a fixed order (thread-strided, then the fixed
+// block tree); L1 is bypassed because other CTAs wrote the slots.
+__device__ double reduce_slots(const double* part, int n, double* red) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += __ldcg(part + i);
+  return block_sum(acc, red);  // thread 0
+}
+
+// Scalar CG / fixed-point logic for RHS r given the reduced sum q = sum / |N|
+// (thread 0 only).  Mirrors solver.py:176-225 and solver.py:264-291.
+__device__ void fin_logic(const FinArgs& f, int r, double sum) {
+  RhsState& S = f.st[r];
+  const double q = sum * f.invN;  // float(np.sum(x*y) / total), solver.py:138-139
+  switch (f.mode) {
+    case FIN_INIT:
+    case FIN_INIT2: {
+      if (f.mode == FIN_INIT) {
+        S.r0 = sqrt(q);
+        S.rr = q;
+        if (f.with_init) return;
+      } else {
+        S.rr = q;
+      }
+      const double h0 = sqrt(S.rr);
+      f.hist[(int64_t)r * f.hcap] = h0;
+      S.hist_len = 1;
+      S.iterations = 0;
+      S.first = 1;
+      S.status = ST_OK;
+      S.beta = 0.0;
+      const bool done = S.r0 == 0.0 || h0 <= f.tol * S.r0;  // solver.py:190-194
+      S.active = done ? 0 : 1;
+      S.converged = done ? 1 : 0;
+      return;
+    }
+    case FIN_ALPHA: {
+      S.pAp = q;
+      if (q <= 0.0) {  // solver.py:203-212
+        S.active = 0;
+        S.converged = 0;
+        S.status = ST_BREAKDOWN;
+        S.detail = q;
+      } else {
+        S.alpha = S.rr / q;
+      }
+      return;
+    }
+    case FIN_BETA: {
+      S.iterations += 1;
+      const double h = sqrt(q);
+      f.hist[(int64_t)r * f.hcap + S.iterations] = h;
+      S.hist_len = S.iterations + 1;
+      if (h <= f.tol * S.r0) {
+        S.converged = 1;
+        S.active = 0;
+      } else {
+        S.beta = q / S.rr;
+        S.rr = q;
+        S.first = 0;
+        if (S.iterations >= f.max_iter) {
+          S.active = 0;
+          S.status = ST_MAXITER;
+        }
+      }
+      return;
+    }
+    case FIN_FP: {
+      const double update = sqrt(q);
+      f.hist[(int64_t)r * f.hcap + S.iterations] = update;
+      S.iterations += 1;
+      S.hist_len = S.iterations;
+      if (update <= f.tol * S.scale) {
+        S.converged = 1;
+        S.active = 0;
+        return;
+      }
+      if (S.has_prev && update > S.prev_update) {
+        S.growth += 1;
+        if (S.growth >= f.window) {
+          S.active = 0;
+          S.status = ST_DIVERGENT;
+          return;
+        }
+      } else {
+        S.growth = 0;
+      }
+      S.prev_update = update;
+      S.has_prev = 1;
+      if (S.iterations >= f.max_iter) {
+        S.active = 0;
+        S.status = ST_MAXITER;
+      }
+      return;
+    }
+    default:
+      return;
+  }
+}
+
+// Arrival of one CTA of a reducing kernel.  Thread 0 must already have stored
+// this CTA's partial.  The last CTA to arrive sums every RHS's slots in fixed
+// order and runs the finalize stage, so no separate finalize launch is needed.
+// Every CTA of the launch must call it exactly once (inactive RHS included).
+__device__ void finish_block(const FinArgs& f, double* red) {
+  if (f.mode == FIN_NONE) return;
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned prev = atomicAdd(f.counter, 1u);
+    last = prev == total - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const bool init = f.mode == FIN_INIT || f.mode == FIN_INIT2;
+  for (int r = 0; r < f.R; ++r) {
+    if (!init && !f.st[r].active) continue;
+    const double sum = reduce_slots(f.part + (int64_t)r * f.nslot, f.nslot, red);
+    if (threadIdx.x == 0) fin_logic(f, r, sum);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int any = 0;
+    for (int r = 0; r < f.R; ++r) any |= f.st[r].active;
+    *f.any_active = any;
+    *f.counter = 0u;
+  }
+}
+
 // Row-sweep geometry: rows of length nl along the contiguous axis, grouped in
 // blocks of B consecutive rows of the previous axis (length np), for each
 // outer index o < no (d = 3: o = i0; d = 2: no = 1).
@@ -194,6 +438,7 @@ __global__ void __launch_bounds__(kThreads) k_row_fwd(Geo g, RowGeo rg, Coef C, 
   const int o = bid % rg.no;
   const int r = (int)(bid / rg.no);
   if (!rhs_active(st, r)) return;
+  const InEval ev = make_eval(ia, g, C, st, r, a);
   const int row0 = tile * rg.B;
   const int nrows = min(rg.B, rg.np - row0);
   const int npairs = (nrows + 1) >> 1;
@@ -206,7 +451,9 @@ __global__ void __launch_bounds__(kThreads) k_row_fwd(Geo g, RowGeo rg, Coef C, 
     double val = 0.0;
     if (row < nrows) {
       const int64_t v = ((int64_t)o * rg.np + row0 + row) * rg.nl + i;
-      val = in_value(ia, g, C, st, r, a, v);
+      double pn = 0.0;
+      val = ev.eval(v, pn);
+      if (ev.mode == IN_PNEW) ia.p_new[ev.base + a * g.N + v] = pn;
     }
     double* dst = reinterpret_cast<double*>(buf0 + (size_t)(row >> 1) * ld + i);
     dst[row & 1] = val;
@@ -238,7 +485,10 @@ __global__ void __launch_bounds__(kThreads) k_row_inv(Geo g, RowGeo rg, EpArgs e
   const int tile = bid % rg.ntiles; bid /= rg.ntiles;
   const int o = bid % rg.no;
   const int r = (int)(bid / rg.no);
-  if (!rhs_active(st, r)) return;
+  if (!rhs_active(st, r)) {
+    finish_block(ea.fin, red);
+    return;
+  }
   const int row0 = tile * rg.B;
   const int nrows = min(rg.B, rg.np - row0);
   const int npairs = (nrows + 1) >> 1;
@@ -262,13 +512,14 @@ __global__ void __launch_bounds__(kThreads) k_row_inv(Geo g, RowGeo rg, EpArgs e
   }
   __syncthreads();
   double2* res = smem_fft<true>(buf0, buf1, npairs, ld, pl);
+  const double Ea = pick(ea.E, r, a);
   double acc = 0.0;
   for (int idx = threadIdx.x; idx < nrows * rg.nl; idx += blockDim.x) {
     const int row = idx / rg.nl, i = idx - row * rg.nl;
     const double2 z = res[(size_t)(row >> 1) * ld + i];
     const double gv = ((row & 1) ? z.y : z.x) * g.invN;
     const int64_t v = ((int64_t)o * rg.np + row0 + row) * rg.nl + i;
-    acc += ep_apply(ea, c, g.N, r, a, v, gv);
+    acc += ep_apply(ea, c, g.N, r, a, v, gv, Ea);
   }
   if (ea.part != nullptr) {
     double s = block_sum(acc, red);
@@ -277,6 +528,7 @@ __global__ void __launch_bounds__(kThreads) k_row_inv(Geo g, RowGeo rg, EpArgs e
       ea.part[(int64_t)r * ea.nslot + slot] = s;
     }
   }
+  finish_block(ea.fin, red);
 }
 
 // Middle sweep (d = 3): W1[r][a][i0][k2][i1] <-> W2[r][a][k2][k1][i0].
@@ -413,11 +665,19 @@ __global__ void __launch_bounds__(kThreads) k_line(Geo g, Coef C, InArgs ia, EpA
   extern __shared__ double2 sm[];
   __shared__ double red[kThreads / 32];
   const int r = blockIdx.x;
-  if (!rhs_active(st, r)) return;
+  if (!rhs_active(st, r)) {
+    finish_block(ea.fin, red);
+    return;
+  }
+  const InEval ev = make_eval(ia, g, C, st, r, 0);
   const int n = g.n[0];
   double2* buf0 = sm;
   double2* buf1 = sm + n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) buf0[i] = make_double2(in_value(ia, g, C, st, r, 0, i), 0.0);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double pn = 0.0;
+    buf0[i] = make_double2(ev.eval(i, pn), 0.0);
+    if (ev.mode == IN_PNEW) ia.p_new[ev.base + i] = pn;
+  }
   __syncthreads();
   double2* res = smem_fft<false>(buf0, buf1, 1, n, pl);
   double2* other = res == buf0 ? buf1 : buf0;
@@ -432,11 +692,13 @@ __global__ void __launch_bounds__(kThreads) k_line(Geo g, Coef C, InArgs ia, EpA
   __syncthreads();
   double2* res2 = smem_fft<true>(other, res, 1, n, pl);
   double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += ep_apply(ea, 1, g.N, r, 0, i, res2[i].x * g.invN);
+  const double Ea = pick(ea.E, r, 0);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += ep_apply(ea, 1, g.N, r, 0, i, res2[i].x * g.invN, Ea);
   if (ea.part != nullptr) {
     double s = block_sum(acc, red);
     if (threadIdx.x == 0) ea.part[(int64_t)r * ea.nslot] = s;
   }
+  finish_block(ea.fin, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -445,30 +707,55 @@ __global__ void __launch_bounds__(kThreads) k_line(Geo g, Coef C, InArgs ia, EpA
 constexpr int kVecTile = kThreads * 16;
 
 // x += alpha p ; r -= alpha Ap ; partial <r, r>     (solver.py:213-216)
-__global__ void __launch_bounds__(kThreads) k_cg_update(int64_t len, RhsState* st, double* x, double* rr,
-                                                        const double* p, const double* Ap, double* part, int nslot) {
+// 16-byte vector accesses when the per-RHS block length is even; the last
+// CTA runs the beta / stop-test finalize (FIN_BETA).
+__global__ void __launch_bounds__(kThreads) k_cg_update(int64_t len, RhsState* st, double* __restrict__ x,
+                                                        double* __restrict__ rr, const double* __restrict__ p,
+                                                        const double* __restrict__ Ap, double* part, int nslot,
+                                                        FinArgs fin) {
   __shared__ double red[kThreads / 32];
   const int r = blockIdx.y;
-  if (!st[r].active) return;
+  if (!st[r].active) {
+    finish_block(fin, red);
+    return;
+  }
   const double alpha = st[r].alpha;
   const int64_t base = (int64_t)r * len;
   const int64_t t0 = (int64_t)blockIdx.x * kVecTile;
   const int64_t t1 = min(len, t0 + kVecTile);
   double acc = 0.0;
-  for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
-    const int64_t e = base + i;
-    x[e] = __dadd_rn(x[e], __dmul_rn(alpha, p[e]));
-    const double rn = __dsub_rn(rr[e], __dmul_rn(alpha, Ap[e]));
-    rr[e] = rn;
-    acc += __dmul_rn(rn, rn);
+  if ((len & 1) == 0) {
+    double2* x2 = reinterpret_cast<double2*>(x + base);
+    double2* r2 = reinterpret_cast<double2*>(rr + base);
+    const double2* p2 = reinterpret_cast<const double2*>(p + base);
+    const double2* a2 = reinterpret_cast<const double2*>(Ap + base);
+    const int64_t h0 = t0 >> 1, h1 = t1 >> 1;
+#pragma unroll 4
+    for (int64_t i = h0 + threadIdx.x; i < h1; i += blockDim.x) {
+      const double2 xv = x2[i], rv = r2[i], pv = __ldg(p2 + i), av = __ldg(a2 + i);
+      x2[i] = make_double2(__dadd_rn(xv.x, __dmul_rn(alpha, pv.x)), __dadd_rn(xv.y, __dmul_rn(alpha, pv.y)));
+      const double2 rn = make_double2(__dsub_rn(rv.x, __dmul_rn(alpha, av.x)), __dsub_rn(rv.y, __dmul_rn(alpha, av.y)));
+      r2[i] = rn;
+      acc += __dmul_rn(rn.x, rn.x);
+      acc += __dmul_rn(rn.y, rn.y);
+    }
+  } else {
+    for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+      const int64_t e = base + i;
+      x[e] = __dadd_rn(x[e], __dmul_rn(alpha, p[e]));
+      const double rn = __dsub_rn(rr[e], __dmul_rn(alpha, Ap[e]));
+      rr[e] = rn;
+      acc += __dmul_rn(rn, rn);
+    }
   }
   double s = block_sum(acc, red);
   if (threadIdx.x == 0) part[(int64_t)r * nslot + blockIdx.x] = s;
+  finish_block(fin, red);
 }
 
 // out = a - b ; partial <out, out>      (r = rhs - op(x), solver.py:186)
 __global__ void __launch_bounds__(kThreads) k_sub_dot(int64_t len, const double* a, const double* b, double* out,
-                                                      double* part, int nslot) {
+                                                      double* part, int nslot, FinArgs fin) {
   __shared__ double red[kThreads / 32];
   const int r = blockIdx.y;
   const int64_t base = (int64_t)r * len;
@@ -482,6 +769,7 @@ __global__ void __launch_bounds__(kThreads) k_sub_dot(int64_t len, const double*
   }
   double s = block_sum(acc, red);
   if (threadIdx.x == 0) part[(int64_t)r * nslot + blockIdx.x] = s;
+  finish_block(fin, red);
 }
 
 // out[r][a][v] = E[r][a] (x == NULL) or x[r][a][v] - E[r][a]   (e = E_N ; solution = e - E_N)
@@ -546,163 +834,6 @@ __global__ void __launch_bounds__(kThreads) k_energy(Geo g, Coef C, Loads L, int
 }
 
 // ---------------------------------------------------------------------------
-// Finalize kernels: one CTA, RHS handled in turn; partials summed in a fixed order.
-__device__ double reduce_slots(const double* part, int n, double* red) {
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += part[i];
-  return block_sum(acc, red);  // thread 0
-}
-
-struct FinArgs {
-  int R;
-  int nslot;
-  const double* part;
-  RhsState* st;
-  double* hist;       // [R][hcap]
-  int hcap;
-  double tol;
-  int max_iter;
-  double invN;
-  int* any_active;
-};
-
-// After rhs = -op(E) (and optionally r = rhs - op(x)): r0, rr, history[0], early exit
-// (solver.py:176-194).  stage 0: rhs norm only ; stage 1: r norm (+ early exit).
-__global__ void k_fin_init(FinArgs f, int stage, int with_init) {
-  __shared__ double red[kThreads / 32];
-  for (int r = 0; r < f.R; ++r) {
-    double s = reduce_slots(f.part + (int64_t)r * f.nslot, f.nslot, red);
-    if (threadIdx.x == 0) {
-      RhsState& S = f.st[r];
-      const double q = s * f.invN;  // float(np.sum(x*y) / total)
-      if (stage == 0) {
-        S.r0 = sqrt(q);
-        S.rr = q;
-      }
-      if (stage == 1 || !with_init) {
-        if (stage == 1) S.rr = q;
-        const double h0 = sqrt(S.rr);
-        f.hist[(int64_t)r * f.hcap] = h0;
-        S.hist_len = 1;
-        S.iterations = 0;
-        S.first = 1;
-        S.status = ST_OK;
-        S.beta = 0.0;
-        if (S.r0 == 0.0 || h0 <= f.tol * S.r0) {
-          S.active = 0;
-          S.converged = 1;
-        } else {
-          S.active = 1;
-          S.converged = 0;
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// pAp, breakdown, alpha (solver.py:202-213)
-__global__ void k_fin_alpha(FinArgs f) {
-  __shared__ double red[kThreads / 32];
-  for (int r = 0; r < f.R; ++r) {
-    if (!f.st[r].active) continue;
-    double s = reduce_slots(f.part + (int64_t)r * f.nslot, f.nslot, red);
-    if (threadIdx.x == 0) {
-      RhsState& S = f.st[r];
-      const double pAp = s * f.invN;
-      S.pAp = pAp;
-      if (pAp <= 0.0) {
-        S.active = 0;
-        S.converged = 0;
-        S.status = ST_BREAKDOWN;
-        S.detail = pAp;
-      } else {
-        S.alpha = S.rr / pAp;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// rr_new, history, stop test, beta (solver.py:216-225)
-__global__ void k_fin_beta(FinArgs f) {
-  __shared__ double red[kThreads / 32];
-  __shared__ int any;
-  if (threadIdx.x == 0) any = 0;
-  for (int r = 0; r < f.R; ++r) {
-    if (!f.st[r].active) continue;
-    double s = reduce_slots(f.part + (int64_t)r * f.nslot, f.nslot, red);
-    if (threadIdx.x == 0) {
-      RhsState& S = f.st[r];
-      const double rr_new = s * f.invN;
-      S.iterations += 1;
-      const double h = sqrt(rr_new);
-      f.hist[(int64_t)r * f.hcap + S.iterations] = h;
-      S.hist_len = S.iterations + 1;
-      if (h <= f.tol * S.r0) {
-        S.converged = 1;
-        S.active = 0;
-      } else {
-        S.beta = rr_new / S.rr;
-        S.rr = rr_new;
-        S.first = 0;
-        if (S.iterations >= f.max_iter) {
-          S.active = 0;
-          S.status = ST_MAXITER;
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    int a = 0;
-    for (int r = 0; r < f.R; ++r) a |= f.st[r].active;
-    *f.any_active = a;
-  }
-}
-
-// Fixed point: update norm, history, stop, growth streak (solver.py:264-291)
-__global__ void k_fin_fp(FinArgs f, int window) {
-  __shared__ double red[kThreads / 32];
-  for (int r = 0; r < f.R; ++r) {
-    if (!f.st[r].active) continue;
-    double s = reduce_slots(f.part + (int64_t)r * f.nslot, f.nslot, red);
-    if (threadIdx.x == 0) {
-      RhsState& S = f.st[r];
-      const double update = sqrt(s * f.invN);
-      f.hist[(int64_t)r * f.hcap + S.iterations] = update;
-      S.iterations += 1;
-      S.hist_len = S.iterations;
-      if (update <= f.tol * S.scale) {
-        S.converged = 1;
-        S.active = 0;
-      } else {
-        if (S.has_prev && update > S.prev_update) {
-          S.growth += 1;
-          if (S.growth >= window) {
-            S.active = 0;
-            S.status = ST_DIVERGENT;
-          }
-        } else {
-          S.growth = 0;
-        }
-        S.prev_update = update;
-        S.has_prev = 1;
-        if (S.active && S.iterations >= f.max_iter) {
-          S.active = 0;
-          S.status = ST_MAXITER;
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    int a = 0;
-    for (int r = 0; r < f.R; ++r) a |= f.st[r].active;
-    *f.any_active = a;
-  }
-}
-
 // Energy matrix finalize: out[i] = (sum of slots) / N in fixed order.
 __global__ void k_fin_matrix(const double* part, int nslot, int nval, double invN, double* out) {
   __shared__ double red[kThreads / 32];

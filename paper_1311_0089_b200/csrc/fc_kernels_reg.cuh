@@ -1,0 +1,257 @@
+// Sweep kernels for power-of-three axis lengths using the register-resident
+// FFT of fc_fft_reg.cuh.  Same data layouts, input modes and epilogues as the
+// generic kernels in fc_kernels.cuh (see the layout comment there).
+#pragma once
+#include "fc_fft_reg.cuh"
+#include "fc_kernels.cuh"
+
+namespace fc {
+
+constexpr int kMaxBlock = 512;   // row / mid sweeps
+constexpr int kMaxBlockOuter = 256;
+
+// First sweep: thread (p, j) of the CTA owns complex pencil p = rows (2p, 2p+1)
+// of the row block and loads elements j + s*TP of both rows, computing the
+// pointwise input on the fly.  After the FFT the spectrum goes through shared
+// memory once more to split the two-for-one pairs and to store transposed.
+template <int L>
+__global__ void __launch_bounds__(kMaxBlock) k_row_fwd_r(Geo g, RowGeo rg, Coef C, InArgs ia, const RhsState* st,
+                                                          const double2* __restrict__ tw, double2* __restrict__ W) {
+  constexpr int TP = R9<L>::TP;
+  extern __shared__ double2 sm[];
+  const int c = g.dim;
+  int64_t bid = blockIdx.x;
+  const int a = bid % c; bid /= c;
+  const int tile = bid % rg.ntiles; bid /= rg.ntiles;
+  const int o = bid % rg.no;
+  const int r = (int)(bid / rg.no);
+  if (!rhs_active(st, r)) return;
+  const int row0 = tile * rg.B;
+  const int nrows = min(rg.B, rg.np - row0);
+  const int p = threadIdx.x / TP;
+  const int j = threadIdx.x - p * TP;
+  const InEval ev = make_eval(ia, g, C, st, r, a);
+  double2 v[1][9];
+  double2 pn[9];  // p' of the (even, odd) row at element s (IN_PNEW)
+  const int re = 2 * p, ro = 2 * p + 1;
+  const bool he = re < nrows, ho = ro < nrows;
+  const int64_t vbase = ((int64_t)o * rg.np + row0) * L;
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+    const int i = j + s * TP;
+    const double2 xe = he ? ev(vbase + (int64_t)re * L + i) : make_double2(0.0, 0.0);
+    const double2 xo = ho ? ev(vbase + (int64_t)ro * L + i) : make_double2(0.0, 0.0);
+    v[0][s] = make_double2(xe.x, xo.x);
+    pn[s] = make_double2(xe.y, xo.y);
+  }
+  if (ev.mode == IN_PNEW) {  // p' = r + beta p, stored once by the CTA owning component a
+    double* pw = ia.p_new + ev.base + (int64_t)a * g.N + vbase;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) {
+      if (he) pw[(int64_t)re * L + j + s * TP] = pn[s].x;
+      if (ho) pw[(int64_t)ro * L + j + s * TP] = pn[s].y;
+    }
+  }
+  double2* smp = sm + (size_t)p * L;
+  fft_reg<L, 1, false>(v, smp, L, j, tw);
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 9; ++s) smp[j + s * TP] = v[0][s];
+  __syncthreads();
+  constexpr int hl = (L + 1) / 2;
+  double2* Wb = W + ((int64_t)(r * c + a) * rg.no + o) * hl * rg.np + row0;
+  for (int idx = threadIdx.x; idx < hl * nrows; idx += blockDim.x) {
+    const int k = idx / nrows, row = idx - k * nrows;
+    const double2* z = sm + (size_t)(row >> 1) * L;
+    const double2 zk = z[k];
+    const double2 zm = z[k == 0 ? 0 : L - k];
+    double2 y;
+    if ((row & 1) == 0) y = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    else y = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+    Wb[(int64_t)k * rg.np + row] = y;
+  }
+}
+
+// Last sweep: transposed half-spectrum load into smem, two-for-one assembly
+// straight into registers, inverse FFT, epilogue from registers (coalesced).
+template <int L>
+__global__ void __launch_bounds__(kMaxBlock, 1) k_row_inv_r(Geo g, RowGeo rg, EpArgs ea, const RhsState* st,
+                                                          const double2* __restrict__ tw,
+                                                          const double2* __restrict__ W) {
+  constexpr int TP = R9<L>::TP;
+  constexpr int hl = (L + 1) / 2;
+  extern __shared__ double2 sm[];
+  __shared__ double red[kMaxBlock / 32];
+  const int c = g.dim;
+  int64_t bid = blockIdx.x;
+  const int a = bid % c; bid /= c;
+  const int tile = bid % rg.ntiles; bid /= rg.ntiles;
+  const int o = bid % rg.no;
+  const int r = (int)(bid / rg.no);
+  if (!rhs_active(st, r)) {
+    finish_block(ea.fin, red);
+    return;
+  }
+  const int row0 = tile * rg.B;
+  const int nrows = min(rg.B, rg.np - row0);
+  const double2* Wb = W + ((int64_t)(r * c + a) * rg.no + o) * hl * rg.np + row0;
+  // Y[row][k] staged at sm[row * hl + k]
+  for (int idx = threadIdx.x; idx < hl * nrows; idx += blockDim.x) {
+    const int k = idx / nrows, row = idx - k * nrows;
+    sm[row * hl + k] = Wb[(int64_t)k * rg.np + row];
+  }
+  __syncthreads();
+  const int p = threadIdx.x / TP;
+  const int j = threadIdx.x - p * TP;
+  const int re = 2 * p, ro = 2 * p + 1;
+  const bool has_o = ro < nrows;
+  double2 v[1][9];
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+    const int i = j + s * TP;
+    const int k = i < hl ? i : L - i;
+    double2 ye = re < nrows ? sm[re * hl + k] : make_double2(0.0, 0.0);
+    double2 yo = has_o ? sm[ro * hl + k] : make_double2(0.0, 0.0);
+    if (i == 0) v[0][s] = make_double2(ye.x, yo.x);
+    else if (i < hl) v[0][s] = make_double2(ye.x - yo.y, ye.y + yo.x);
+    else v[0][s] = make_double2(ye.x + yo.y, yo.x - ye.y);
+  }
+  // the exchange buffer overlaps the Y staging area: fft_reg syncs before its first write
+  double2* smp = sm + (size_t)p * L;
+  fft_reg<L, 1, true>(v, smp, L, j, tw);
+  double acc = 0.0;
+  const double Ea = pick(ea.E, r, a);
+  const int64_t vbase = ((int64_t)o * rg.np + row0) * L;
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+    const int i = j + s * TP;
+    if (re < nrows) acc += ep_apply(ea, c, g.N, r, a, vbase + (int64_t)re * L + i, v[0][s].x * g.invN, Ea);
+    if (has_o) acc += ep_apply(ea, c, g.N, r, a, vbase + (int64_t)ro * L + i, v[0][s].y * g.invN, Ea);
+  }
+  if (ea.part != nullptr) {
+    double sum = block_sum(acc, red);
+    if (threadIdx.x == 0) {
+      const int slot = (o * rg.ntiles + tile) * c + a;
+      ea.part[(int64_t)r * ea.nslot + slot] = sum;
+    }
+  }
+  finish_block(ea.fin, red);
+}
+
+// Middle sweep (d = 3), thread mapping pencil-fastest (t = j * BP + p) so the
+// transposed side is written / read in chunks of BP consecutive i0.
+template <int L, bool INV>
+__global__ void __launch_bounds__(kMaxBlock) k_mid_r(Geo g, MidGeo mg, const RhsState* st,
+                                                      const double2* __restrict__ tw,
+                                                      const double2* __restrict__ src, double2* __restrict__ dst) {
+  constexpr int TP = R9<L>::TP;
+  extern __shared__ double2 sm[];
+  const int c = g.dim;
+  int64_t bid = blockIdx.x;
+  const int ib = bid % mg.nib; bid /= mg.nib;
+  const int k2 = bid % mg.h2; bid /= mg.h2;
+  const int a = bid % c;
+  const int r = (int)(bid / c);
+  if (!rhs_active(st, r)) return;
+  const int BP = mg.B;
+  const int p = threadIdx.x % BP;
+  const int j = threadIdx.x / BP;
+  const int i00 = ib * BP;
+  const bool live = i00 + p < mg.n0;
+  const int64_t rc = (int64_t)(r * c + a);
+  double2 v[1][9];
+  if (!INV) {
+    const double2* s0 = src + ((rc * mg.n0 + i00 + p) * mg.h2 + k2) * L;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) v[0][s] = live ? s0[j + s * TP] : make_double2(0.0, 0.0);
+  } else {
+    const double2* s0 = src + (rc * mg.h2 + k2) * (int64_t)L * mg.n0 + i00 + p;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) v[0][s] = live ? s0[(int64_t)(j + s * TP) * mg.n0] : make_double2(0.0, 0.0);
+  }
+  fft_reg<L, 1, INV>(v, sm + (size_t)p * L, L, j, tw);
+  if (!live) return;
+  if (!INV) {
+    double2* d0 = dst + (rc * mg.h2 + k2) * (int64_t)L * mg.n0 + i00 + p;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) d0[(int64_t)(j + s * TP) * mg.n0] = v[0][s];
+  } else {
+    double2* d0 = dst + ((rc * mg.n0 + i00 + p) * mg.h2 + k2) * L;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) d0[j + s * TP] = v[0][s];
+  }
+}
+
+// Outer sweep: each thread owns the C component pencils of one q so Gamma_hat
+// is applied in registers between the forward and inverse transforms.
+template <int L, int C>
+__global__ void __launch_bounds__(kMaxBlockOuter) k_outer_r(Geo g, OuterGeo og, const RhsState* st,
+                                                        const double2* __restrict__ tw, double2* __restrict__ W) {
+  constexpr int TP = R9<L>::TP;
+  extern __shared__ double2 sm[];
+  const int qb = blockIdx.x % og.nqb;
+  const int r = blockIdx.x / og.nqb;
+  if (!rhs_active(st, r)) return;
+  const int qq = threadIdx.x / TP;
+  const int j = threadIdx.x - qq * TP;
+  const int q = qb * og.QB + qq;
+  const bool live = q < og.Q;
+  double2 v[C][9];
+#pragma unroll
+  for (int a = 0; a < C; ++a) {
+    const double2* s0 = W + (((int64_t)(r * C + a)) * og.Q + q) * L;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) v[a][s] = live ? s0[j + s * TP] : make_double2(0.0, 0.0);
+  }
+  double2* smp = sm + (size_t)qq * C * L;
+  fft_reg<L, C, false>(v, smp, L, j, tw);
+  // Gamma_hat(k) v = xi (xi . v) / den ; 0 at k = 0
+  double xi1 = 0.0, xi2 = 0.0;
+  bool qzero = q == 0;
+  if (C == 2) {
+    xi1 = g.xi[1][live ? q : 0];
+  } else if (C == 3) {
+    const int k2 = q / og.n1, k1 = q - k2 * og.n1;
+    xi1 = g.xi[1][live ? k1 : 0];
+    xi2 = g.xi[2][live ? k2 : 0];
+  }
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+    const int i0 = j + s * TP;
+    double xi[3] = {g.xi[0][i0], xi1, xi2};
+    if (qzero && i0 == 0) {
+#pragma unroll
+      for (int a = 0; a < C; ++a) v[a][s] = make_double2(0.0, 0.0);
+      continue;
+    }
+    double2 dots = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int a = 0; a < C; ++a) {
+      dots.x += xi[a] * v[a][s].x;
+      dots.y += xi[a] * v[a][s].y;
+    }
+    double den = 0.0;
+    if (og.orth) {
+#pragma unroll
+      for (int a = 0; a < C; ++a) den += xi[a] * xi[a];
+    } else {
+#pragma unroll
+      for (int a = 0; a < C; ++a)
+#pragma unroll
+        for (int b = 0; b < C; ++b) den += xi[a] * og.M[a][b] * xi[b];
+    }
+    const double2 qv = make_double2(dots.x / den, dots.y / den);
+#pragma unroll
+    for (int a = 0; a < C; ++a) v[a][s] = make_double2(xi[a] * qv.x, xi[a] * qv.y);
+  }
+  fft_reg<L, C, true>(v, smp, L, j, tw);
+  if (!live) return;
+#pragma unroll
+  for (int a = 0; a < C; ++a) {
+    double2* d0 = W + (((int64_t)(r * C + a)) * og.Q + q) * L;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) d0[j + s * TP] = v[a][s];
+  }
+}
+
+}  // namespace fc
