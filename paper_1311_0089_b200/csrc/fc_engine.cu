@@ -169,8 +169,8 @@ struct fc_ctx {
   const FftPlan& plan(int L) const { return plans.at(L).plan; }
   const double2* rtw(int L) const { return plans.at(L).rtw; }
   // register-path tiling per sweep (0 = generic path)
-  int row_npen = 0, mid_bp = 0, outer_qb = 0;
-  size_t smem_row_r = 0, smem_mid_r = 0, smem_outer_r = 0;
+  int row_npen = 0, mid_bp = 0, outer_qb = 0, inv_prefetch = 1;
+  size_t smem_row_r = 0, smem_row_inv_r = 0, smem_mid_r = 0, smem_outer_r = 0;
 };
 
 namespace {
@@ -330,12 +330,16 @@ int choose_tiles(fc_ctx* c) {
   if (c->force_generic) return FC_OK;
   if (is_pow3_reg(rg.nl)) {
     const int TP = rg.nl / 9;
-    int npen = std::max(1, std::min(16, std::min(env_int("FC_ROW_THREADS", 512), kMaxBlock) / TP));
+    int npen = std::max(1, std::min(16, std::min(env_int("FC_ROW_THREADS", 256), kMaxBlock) / TP));
     npen = std::min(npen, (rg.np + 1) / 2);
     rg.B = 2 * npen;
     rg.ntiles = (rg.np + rg.B - 1) / rg.B;
     c->row_npen = npen;
-    c->smem_row_r = (size_t)16 * npen * (rg.nl + 1);
+    // exchange buffer (16 npen (L+1)) + staging: first sweep u, p_old, A (3 x 2 npen L
+    // doubles), last sweep p / e (2 npen L doubles)
+    c->smem_row_r = (size_t)48 * npen * rg.nl;
+    c->inv_prefetch = env_int("FC_INV_PREFETCH", 0);
+    c->smem_row_inv_r = (size_t)16 * npen * (rg.nl + 1) + (c->inv_prefetch ? (size_t)16 * npen * rg.nl : 0);
   }
   if (d == 3 && is_pow3_reg(c->n[1])) {
     MidGeo& mg = c->mg;
@@ -506,7 +510,7 @@ int run_operator(fc_ctx* c, int R, const InArgs& ia, EpArgs ea, int orth, const 
     const int nt = c->row_npen * (rg.nl / 9);
     const double2* tw = c->rtw(rg.nl);
     return launch(c, "row_inv", [&] {
-      FC_POW3_SWITCH(rg.nl, (k_row_inv_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, ea, st, tw, Wrow)));
+      FC_POW3_SWITCH(rg.nl, (k_row_inv_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_inv_r, s>>>(g, rg, ea, st, tw, Wrow, c->inv_prefetch)));
     });
   }
   const FftPlan pl_last = c->plan(rg.nl);

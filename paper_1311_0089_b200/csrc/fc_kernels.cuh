@@ -153,6 +153,59 @@ struct InEval {
     const double y = eval(v, pn);
     return make_double2(y, pn);
   }
+  // compile-time specialisation (mode / coefficient kind hoisted out of voxel loops)
+  template <int MODE, int KIND>
+  __device__ __forceinline__ double eval_t(int64_t v, double& pn) const {
+    if constexpr (MODE == IN_RAW) {
+      const double x = __ldg(u + base + a * N + v);
+      return s == 1.0 ? x : __dmul_rn(s, x);
+    } else if constexpr (MODE == IN_FIELD || MODE == IN_CONST) {
+      double acc = 0.0;
+      if constexpr (KIND == 0) {
+        const double x = MODE == IN_CONST ? Ea : __ldg(u + base + a * N + v);
+        acc = __dmul_rn(__ldg(A + v), x);
+      } else {
+#pragma unroll
+        for (int b = 0; b < kMaxDim; ++b) {
+          if (b >= d) break;
+          const double x = MODE == IN_CONST ? sel(b, E0, E1, E2) : __ldg(u + base + b * N + v);
+          acc = __dadd_rn(acc, __dmul_rn(__ldg(A + (int64_t)pidx(d, a, b) * N + v), x));
+        }
+      }
+      return s == 1.0 ? acc : __dmul_rn(s, acc);
+    } else if constexpr (MODE == IN_PNEW) {
+      double acc = 0.0;
+      if constexpr (KIND == 0) {
+        const int64_t e = base + a * N + v;
+        const double x = __ldg(u + e);
+        const double q = first ? x : __dadd_rn(x, __dmul_rn(beta, __ldg(p_old + e)));
+        pn = q;
+        acc = __dmul_rn(__ldg(A + v), q);
+      } else {
+#pragma unroll
+        for (int b = 0; b < kMaxDim; ++b) {
+          if (b >= d) break;
+          const int64_t e = base + b * N + v;
+          const double x = __ldg(u + e);
+          const double q = first ? x : __dadd_rn(x, __dmul_rn(beta, __ldg(p_old + e)));
+          if (b == a) pn = q;
+          acc = __dadd_rn(acc, __dmul_rn(__ldg(A + (int64_t)pidx(d, a, b) * N + v), q));
+        }
+      }
+      return s == 1.0 ? acc : __dmul_rn(s, acc);
+    } else {
+      double acc = 0.0;
+#pragma unroll
+      for (int b = 0; b < kMaxDim; ++b) {
+        if (b >= d) break;
+        const double A_ab = KIND == 0 ? (a == b ? __ldg(A + v) : 0.0) : __ldg(A + (int64_t)pidx(d, a, b) * N + v);
+        const double cab = __dsub_rn(A_ab, sel(b, R0, R1, R2));
+        acc = __dadd_rn(acc, __dmul_rn(cab, __ldg(u + base + b * N + v)));
+      }
+      return acc;
+    }
+  }
+
   __device__ __forceinline__ double eval(int64_t v, double& pn) const {
     switch (mode) {
       case IN_RAW: {
@@ -270,6 +323,77 @@ __device__ __forceinline__ double ep_apply(const EpArgs& ea, int d, int64_t N, i
       ea.out[e] = en;
       return __dmul_rn(df, df);
     }
+  }
+}
+
+// Epilogue with the input already loaded (q = p for EP_AP, old e for EP_FP).
+__device__ __forceinline__ double ep_store(const EpArgs& ea, int64_t e, double gval, double Ea, double q) {
+  switch (ea.mode) {
+    case EP_STORE: ea.out[e] = gval; return 0.0;
+    case EP_RHS: { double o = -gval; ea.out[e] = o; return __dmul_rn(o, o); }
+    case EP_AP: ea.out[e] = gval; return __dmul_rn(q, gval);
+    default: {
+      const double en = __dsub_rn(Ea, gval);
+      const double df = __dsub_rn(en, q);
+      ea.out[e] = en;
+      return __dmul_rn(df, df);
+    }
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ double ep_store_t(double* __restrict__ out, int64_t e, double gval, double Ea, double q) {
+  if constexpr (MODE == EP_STORE) {
+    out[e] = gval;
+    return 0.0;
+  } else if constexpr (MODE == EP_RHS) {
+    const double o = -gval;
+    out[e] = o;
+    return __dmul_rn(o, o);
+  } else if constexpr (MODE == EP_AP) {
+    out[e] = gval;
+    return __dmul_rn(q, gval);
+  } else {
+    const double en = __dsub_rn(Ea, gval);
+    const double df = __dsub_rn(en, q);
+    out[e] = en;
+    return __dmul_rn(df, df);
+  }
+}
+
+// Run f(integral_constant<MODE>, integral_constant<KIND>) with runtime values
+// lifted to compile time (the switch sits outside every voxel loop).
+template <int V>
+struct IC {
+  static constexpr int value = V;
+};
+template <typename F>
+__device__ __forceinline__ void with_in_mode(int mode, int kind, F&& f) {
+  if (kind == 0) {
+    switch (mode) {
+      case IN_FIELD: f(IC<IN_FIELD>{}, IC<0>{}); break;
+      case IN_PNEW: f(IC<IN_PNEW>{}, IC<0>{}); break;
+      case IN_CONST: f(IC<IN_CONST>{}, IC<0>{}); break;
+      case IN_FP: f(IC<IN_FP>{}, IC<0>{}); break;
+      default: f(IC<IN_RAW>{}, IC<0>{}); break;
+    }
+  } else {
+    switch (mode) {
+      case IN_FIELD: f(IC<IN_FIELD>{}, IC<1>{}); break;
+      case IN_PNEW: f(IC<IN_PNEW>{}, IC<1>{}); break;
+      case IN_CONST: f(IC<IN_CONST>{}, IC<1>{}); break;
+      case IN_FP: f(IC<IN_FP>{}, IC<1>{}); break;
+      default: f(IC<IN_RAW>{}, IC<1>{}); break;
+    }
+  }
+}
+template <typename F>
+__device__ __forceinline__ void with_ep_mode(int mode, F&& f) {
+  switch (mode) {
+    case EP_STORE: f(IC<EP_STORE>{}); break;
+    case EP_RHS: f(IC<EP_RHS>{}); break;
+    case EP_AP: f(IC<EP_AP>{}); break;
+    default: f(IC<EP_FP>{}); break;
   }
 }
 

@@ -8,6 +8,20 @@
 namespace fc {
 
 constexpr int kMaxBlock = 512;   // row / mid sweeps
+
+// 8-byte asynchronous global->shared copies (LDGSTS): loads stay in flight
+// without holding registers, so a CTA issues its whole input tile at once.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+// Copy n contiguous doubles to shared memory, block-strided.
+__device__ __forceinline__ void stage_doubles(double* dst, const double* src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) cp_async8(dst + i, src + i);
+}
 constexpr int kMaxBlockOuter = 256;
 
 // First sweep: thread (p, j) of the CTA owns complex pencil p = rows (2p, 2p+1)
@@ -36,13 +50,62 @@ __global__ void __launch_bounds__(kMaxBlock) k_row_fwd_r(Geo g, RowGeo rg, Coef 
   const int re = 2 * p, ro = 2 * p + 1;
   const bool he = re < nrows, ho = ro < nrows;
   const int64_t vbase = ((int64_t)o * rg.np + row0) * L;
+  // staged path: isotropic A, and for the fixed point a reference row without
+  // off-diagonal entries (then (A - A0) e is diagonal, solver.py:253-255)
+  const bool fp_diag = ev.mode != IN_FP ||
+                       ((a == 0 || ev.R0 == 0.0) && (a == 1 || ev.R1 == 0.0) && (a == 2 || ev.R2 == 0.0));
+  if (ev.kind == 0 && ev.mode != IN_CONST && fp_diag) {
+    // isotropic: stage u (r / e / field), p_old and A for the whole row block in
+    // smem with cp.async, then evaluate from smem (the staging area is reused as
+    // the FFT exchange buffer afterwards)
+    double* st_u = reinterpret_cast<double*>(sm);
+    double* st_p = st_u + rg.B * L;
+    double* st_a = st_p + rg.B * L;
+    const int n = nrows * L;
+    const int64_t ub = ev.base + (int64_t)a * g.N + vbase;
+    stage_doubles(st_u, ev.u + ub, n);
+    if (ev.mode == IN_PNEW && !ev.first) stage_doubles(st_p, ev.p_old + ub, n);
+    if (ev.mode != IN_RAW) stage_doubles(st_a, ev.A + vbase, n);
+    cp_async_wait_all();
+    __syncthreads();
 #pragma unroll
-  for (int s = 0; s < 9; ++s) {
-    const int i = j + s * TP;
-    const double2 xe = he ? ev(vbase + (int64_t)re * L + i) : make_double2(0.0, 0.0);
-    const double2 xo = ho ? ev(vbase + (int64_t)ro * L + i) : make_double2(0.0, 0.0);
-    v[0][s] = make_double2(xe.x, xo.x);
-    pn[s] = make_double2(xe.y, xo.y);
+    for (int s = 0; s < 9; ++s) {
+      const int i = j + s * TP;
+      double y[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = 2 * p + h;
+        if (row < nrows) {
+          const int e = row * L + i;
+          double x = st_u[e];
+          if (ev.mode == IN_PNEW) {
+            x = ev.first ? x : __dadd_rn(x, __dmul_rn(ev.beta, st_p[e]));
+            q[h] = x;
+          }
+          double val;
+          if (ev.mode == IN_RAW) val = x;
+          else if (ev.mode == IN_FP) val = __dmul_rn(__dsub_rn(st_a[e], InEval::sel(a, ev.R0, ev.R1, ev.R2)), x);
+          else val = __dmul_rn(st_a[e], x);
+          if (ev.mode != IN_FP && ev.s != 1.0) val = __dmul_rn(ev.s, val);
+          y[h] = val;
+        }
+      }
+      v[0][s] = make_double2(y[0], y[1]);
+      pn[s] = make_double2(q[0], q[1]);
+    }
+  } else {
+    with_in_mode(ev.mode, ev.kind, [&](auto M, auto K) {
+      constexpr int MODE = decltype(M)::value, KIND = decltype(K)::value;
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+        const int i = j + s * TP;
+        double pe = 0.0, po = 0.0;
+        const double xe = he ? ev.template eval_t<MODE, KIND>(vbase + (int64_t)re * L + i, pe) : 0.0;
+        const double xo = ho ? ev.template eval_t<MODE, KIND>(vbase + (int64_t)ro * L + i, po) : 0.0;
+        v[0][s] = make_double2(xe, xo);
+        pn[s] = make_double2(pe, po);
+      }
+    });
   }
   if (ev.mode == IN_PNEW) {  // p' = r + beta p, stored once by the CTA owning component a
     double* pw = ia.p_new + ev.base + (int64_t)a * g.N + vbase;
@@ -77,7 +140,7 @@ __global__ void __launch_bounds__(kMaxBlock) k_row_fwd_r(Geo g, RowGeo rg, Coef 
 template <int L>
 __global__ void __launch_bounds__(kMaxBlock, 1) k_row_inv_r(Geo g, RowGeo rg, EpArgs ea, const RhsState* st,
                                                           const double2* __restrict__ tw,
-                                                          const double2* __restrict__ W) {
+                                                          const double2* __restrict__ W, int prefetch) {
   constexpr int TP = R9<L>::TP;
   constexpr int hl = (L + 1) / 2;
   extern __shared__ double2 sm[];
@@ -95,10 +158,36 @@ __global__ void __launch_bounds__(kMaxBlock, 1) k_row_inv_r(Geo g, RowGeo rg, Ep
   const int row0 = tile * rg.B;
   const int nrows = min(rg.B, rg.np - row0);
   const double2* Wb = W + ((int64_t)(r * c + a) * rg.no + o) * hl * rg.np + row0;
-  // Y[row][k] staged at sm[row * hl + k]
-  for (int idx = threadIdx.x; idx < hl * nrows; idx += blockDim.x) {
-    const int k = idx / nrows, row = idx - k * nrows;
-    sm[row * hl + k] = Wb[(int64_t)k * rg.np + row];
+  const int64_t vbase = ((int64_t)o * rg.np + row0) * L;
+  const int64_t ebase = ((int64_t)r * c + a) * g.N + vbase;
+  // epilogue input (p for EP_AP, e for EP_FP) prefetched with cp.async into the
+  // area behind the exchange buffer; it lands while the spectrum is transformed
+  double* st_q = reinterpret_cast<double*>(sm + (size_t)(rg.B / 2) * (L + 1));
+  const bool need_q = ea.mode == EP_AP || ea.mode == EP_FP;
+  const double* qsrc = (ea.mode == EP_AP ? ea.p : ea.out) + ebase;
+  if (need_q && prefetch) stage_doubles(st_q, qsrc, nrows * L);
+  // Y[row][k] staged at sm[row * hl + k]; 8 loads in flight per thread
+  {
+    const int total = hl * nrows;
+    for (int base = 0; base < total; base += 8 * blockDim.x) {
+      double2 t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = base + u * blockDim.x + threadIdx.x;
+        if (idx < total) {
+          const int k = idx / nrows, row = idx - k * nrows;
+          t[u] = __ldg(Wb + (int64_t)k * rg.np + row);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = base + u * blockDim.x + threadIdx.x;
+        if (idx < total) {
+          const int k = idx / nrows, row = idx - k * nrows;
+          sm[row * hl + k] = t[u];
+        }
+      }
+    }
   }
   __syncthreads();
   const int p = threadIdx.x / TP;
@@ -119,15 +208,37 @@ __global__ void __launch_bounds__(kMaxBlock, 1) k_row_inv_r(Geo g, RowGeo rg, Ep
   // the exchange buffer overlaps the Y staging area: fft_reg syncs before its first write
   double2* smp = sm + (size_t)p * L;
   fft_reg<L, 1, true>(v, smp, L, j, tw);
-  double acc = 0.0;
   const double Ea = pick(ea.E, r, a);
-  const int64_t vbase = ((int64_t)o * rg.np + row0) * L;
+  const bool he = re < nrows;
+  double2 q[9];
+  if (need_q && prefetch) {
+    cp_async_wait_all();
+    __syncthreads();
 #pragma unroll
-  for (int s = 0; s < 9; ++s) {
-    const int i = j + s * TP;
-    if (re < nrows) acc += ep_apply(ea, c, g.N, r, a, vbase + (int64_t)re * L + i, v[0][s].x * g.invN, Ea);
-    if (has_o) acc += ep_apply(ea, c, g.N, r, a, vbase + (int64_t)ro * L + i, v[0][s].y * g.invN, Ea);
+    for (int s = 0; s < 9; ++s) {
+      const int i = j + s * TP;
+      q[s].x = he ? st_q[re * L + i] : 0.0;
+      q[s].y = has_o ? st_q[ro * L + i] : 0.0;
+    }
+  } else if (need_q) {
+#pragma unroll
+    for (int s = 0; s < 9; ++s) {
+      const int i = j + s * TP;
+      q[s].x = he ? __ldg(qsrc + re * L + i) : 0.0;
+      q[s].y = has_o ? __ldg(qsrc + ro * L + i) : 0.0;
+    }
   }
+  double acc = 0.0;
+  with_ep_mode(ea.mode, [&](auto M) {
+    constexpr int MODE = decltype(M)::value;
+    double* __restrict__ out = ea.out;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) {
+      const int i = j + s * TP;
+      if (he) acc += ep_store_t<MODE>(out, ebase + (int64_t)re * L + i, v[0][s].x * g.invN, Ea, q[s].x);
+      if (has_o) acc += ep_store_t<MODE>(out, ebase + (int64_t)ro * L + i, v[0][s].y * g.invN, Ea, q[s].y);
+    }
+  });
   if (ea.part != nullptr) {
     double sum = block_sum(acc, red);
     if (threadIdx.x == 0) {
@@ -185,7 +296,7 @@ __global__ void __launch_bounds__(kMaxBlock) k_mid_r(Geo g, MidGeo mg, const Rhs
 // Outer sweep: each thread owns the C component pencils of one q so Gamma_hat
 // is applied in registers between the forward and inverse transforms.
 template <int L, int C>
-__global__ void __launch_bounds__(kMaxBlockOuter) k_outer_r(Geo g, OuterGeo og, const RhsState* st,
+__global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Geo g, OuterGeo og, const RhsState* st,
                                                         const double2* __restrict__ tw, double2* __restrict__ W) {
   constexpr int TP = R9<L>::TP;
   extern __shared__ double2 sm[];
