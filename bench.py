@@ -131,46 +131,108 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- workload
-def workload(n):
-    from paper_1311_0089_b200 import generators as gen
+class Workload:
+    """One BASELINE configuration: device setup, loads, byte model, CPU sample."""
 
-    a = gen.cfg2_random_two_phase(n)
-    return a, np.array(gen.CFG2_LOADS)
+    def __init__(self, name, n):
+        from paper_1311_0089_b200 import generators as gen
 
+        self.name = name
+        if name == "cfg2":
+            self.n = n or 2187
+            self.shape = (self.n, self.n)
+            self.loads = np.array(gen.CFG2_LOADS)
+            self.nA = 1
+            self.desc = (f"cfg2: {self.n}x{self.n} two-phase random medium (contrast 100, seed 2187), "
+                         f"3 load cases batched in one CG solve to 1e-8 (BASELINE configs[1])")
+        elif name == "cfg3":
+            self.n = n or 243
+            self.shape = (self.n,) * 3
+            self.loads = np.array([[1.0, 0.0, 0.0]])
+            self.nA = 1
+            self.desc = f"cfg3: {self.n}^3 centred sphere (radius 0.35 cell, contrast 50), E=(1,0,0), CG to 1e-8"
+        elif name == "cfg4":
+            self.n = n or 729
+            self.shape = (self.n,) * 3
+            self.loads = np.array([[1.0, 0.0, 0.0]])
+            self.nA = 6
+            self.desc = (f"cfg4: {self.n}^3 polycrystal, 512 seeded Voronoi grains (seed 729) with lognormal "
+                         f"SPD tensors, generated on the device; E=(1,0,0), CG to 1e-8")
+        else:
+            raise ValueError(name)
+        self.d = len(self.shape)
+        self.R = self.loads.shape[0]
+        self.N = int(np.prod(self.shape))
 
-def kernel_bytes_per_voxel(name, c, R, nA):
-    """Algorithmic bytes per voxel of one launch (SURVEY 8(d) byte model, CG loop)."""
-    w = 8
-    return {
-        "row_fwd": w * (nA + 4 * c * R),   # read r, p ; write p' ; write spectrum  (+ A once)
-        "mid_fwd": w * 2 * c * R,
-        "outer": w * 2 * c * R,
-        "mid_inv": w * 2 * c * R,
-        "row_inv": w * 3 * c * R,          # read spectrum, write Ap, read p
-        "cg_update": w * 6 * c * R,        # read x, r, p, Ap ; write x, r
-    }.get(name)
+    def host_field(self):
+        from paper_1311_0089_b200 import generators as gen
+
+        if self.name == "cfg2":
+            return gen.cfg2_random_two_phase(self.n)
+        if self.name == "cfg3":
+            return gen.cfg3_sphere(self.n)
+        return None
+
+    def setup(self, ctx, host_field=None):
+        """Put the coefficient field in HBM (upload, or generate on the device for cfg4)."""
+        if self.name == "cfg4":
+            from paper_1311_0089_b200 import generators as gen
+
+            seeds, packed = gen.cfg4_grains(512, gen.SEEDS["cfg4"], self.n)
+            ctx.generate_voronoi(seeds, packed)
+            return 3 * 512 * 8 + 6 * 512 * 8
+        ctx.set_coefficients(host_field)
+        return host_field.isotropic_values.nbytes
+
+    def iter_bytes(self):
+        c, R = self.d, self.R
+        S = 2 * self.d - 1
+        return 8 * self.N * (self.nA + 2 * S * c * R + 9 * c * R)
+
+    def kernel_bytes(self, name):
+        """Algorithmic bytes of one launch (SURVEY 8(d) byte model, CG loop)."""
+        w, c, R, nA = 8, self.d, self.R, self.nA
+        per = {
+            "row_fwd": w * (nA + 4 * c * R),   # read r, p ; write p' ; write spectrum  (+ A once)
+            "mid_fwd": w * 2 * c * R,
+            "outer": w * 2 * c * R,
+            "mid_inv": w * 2 * c * R,
+            "row_inv": w * 3 * c * R,          # read spectrum, write Ap, read p
+            "cg_update": w * 6 * c * R,        # read x, r, p, Ap ; write x, r
+        }.get(name)
+        return None if per is None else per * self.N
 
 
 def _oracle_worker(args):
-    n, E, seconds = args
+    name, n, E, seconds = args
     from oracle import fftcell_oracle as orc
     from paper_1311_0089_b200 import generators as gen
 
-    a = gen.cfg2_random_two_phase(n)
-    full = orc.isotropic_full(a.components[0], 2)
+    if name == "cfg2":
+        a = gen.cfg2_random_two_phase(n)
+        full = orc.isotropic_full(a.components[0], 2)
+    elif name == "cfg3":
+        a = gen.cfg3_sphere(n)
+        full = orc.isotropic_full(a.components[0], 3)
+    else:
+        a = gen.cfg4_polycrystal(n)
+        full = orc.unpack(a.components, 3)
     rep = orc.solve_cg(full, tuple(E), a.spec.shape, a.spec.half_periods, TOL, MAX_ITER, max_seconds=seconds)
-    return rep["iterations"], rep["loop_seconds"]
+    return rep["iterations"], rep["loop_seconds"], a.spec.total
 
 
-def cpu_sample(n, loads, seconds):
-    """Time-bounded oracle CG, one process per load case (the reference is single-threaded)."""
-    with ProcessPoolExecutor(len(loads)) as ex:
-        res = list(ex.map(_oracle_worker, [(n, E, seconds) for E in loads]))
-    N = n * n
-    work = sum(N * it for it, _ in res)
-    t = max(s for _, s in res)
-    its = [it for it, _ in res]
-    return work, t, its
+def cpu_sample(wl, seconds):
+    """Time-bounded oracle CG, one process per load case (the reference is single-threaded).
+
+    cfg4 at 729^3 does not fit the reference's ~440 B/voxel; its sample runs the same
+    generator at 81^3 (throughput per grid point is reported)."""
+    n = wl.n if wl.name != "cfg4" else min(wl.n, 81)
+    with ProcessPoolExecutor(len(wl.loads)) as ex:
+        res = list(ex.map(_oracle_worker, [(wl.name, n, E, seconds) for E in wl.loads]))
+    work = sum(N * it for it, _, N in res)
+    t = max(s for _, s, _ in res)
+    its = [it for it, _, _ in res]
+    return work, t, its, n
 
 
 # --------------------------------------------------------------------------- arms
@@ -178,35 +240,34 @@ def run_reference(args):
     world, rank, _ = dist_setup()
     if rank != 0:
         return
-    n = args.n
-    _, loads = workload(n)
+    wl = Workload(args.config, args.n)
     total_work, total_t = 0.0, 0.0
-    sample_its = []
+    sample = None
     for step in range(args.warmup + args.steps):
-        work, t, its = cpu_sample(n, loads, args.cpu_seconds)
+        work, t, its, n = cpu_sample(wl, args.cpu_seconds)
         if step >= args.warmup:
             total_work += work
             total_t += t
-            sample_its.append(its)
+            sample = (its, n)
     v = total_work / total_t
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total_t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(n),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": len(loads), "kind": "port",
-                         "sample": f"per step: the first CG iterations of each of the {len(loads)} load cases "
-                                   f"of cfg2 ({n}^2), {args.cpu_seconds:g} s per load case, one process each "
-                                   f"(numpy pocketfft restatement of solver.py:142-230); iterations {sample_its[0]}"},
+        "data": "synthetic", "config": config_dict(wl),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": len(wl.loads), "kind": "port",
+                         "sample": f"per step: the first CG iterations of each of the {len(wl.loads)} load case(s) "
+                                   f"of {wl.name} at {sample[1]}^{wl.d}, {args.cpu_seconds:g} s each, one process "
+                                   f"per load case (numpy pocketfft restatement of solver.py:142-230); "
+                                   f"iterations {sample[0]}"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def config_dict(n):
-    return {"workload": f"cfg2: {n}x{n} two-phase random medium (contrast 100, seed 2187), 3 load cases "
-                        f"batched in one CG solve to 1e-8 (BASELINE configs[1])",
-            "grid": [n, n], "load_cases": 3, "tol": TOL, "parallelism": "replicas",
+def config_dict(wl):
+    return {"workload": wl.desc, "grid": list(wl.shape), "load_cases": wl.R, "tol": TOL,
+            "parallelism": "replicas",
             "l2": "inputs larger than L2 (per-iteration working set > 126 MB)"}
 
 
@@ -214,20 +275,19 @@ def run_gpu(args):
     world, rank, local = dist_setup()
     from paper_1311_0089_b200 import _native
     from paper_1311_0089_b200.material import CoefficientField
+    from paper_1311_0089_b200.grid import GridSpec
 
-    n = args.n
-    a_host, loads = workload(n)
-    R = len(loads)
-    N = n * n
-    d = 2
-    ctx = _native.Context(a_host.spec, local)
-    ctx.set_coefficients(a_host)
+    wl = Workload(args.config, args.n)
+    loads, R, N, d = wl.loads, wl.R, wl.N, wl.d
+    host = wl.host_field()
+    spec = GridSpec((1.0,) * d, wl.shape)
+    ctx = _native.Context(spec, local)
+    wl.setup(ctx, host)
 
     def solve_resident():
         reps, _, _ = ctx.solve_cg(loads, TOL, MAX_ITER, want_x=False)
         return reps
 
-    # warm-up
     for _ in range(args.warmup):
         reps = solve_resident()
     iters = [r["iterations"] for r in reps]
@@ -254,68 +314,74 @@ def run_gpu(args):
     # ---- e2e: host buffers through the public API -----------------------------
     import torch
 
-    pin_a = torch.empty(a_host.components.shape, dtype=torch.float64, pin_memory=True).numpy()
-    pin_a[...] = a_host.components
-    a_pinned = CoefficientField(a_host.spec, pin_a)
-    x_out = torch.empty((R, d, n, n), dtype=torch.float64, pin_memory=True).numpy()
-    h2d = a_pinned.isotropic_values.nbytes + loads.nbytes
+    x_out = torch.empty((R, d) + wl.shape, dtype=torch.float64, pin_memory=True).numpy()
+    a_pinned = None
+    if host is not None:
+        pin_a = torch.empty(host.components.shape, dtype=torch.float64, pin_memory=True).numpy()
+        pin_a[...] = host.components
+        a_pinned = CoefficientField(host.spec, pin_a)
+    h2d = wl.setup(ctx, a_pinned) + loads.nbytes
+    ctx.solve_cg(loads, TOL, MAX_ITER, out=x_out)
     d2h = x_out.nbytes
-    for _ in range(1):
-        ctx.set_coefficients(a_pinned)
-        ctx.solve_cg(loads, TOL, MAX_ITER, out=x_out)
+    e2e_steps = max(1, args.steps if wl.name != "cfg4" else 1)
     barrier(world)
     ctx.timer_mark(2)
-    for _ in range(args.steps):
-        ctx.set_coefficients(a_pinned)
+    for _ in range(e2e_steps):
+        wl.setup(ctx, a_pinned)
         ctx.solve_cg(loads, TOL, MAX_ITER, out=x_out)
     ctx.timer_mark(3)
     ms_e2e = max_over_ranks(world, ctx.timer_elapsed(2, 3))
-    e2e = world * work_per_step * args.steps / (ms_e2e / 1000.0)
+    e2e = world * work_per_step * e2e_steps / (ms_e2e / 1000.0)
 
     if rank != 0:
         return
-    # ---- roofline of the dominant kernel ------------------------------------------
     peak, peak_kind = peaks()
-    kern = {k: v for k, v in prof.items() if kernel_bytes_per_voxel(k, d, R, 1) is not None}
+    kern = {k: v for k, v in prof.items() if wl.kernel_bytes(k) is not None}
     top = max(kern, key=lambda k: kern[k][1])
-    nl, avg_ms = kern[top][0], kern[top][1] / kern[top][0]
-    bytes_launch = kernel_bytes_per_voxel(top, d, R, 1) * N
+    avg_ms = kern[top][1] / kern[top][0]
+    bytes_launch = wl.kernel_bytes(top)
     achieved = bytes_launch / (avg_ms / 1000.0) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "ncu_traffic.json"
     if tp.exists():
-        traffic = json.loads(tp.read_text()).get(f"cfg2/{top}")
+        traffic = json.loads(tp.read_text()).get(f"{wl.name}/{top}")
     step_ms = ms / args.steps
-    iter_bytes = 728 * N  # B_iter/voxel for cfg2 (R=3, isotropic)
-    n_iter_launch = max(iters)
+    n_iter = max(iters)
     roofline = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
                 "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_ms,
                 "share_of_step": kern[top][1] / ms}
-    per_kernel = {k: {"launches": v[0], "avg_ms": v[1] / max(v[0], 1),
-                      "GBps": (kernel_bytes_per_voxel(k, d, R, 1) * N / (v[1] / max(v[0], 1) / 1000) / 1e9)
-                      if kernel_bytes_per_voxel(k, d, R, 1) else None}
-                  for k, v in prof.items()}
-    iteration = {"bytes": iter_bytes, "ms": step_ms / n_iter_launch,
-                 "GBps": iter_bytes / (step_ms / n_iter_launch / 1000) / 1e9}
+    per_kernel = {}
+    for k, v in prof.items():
+        avg = v[1] / max(v[0], 1)
+        kb = wl.kernel_bytes(k)
+        per_kernel[k] = {"launches": v[0], "avg_ms": avg, "GBps": kb / (avg / 1000) / 1e9 if kb else None}
+    iteration = {"bytes": wl.iter_bytes(), "ms": step_ms / n_iter,
+                 "GBps": wl.iter_bytes() / (step_ms / n_iter / 1000) / 1e9}
     iteration["frac"] = iteration["GBps"] / peak
+    op_names = [k for k in ("row_fwd", "mid_fwd", "outer", "mid_inv", "row_inv") if k in prof]
+    op_ms = sum(per_kernel[k]["avg_ms"] for k in op_names)
+    op_bytes = sum(wl.kernel_bytes(k) for k in op_names)
+    operator = {"kernels": op_names, "ms": op_ms, "GBps": op_bytes / (op_ms / 1000) / 1e9}
+    operator["frac"] = operator["GBps"] / peak
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        work, t, its = cpu_sample(n, loads, args.cpu_seconds)
+        work, t, its, n = cpu_sample(wl, args.cpu_seconds)
         cpu = {"value": work / t, "unit": UNIT, "cores": R, "kind": "port",
-               "sample": f"first CG iterations of each of the {R} load cases of cfg2 ({n}^2), "
-                         f"{args.cpu_seconds:g} s per load case, one process each; iterations {its}"}
+               "sample": f"first CG iterations of each of the {R} load case(s) of {wl.name} at {n}^{d}, "
+                         f"{args.cpu_seconds:g} s each, one process per load case; iterations {its}"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(n),
+        "config": config_dict(wl),
         "iterations": iters,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,
         "roofline": roofline,
         "iteration_roofline": iteration,
+        "operator_roofline": operator,
         "kernels": per_kernel,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
@@ -329,7 +395,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=2187, help="grid size (BASELINE cfg2: 2187)")
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4"],
+                    help="BASELINE configuration (default cfg2 = configs[1], the metric's workload)")
+    ap.add_argument("--n", type=int, default=0, help="override the grid size (0 = BASELINE size)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -109,6 +109,13 @@ int32_t fc_solve_fixed_point(fc_ctx* ctx, int32_t nrhs, const double* E, double 
  * solution resident on the device; otherwise x is (nrhs, d, *N) on the host. */
 int32_t fc_energy(fc_ctx* ctx, int32_t nrhs, const double* E, const double* x, double* out);
 
+/* Device generator for the BASELINE cfg4 polycrystal: nearest of n_seeds
+ * seeds (voxel units on the periodic torus, (n_seeds, 3)) under the minimum image; the
+ * coefficient field becomes the grain tensors packed[(n_seeds, 6)].  labels_out (N int32)
+ * may be NULL.  Bit-identical to generators.voronoi_labels. */
+int32_t fc_generate_voronoi(fc_ctx* ctx, int32_t n_seeds, const double* seeds, const double* packed,
+                            int32_t* labels_out);
+
 /* Instrumentation used by bench.py: per-kernel CUDA-event timing and a launch counter. */
 int32_t fc_set_profiling(fc_ctx* ctx, int32_t on);
 int32_t fc_profile_count(fc_ctx* ctx);

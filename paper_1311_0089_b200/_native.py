@@ -54,6 +54,8 @@ SIGNATURES = [
      [ctypes.c_void_p, ctypes.c_int32, _dp, ctypes.c_double, ctypes.c_int32, _dp, _dp, _dp,
       ctypes.POINTER(Report), _dp]),
     ("fc_energy", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, _dp, _dp, _dp]),
+    ("fc_generate_voronoi", ctypes.c_int32,
+     [ctypes.c_void_p, ctypes.c_int32, _dp, _dp, ctypes.POINTER(ctypes.c_int32)]),
     ("fc_set_profiling", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32]),
     ("fc_profile_count", ctypes.c_int32, [ctypes.c_void_p]),
     ("fc_profile_get", ctypes.c_int32,
@@ -141,6 +143,16 @@ class Context:
             kind = 1
         _check(lib().fc_set_coefficients(self._h, kind, _ptr(host), host.size))
         self.isotropic = kind == 0
+
+    def generate_voronoi(self, seeds, packed, want_labels=False):
+        """Device-side cfg4 polycrystal (replaces the coefficient field)."""
+        seeds = _c64(seeds)
+        packed = _c64(packed)
+        labels = np.empty(self.shape, dtype=np.int32) if want_labels else None
+        lp = labels.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)) if want_labels else None
+        _check(lib().fc_generate_voronoi(self._h, seeds.shape[0], _ptr(seeds), _ptr(packed), lp))
+        self.isotropic = False
+        return labels
 
     # -- batched field operators ------------------------------------------
     def _batched(self, fn, u, *extra):

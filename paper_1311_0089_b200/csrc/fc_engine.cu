@@ -979,6 +979,42 @@ int32_t fc_energy(fc_ctx* c, int32_t R, const double* E, const double* x, double
   return sync(c);
 }
 
+int32_t fc_generate_voronoi(fc_ctx* c, int32_t n_seeds, const double* seeds, const double* packed,
+                            int32_t* labels_out) {
+  TRY(check_ctx(c, false));
+  if (c->dim != 3) return set_err(FC_EINVAL, "the Voronoi generator is three-dimensional");
+  if (n_seeds < 1 || n_seeds > 4096) return set_err(FC_EINVAL, "n_seeds must lie in [1, 4096]");
+  const int nsym = 6;
+  double *d_seeds = nullptr, *d_packed = nullptr;
+  int* d_lab = nullptr;
+  CK(cudaMalloc(&d_seeds, sizeof(double) * 3 * n_seeds));
+  CK(cudaMalloc(&d_packed, sizeof(double) * nsym * n_seeds));
+  CK(cudaMemcpy(d_seeds, seeds, sizeof(double) * 3 * n_seeds, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_packed, packed, sizeof(double) * nsym * n_seeds, cudaMemcpyHostToDevice));
+  if (labels_out) CK(cudaMalloc(&d_lab, sizeof(int) * c->N));
+  const int64_t count = (int64_t)nsym * c->N;
+  if (c->A == nullptr || c->A_count != count) {
+    cudaFree(c->A);
+    c->A = nullptr;
+    CK(cudaMalloc(&c->A, sizeof(double) * count));
+    c->A_count = count;
+  }
+  c->coef_kind = FC_COEF_PACKED;
+  const int blocks = c->num_sms * 8;
+  const size_t sm = sizeof(double) * 3 * n_seeds;
+  CK(cudaFuncSetAttribute(k_gen_voronoi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  TRY(launch(c, "gen_voronoi", [&] {
+    k_gen_voronoi<<<blocks, 256, sm, c->stream>>>(c->n[0], c->n[1], c->n[2], n_seeds, d_seeds, d_packed, nsym, c->N,
+                                                  c->A, d_lab);
+  }));
+  if (labels_out) CK(cudaMemcpyAsync(labels_out, d_lab, sizeof(int) * c->N, cudaMemcpyDeviceToHost, c->stream));
+  TRY(sync(c));
+  cudaFree(d_seeds);
+  cudaFree(d_packed);
+  cudaFree(d_lab);
+  return FC_OK;
+}
+
 int32_t fc_set_profiling(fc_ctx* c, int32_t on) {
   if (c == nullptr) return set_err(FC_EINVAL, "null context");
   if (!on && c->prof_on) {

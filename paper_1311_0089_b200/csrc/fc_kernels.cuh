@@ -969,3 +969,48 @@ __global__ void k_fin_matrix(const double* part, int nslot, int nval, double inv
 }
 
 }  // namespace fc
+
+namespace fc {
+
+// ---------------------------------------------------------------------------
+// Device generators (SURVEY 8(d) contracts; the host generators in
+// generators.py are the bit-exact references on small grids).
+
+// cfg4: nearest seed under the periodic minimum image, voxel centres at the
+// integer slot indices; squared distance accumulated axis 0, 1, 2 with
+// round-to-nearest ops (no FMA) and strict "<" so the first seed wins ties,
+// exactly as generators.voronoi_labels.  Writes the packed tensor of the grain.
+__global__ void k_gen_voronoi(int n0, int n1, int n2, int G, const double* __restrict__ seeds,
+                              const double* __restrict__ packed, int nsym, int64_t N, double* __restrict__ A,
+                              int* __restrict__ labels) {
+  extern __shared__ double sseeds[];
+  for (int i = threadIdx.x; i < 3 * G; i += blockDim.x) sseeds[i] = seeds[i];
+  __syncthreads();
+  const double L0 = n0, L1 = n1, L2 = n2;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < N; v += (int64_t)gridDim.x * blockDim.x) {
+    const int i2 = (int)(v % n2);
+    const int64_t t = v / n2;
+    const int i1 = (int)(t % n1);
+    const int i0 = (int)(t / n1);
+    const double p0 = i0, p1 = i1, p2 = i2;
+    double best = INFINITY;
+    int lab = 0;
+    for (int g = 0; g < G; ++g) {
+      double a0 = fabs(__dsub_rn(p0, sseeds[3 * g + 0]));
+      a0 = fmin(a0, __dsub_rn(L0, a0));
+      double a1 = fabs(__dsub_rn(p1, sseeds[3 * g + 1]));
+      a1 = fmin(a1, __dsub_rn(L1, a1));
+      double a2 = fabs(__dsub_rn(p2, sseeds[3 * g + 2]));
+      a2 = fmin(a2, __dsub_rn(L2, a2));
+      double d2 = __dadd_rn(__dadd_rn(__dadd_rn(0.0, __dmul_rn(a0, a0)), __dmul_rn(a1, a1)), __dmul_rn(a2, a2));
+      if (d2 < best) {
+        best = d2;
+        lab = g;
+      }
+    }
+    for (int c = 0; c < nsym; ++c) A[(int64_t)c * N + v] = packed[(int64_t)lab * nsym + c];
+    if (labels) labels[v] = lab;
+  }
+}
+
+}  // namespace fc

@@ -327,3 +327,22 @@ def test_cfg3_full_size():
     assert abs(en[0, 0] - float(g["cg_energy"])) <= AH_TOL * abs(float(g["cg_energy"]))
     if "fp_iterations" in g:
         check_report(solve_neumann(a, load, SolverConfig(method="neumann", tol=1e-6, max_iter=2000)), g, "fp_")
+
+
+def test_device_voronoi_generator_matches_host():
+    """fc_generate_voronoi == generators.voronoi_labels bit for bit, and the poly27
+    golden solve is reproduced from the device-generated field."""
+    from paper_1311_0089_b200 import _native
+
+    for n in (27, 45):
+        seeds, packed = gen.cfg4_grains(512, gen.SEEDS["cfg4"], n)
+        ctx = _native.Context(GridSpec((1.0,) * 3, (n,) * 3))
+        labels = ctx.generate_voronoi(seeds, packed, want_labels=True)
+        assert np.array_equal(labels, gen.voronoi_labels(n, seeds))
+    g = golden("poly27")
+    seeds, packed = gen.cfg4_grains(512, gen.SEEDS["cfg4"], 27)
+    ctx = _native.Context(GridSpec((1.0,) * 3, (27,) * 3))
+    ctx.generate_voronoi(seeds, packed)
+    outs, x, _ = ctx.solve_cg(np.array([[1.0, 0.0, 0.0]]), 1e-8, 2000)
+    assert outs[0]["iterations"] == int(g["cg_iterations"])
+    assert rel_l2(x[0], g["cg_solution"]) <= max(SOL_TOL, 10 * float(g["cg_floor"]))
