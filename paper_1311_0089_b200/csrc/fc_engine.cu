@@ -170,6 +170,8 @@ struct fc_ctx {
   const double2* rtw(int L) const { return plans.at(L).rtw; }
   // register-path tiling per sweep (0 = generic path)
   int row_npen = 0, mid_bp = 0, outer_qb = 0, inv_prefetch = 1;
+  int aniso_npen = 0;       // all-components first sweep for packed coefficients (0 = off)
+  size_t smem_aniso_r = 0;
   size_t smem_row_r = 0, smem_row_inv_r = 0, smem_mid_r = 0, smem_outer_r = 0;
 };
 
@@ -340,7 +342,21 @@ int choose_tiles(fc_ctx* c) {
     c->smem_row_r = (size_t)48 * npen * rg.nl;
     c->inv_prefetch = env_int("FC_INV_PREFETCH", 0);
     c->smem_row_inv_r = (size_t)16 * npen * (rg.nl + 1) + (c->inv_prefetch ? (size_t)16 * npen * rg.nl : 0);
-  }
+    // packed coefficients: one CTA per row block for all components (its own
+    // row-block size: the c inputs, c old directions and nsym tensor entries of
+    // 2 npen rows are staged in shared memory)
+    {
+      const size_t arrays = (size_t)(2 * d + d * (d + 1) / 2);
+      const size_t per_pen = arrays * 2 * rg.nl * 8;
+      const size_t cap = (size_t)env_int("FC_ANISO_SMEM_KB", 160) * 1024;
+      int na = (int)std::min<size_t>(cap / per_pen, (size_t)(kMaxBlock / (d * (rg.nl / 9))));
+      na = std::min(na, (rg.np + 1) / 2);
+      if (env_int("FC_ANISO_ROWS", 1) && na >= 1) {
+        c->aniso_npen = na;
+        c->smem_aniso_r = std::max(per_pen * na, (size_t)16 * d * na * rg.nl);
+      }
+    }
+    }
   if (d == 3 && is_pow3_reg(c->n[1])) {
     MidGeo& mg = c->mg;
     const int TP = c->n[1] / 9;
@@ -382,6 +398,7 @@ int allow_reg_smem(int mx) {
   for (int L : {9, 27, 81, 243, 729, 2187}) {
     FC_POW3_SWITCH(L, {
       al(k_row_fwd_r<LL>);
+      al(k_row_fwd_aniso_r<LL>);
       al(k_row_inv_r<LL>);
       al(k_mid_r<LL, false>);
       al(k_mid_r<LL, true>);
@@ -456,7 +473,18 @@ int run_operator(fc_ctx* c, int R, const InArgs& ia, EpArgs ea, int orth, const 
   const RowGeo rg = c->rg;
   const int64_t nrow_blocks = (int64_t)R * rg.no * rg.ntiles * d;
   double2* Wrow = d == 3 ? c->W1 : c->W2;
-  if (c->row_npen) {
+  if (c->aniso_npen && C.kind == 1) {
+    const int nt = d * c->aniso_npen * (rg.nl / 9);
+    const double2* tw = c->rtw(rg.nl);
+    RowGeo ra = rg;
+    ra.B = 2 * c->aniso_npen;
+    ra.ntiles = (rg.np + ra.B - 1) / ra.B;
+    const int64_t nb = (int64_t)R * ra.no * ra.ntiles;
+    const int np_ = c->aniso_npen;
+    TRY(launch(c, "row_fwd", [&] {
+      FC_POW3_SWITCH(rg.nl, (k_row_fwd_aniso_r<LL><<<(unsigned)nb, nt, c->smem_aniso_r, s>>>(g, ra, C, ia, st, tw, Wrow, np_)));
+    }));
+  } else if (c->row_npen) {
     const int nt = c->row_npen * (rg.nl / 9);
     const double2* tw = c->rtw(rg.nl);
     TRY(launch(c, "row_fwd", [&] {

@@ -366,3 +366,119 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
 }
 
 }  // namespace fc
+
+namespace fc {
+
+// First sweep for packed (anisotropic) coefficients: one CTA owns a row block
+// for ALL c components (thread groups per component), so r, p_old (or e / u)
+// and the packed tensor are staged once per voxel with cp.async instead of
+// being re-read by c per-component CTAs.  Thread (a, p, j): component a,
+// pencil p (rows 2p, 2p+1), FFT lane j.  Staging layout (doubles):
+//   U[b][row][i]  (b < c)   PO[b][row][i] (b < c, IN_PNEW)   A[m][row][i] (m < nsym)
+template <int L>
+__global__ void __launch_bounds__(kMaxBlock, 1) k_row_fwd_aniso_r(Geo g, RowGeo rg, Coef C, InArgs ia,
+                                                                  const RhsState* st, const double2* __restrict__ tw,
+                                                                  double2* __restrict__ W, int npen) {
+  constexpr int TP = R9<L>::TP;
+  extern __shared__ double2 sm[];
+  const int c = g.dim;
+  const int nsym = c * (c + 1) / 2;
+  int64_t bid = blockIdx.x;
+  const int tile = bid % rg.ntiles; bid /= rg.ntiles;
+  const int o = bid % rg.no;
+  const int r = (int)(bid / rg.no);
+  if (!rhs_active(st, r)) return;
+  const int row0 = tile * rg.B;
+  const int nrows = min(rg.B, rg.np - row0);
+  const int per_a = npen * TP;
+  const int a = threadIdx.x / per_a;
+  const int t = threadIdx.x - a * per_a;
+  const int p = t / TP;
+  const int j = t - p * TP;
+  const InEval ev = make_eval(ia, g, C, st, r, a);
+  const int mode = ev.mode;
+  const bool use_u = mode != IN_CONST;
+  const bool use_p = mode == IN_PNEW && !ev.first;
+  const bool use_a = mode != IN_RAW;
+  const int blk = rg.B * L;  // doubles per staged array
+  double* S = reinterpret_cast<double*>(sm);
+  double* SU = S;
+  double* SP = SU + (use_u ? c * blk : 0);
+  double* SA = SP + (use_p ? c * blk : 0);
+  const int n = nrows * L;
+  const int64_t vbase = ((int64_t)o * rg.np + row0) * L;
+  const int64_t rbase = (int64_t)r * c * g.N;
+  for (int b = 0; b < c; ++b) {
+    if (use_u) stage_doubles(SU + b * blk, ia.u + rbase + (int64_t)b * g.N + vbase, n);
+    if (use_p) stage_doubles(SP + b * blk, ia.p_old + rbase + (int64_t)b * g.N + vbase, n);
+  }
+  if (use_a)
+    for (int m = 0; m < nsym; ++m) stage_doubles(SA + m * blk, C.A + (int64_t)m * g.N + vbase, n);
+  cp_async_wait_all();
+  __syncthreads();
+  double2 v[1][9];
+  double2 pn[9];
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+    const int i = j + s * TP;
+    double y[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = 2 * p + h;
+      if (row >= nrows) continue;
+      const int e = row * L + i;
+      double acc = 0.0;
+      for (int b = 0; b < c; ++b) {
+        double x;
+        if (mode == IN_CONST) {
+          x = InEval::sel(b, ev.E0, ev.E1, ev.E2);
+        } else {
+          x = SU[b * blk + e];
+          if (mode == IN_PNEW && !ev.first) x = __dadd_rn(x, __dmul_rn(ev.beta, SP[b * blk + e]));
+        }
+        if (mode == IN_PNEW && b == a) q[h] = x;
+        if (mode == IN_RAW) {
+          if (b == a) acc = x;
+          continue;
+        }
+        double Aab = SA[pidx(c, a, b) * blk + e];
+        if (mode == IN_FP) Aab = __dsub_rn(Aab, InEval::sel(b, ev.R0, ev.R1, ev.R2));
+        acc = __dadd_rn(acc, __dmul_rn(Aab, x));
+      }
+      if (mode != IN_FP && ev.s != 1.0) acc = __dmul_rn(ev.s, acc);
+      y[h] = acc;
+    }
+    v[0][s] = make_double2(y[0], y[1]);
+    pn[s] = make_double2(q[0], q[1]);
+  }
+  if (mode == IN_PNEW) {
+    double* pw = ia.p_new + rbase + (int64_t)a * g.N + vbase;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) {
+      if (2 * p < nrows) pw[(int64_t)(2 * p) * L + j + s * TP] = pn[s].x;
+      if (2 * p + 1 < nrows) pw[(int64_t)(2 * p + 1) * L + j + s * TP] = pn[s].y;
+    }
+  }
+  double2* smp = sm + (size_t)(a * npen + p) * L;
+  fft_reg<L, 1, false>(v, smp, L, j, tw);
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 9; ++s) smp[j + s * TP] = v[0][s];
+  __syncthreads();
+  constexpr int hl = (L + 1) / 2;
+  const int per_comp = hl * nrows;
+  for (int idx = threadIdx.x; idx < c * per_comp; idx += blockDim.x) {
+    const int aa = idx / per_comp;
+    const int rem = idx - aa * per_comp;
+    const int k = rem / nrows, row = rem - k * nrows;
+    const double2* z = sm + (size_t)(aa * npen + (row >> 1)) * L;
+    const double2 zk = z[k];
+    const double2 zm = z[k == 0 ? 0 : L - k];
+    double2 y;
+    if ((row & 1) == 0) y = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    else y = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+    W[((int64_t)(r * c + aa) * rg.no + o) * hl * rg.np + row0 + (int64_t)k * rg.np + row] = y;
+  }
+}
+
+}  // namespace fc
