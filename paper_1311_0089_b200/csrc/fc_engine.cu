@@ -171,6 +171,7 @@ struct fc_ctx {
   // register-path tiling per sweep (0 = generic path)
   int row_npen = 0, mid_bp = 0, outer_qb = 0, inv_prefetch = 1;
   int aniso_npen = 0;       // all-components first sweep for packed coefficients (0 = off)
+  int aniso_split = 1;      // packed coefficients: pointwise kernel + staged row FFT
   size_t smem_aniso_r = 0;
   size_t smem_row_r = 0, smem_row_inv_r = 0, smem_mid_r = 0, smem_outer_r = 0;
 };
@@ -332,7 +333,7 @@ int choose_tiles(fc_ctx* c) {
   if (c->force_generic) return FC_OK;
   if (is_pow3_reg(rg.nl)) {
     const int TP = rg.nl / 9;
-    int npen = std::max(1, std::min(16, std::min(env_int("FC_ROW_THREADS", 256), kMaxBlock) / TP));
+    int npen = std::max(1, std::min(16, std::min(env_int("FC_ROW_THREADS", 256), 256) / TP));
     npen = std::min(npen, (rg.np + 1) / 2);
     rg.B = 2 * npen;
     rg.ntiles = (rg.np + rg.B - 1) / rg.B;
@@ -342,6 +343,7 @@ int choose_tiles(fc_ctx* c) {
     c->smem_row_r = (size_t)48 * npen * rg.nl;
     c->inv_prefetch = env_int("FC_INV_PREFETCH", 0);
     c->smem_row_inv_r = (size_t)16 * npen * (rg.nl + 1) + (c->inv_prefetch ? (size_t)16 * npen * rg.nl : 0);
+    c->aniso_split = env_int("FC_ANISO_SPLIT", 1);
     // packed coefficients: one CTA per row block for all components (its own
     // row-block size: the c inputs, c old directions and nsym tensor entries of
     // 2 npen rows are staged in shared memory)
@@ -473,7 +475,22 @@ int run_operator(fc_ctx* c, int R, const InArgs& ia, EpArgs ea, int orth, const 
   const RowGeo rg = c->rg;
   const int64_t nrow_blocks = (int64_t)R * rg.no * rg.ntiles * d;
   double2* Wrow = d == 3 ? c->W1 : c->W2;
-  if (c->aniso_npen && C.kind == 1) {
+  if (C.kind == 1 && c->aniso_split && c->row_npen && ia.mode != IN_RAW) {
+    // split variant: pointwise y = M(x) u (+ p') at streaming bandwidth, then the
+    // staged row FFT on y.  y lives in the Ap buffer (free until the last sweep).
+    double* y = c->Ap;
+    const int blocks = c->num_sms * 8;
+    TRY(launch(c, "pointwise", [&] { k_pointwise_aniso<<<blocks, 256, 0, s>>>(g, C, ia, st, R, y); }));
+    InArgs raw{};
+    raw.mode = IN_RAW;
+    raw.s = 1.0;
+    raw.u = y;
+    const int nt = c->row_npen * (rg.nl / 9);
+    const double2* tw = c->rtw(rg.nl);
+    TRY(launch(c, "row_fwd", [&] {
+      FC_POW3_SWITCH(rg.nl, (k_row_fwd_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, C, raw, st, tw, Wrow)));
+    }));
+  } else if (c->aniso_npen && C.kind == 1) {
     const int nt = d * c->aniso_npen * (rg.nl / 9);
     const double2* tw = c->rtw(rg.nl);
     RowGeo ra = rg;
@@ -819,7 +836,7 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
       for (int a = 0; a < d; ++a) ia.E[r][a] = E[r * d + a];
     EpArgs ea{};
     ea.mode = EP_RHS;
-    ea.out = init != nullptr ? c->Ap : c->r;
+    ea.out = init != nullptr ? c->p[1] : c->r;  // Ap is the split first sweep's scratch
     ea.part = c->part;
     ea.fin = fin_args(c, FIN_INIT, R, nrow, tol, max_iter, init != nullptr);
     TRY(run_operator(c, R, ia, ea, orth, M, nullptr));
@@ -837,7 +854,7 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
     dim3 grid(nvec, R);
     FinArgs f = fin_args(c, FIN_INIT2, R, nvec, tol, max_iter);
     TRY(launch(c, "sub_dot", [&] {
-      k_sub_dot<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->Ap, c->p[0], c->r, c->part, nvec, f);
+      k_sub_dot<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->p[1], c->p[0], c->r, c->part, nvec, f);
     }));
   }
   std::vector<RhsState> hs(R);

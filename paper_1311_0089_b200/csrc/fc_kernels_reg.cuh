@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kMaxBlock) k_row_fwd_r(Geo g, RowGeo rg, Coef 
   // off-diagonal entries (then (A - A0) e is diagonal, solver.py:253-255)
   const bool fp_diag = ev.mode != IN_FP ||
                        ((a == 0 || ev.R0 == 0.0) && (a == 1 || ev.R1 == 0.0) && (a == 2 || ev.R2 == 0.0));
-  if (ev.kind == 0 && ev.mode != IN_CONST && fp_diag) {
+  if ((ev.kind == 0 || ev.mode == IN_RAW) && ev.mode != IN_CONST && fp_diag) {
     // isotropic: stage u (r / e / field), p_old and A for the whole row block in
     // smem with cp.async, then evaluate from smem (the staging area is reused as
     // the FFT exchange buffer afterwards)
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kMaxBlock) k_row_fwd_r(Geo g, RowGeo rg, Coef 
 // Last sweep: transposed half-spectrum load into smem, two-for-one assembly
 // straight into registers, inverse FFT, epilogue from registers (coalesced).
 template <int L>
-__global__ void __launch_bounds__(kMaxBlock, 1) k_row_inv_r(Geo g, RowGeo rg, EpArgs ea, const RhsState* st,
+__global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs ea, const RhsState* st,
                                                           const double2* __restrict__ tw,
                                                           const double2* __restrict__ W, int prefetch) {
   constexpr int TP = R9<L>::TP;
