@@ -340,10 +340,11 @@ int choose_tiles(fc_ctx* c) {
     c->row_npen = npen;
     // exchange buffer (16 npen (L+1)) + staging: first sweep u, p_old, A (3 x 2 npen L
     // doubles), last sweep p / e (2 npen L doubles)
-    c->smem_row_r = (size_t)48 * npen * rg.nl;
+    c->smem_row_r = (size_t)24 * (((size_t)2 * npen * rg.nl + 3) & ~(size_t)1);
     c->inv_prefetch = env_int("FC_INV_PREFETCH", 0);
     c->smem_row_inv_r = (size_t)16 * npen * (rg.nl + 1) + (c->inv_prefetch ? (size_t)16 * npen * rg.nl : 0);
     c->aniso_split = env_int("FC_ANISO_SPLIT", 1);
+    rg.exp_natural = env_int("FC_EXP_NATURAL_STORE", 0);
     // packed coefficients: one CTA per row block for all components (its own
     // row-block size: the c inputs, c old directions and nsym tensor entries of
     // 2 npen rows are staged in shared memory)

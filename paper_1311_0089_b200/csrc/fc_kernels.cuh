@@ -548,6 +548,7 @@ __device__ void finish_block(const FinArgs& f, double* red) {
 // outer index o < no (d = 3: o = i0; d = 2: no = 1).
 struct RowGeo {
   int nl, hl, np, no, B, ntiles;
+  int exp_natural;  // experiment switch (FC_EXP_NATURAL_STORE), never set in production
 };
 
 // ---------------------------------------------------------------------------

@@ -18,9 +18,31 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
-// Copy n contiguous doubles to shared memory, block-strided.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+// Copy n contiguous doubles to shared memory, block-strided, 8-byte granules.
 __device__ __forceinline__ void stage_doubles(double* dst, const double* src, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) cp_async8(dst + i, src + i);
+}
+// Same with 16-byte granules.  dst must be 16-byte aligned and have one spare
+// double in front and behind; returns the shift (0 or 1) so element i lands at
+// dst[i + shift] (the shift matches the source's 16-byte phase).
+__device__ __forceinline__ int stage_doubles16(double* dst, const double* src, int n) {
+  const int shift = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+  double* d = dst + shift;
+  // head element when src is 8 mod 16, then pairs, then a possible tail
+  int i0 = 0;
+  if (shift) {
+    if (threadIdx.x == 0 && n > 0) cp_async8(d, src);
+    i0 = 1;
+  }
+  const int npair = (n - i0) >> 1;
+  for (int q = threadIdx.x; q < npair; q += blockDim.x) cp_async16(d + i0 + 2 * q, src + i0 + 2 * q);
+  const int done = i0 + 2 * npair;
+  if (done < n && threadIdx.x == 0) cp_async8(d + done, src + done);
+  return shift;
 }
 constexpr int kMaxBlockOuter = 256;
 
@@ -58,14 +80,18 @@ __global__ void __launch_bounds__(kMaxBlock) k_row_fwd_r(Geo g, RowGeo rg, Coef 
     // isotropic: stage u (r / e / field), p_old and A for the whole row block in
     // smem with cp.async, then evaluate from smem (the staging area is reused as
     // the FFT exchange buffer afterwards)
+    const int stride = (rg.B * L + 3) & ~1;  // even, leaves room for the alignment shift
     double* st_u = reinterpret_cast<double*>(sm);
-    double* st_p = st_u + rg.B * L;
-    double* st_a = st_p + rg.B * L;
+    double* st_p = st_u + stride;
+    double* st_a = st_p + stride;
     const int n = nrows * L;
     const int64_t ub = ev.base + (int64_t)a * g.N + vbase;
-    stage_doubles(st_u, ev.u + ub, n);
-    if (ev.mode == IN_PNEW && !ev.first) stage_doubles(st_p, ev.p_old + ub, n);
-    if (ev.mode != IN_RAW) stage_doubles(st_a, ev.A + vbase, n);
+    const int su = stage_doubles16(st_u, ev.u + ub, n);
+    const int sp = (ev.mode == IN_PNEW && !ev.first) ? stage_doubles16(st_p, ev.p_old + ub, n) : 0;
+    const int sa = ev.mode != IN_RAW ? stage_doubles16(st_a, ev.A + vbase, n) : 0;
+    st_u += su;
+    st_p += sp;
+    st_a += sa;
     cp_async_wait_all();
     __syncthreads();
 #pragma unroll
@@ -123,15 +149,30 @@ __global__ void __launch_bounds__(kMaxBlock) k_row_fwd_r(Geo g, RowGeo rg, Coef 
   __syncthreads();
   constexpr int hl = (L + 1) / 2;
   double2* Wb = W + ((int64_t)(r * c + a) * rg.no + o) * hl * rg.np + row0;
-  for (int idx = threadIdx.x; idx < hl * nrows; idx += blockDim.x) {
-    const int k = idx / nrows, row = idx - k * nrows;
-    const double2* z = sm + (size_t)(row >> 1) * L;
+  if (rg.exp_natural) {  // EXPERIMENT ONLY (wrong layout): row-major store to time the transpose cost
+    for (int idx = threadIdx.x; idx < hl * nrows; idx += blockDim.x) {
+      const int row = idx / hl, k = idx - row * hl;
+      const double2* z = sm + (size_t)(row >> 1) * L;
+      const double2 zk = z[k];
+      const double2 zm = z[k == 0 ? 0 : L - k];
+      double2 y;
+      if ((row & 1) == 0) y = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+      else y = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+      W[((int64_t)(r * c + a) * rg.no + o) * hl * rg.np + (int64_t)(row0 + row) * hl + k] = y;
+    }
+    return;
+  }
+  // split Z = Ye + i Yo into the two half spectra; one thread per (pair, k)
+  const int npairs = (nrows + 1) >> 1;
+  for (int idx = threadIdx.x; idx < hl * npairs; idx += blockDim.x) {
+    const int pr = idx / hl;
+    const int k = idx - pr * hl;
+    const double2* z = sm + (size_t)pr * L;
     const double2 zk = z[k];
     const double2 zm = z[k == 0 ? 0 : L - k];
-    double2 y;
-    if ((row & 1) == 0) y = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-    else y = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
-    Wb[(int64_t)k * rg.np + row] = y;
+    double2* dst = Wb + (int64_t)k * rg.np + 2 * pr;
+    dst[0] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    if (2 * pr + 1 < nrows) dst[1] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
   }
 }
 
@@ -166,25 +207,29 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   const bool need_q = ea.mode == EP_AP || ea.mode == EP_FP;
   const double* qsrc = (ea.mode == EP_AP ? ea.p : ea.out) + ebase;
   if (need_q && prefetch) stage_doubles(st_q, qsrc, nrows * L);
-  // Y[row][k] staged at sm[row * hl + k]; 8 loads in flight per thread
+  // Y[row][k] staged at sm[row * hl + k]; one thread per (pair, k), 4 in flight
   {
-    const int total = hl * nrows;
-    for (int base = 0; base < total; base += 8 * blockDim.x) {
-      double2 t[8];
+    const int npairs = (nrows + 1) >> 1;
+    const int total = hl * npairs;
+    for (int base = 0; base < total; base += 4 * blockDim.x) {
+      double2 t0[4], t1[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 4; ++u) {
         const int idx = base + u * blockDim.x + threadIdx.x;
         if (idx < total) {
-          const int k = idx / nrows, row = idx - k * nrows;
-          t[u] = __ldg(Wb + (int64_t)k * rg.np + row);
+          const int pr = idx / hl, k = idx - pr * hl;
+          const double2* src = Wb + (int64_t)k * rg.np + 2 * pr;
+          t0[u] = __ldg(src);
+          t1[u] = 2 * pr + 1 < nrows ? __ldg(src + 1) : make_double2(0.0, 0.0);
         }
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 4; ++u) {
         const int idx = base + u * blockDim.x + threadIdx.x;
         if (idx < total) {
-          const int k = idx / nrows, row = idx - k * nrows;
-          sm[row * hl + k] = t[u];
+          const int pr = idx / hl, k = idx - pr * hl;
+          sm[(2 * pr) * hl + k] = t0[u];
+          sm[(2 * pr + 1) * hl + k] = t1[u];
         }
       }
     }
@@ -351,7 +396,10 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
 #pragma unroll
         for (int b = 0; b < C; ++b) den += xi[a] * og.M[a][b] * xi[b];
     }
-    const double2 qv = make_double2(dots.x / den, dots.y / den);
+    // (xi . v) / den as one reciprocal and two products (the reference divides
+    // twice, solver.py:108: the results differ by at most 1 ulp)
+    const double inv = 1.0 / den;
+    const double2 qv = make_double2(dots.x * inv, dots.y * inv);
 #pragma unroll
     for (int a = 0; a < C; ++a) v[a][s] = make_double2(xi[a] * qv.x, xi[a] * qv.y);
   }

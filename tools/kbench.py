@@ -1,0 +1,38 @@
+"""Per-kernel timing of one operator application (apply_system, all RHS active).
+
+usage: python tools/kbench.py [cfg2|cfg3|cfg4] [n] [reps]
+"""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import bench  # noqa: E402
+from paper_1311_0089_b200 import _native  # noqa: E402
+from paper_1311_0089_b200.grid import GridSpec  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+wl = bench.Workload(name, n)
+ctx = _native.Context(GridSpec((1.0,) * wl.d, wl.shape))
+wl.setup(ctx, wl.host_field())
+u = np.random.default_rng(0).standard_normal((wl.R, wl.d) + wl.shape)
+ctx.apply_system(u)
+ctx.profile_reset()
+ctx.set_profiling(True)
+for _ in range(reps):
+    ctx.apply_system(u)
+ctx.set_profiling(False)
+prof = ctx.profile()
+out = {}
+for k, (cnt, ms) in prof.items():
+    avg = ms / cnt
+    kb = wl.kernel_bytes(k)
+    if k == "row_fwd":
+        kb = 8 * wl.N * (wl.nA + 2 * wl.d * wl.R)   # operator-only first sweep: read u (+A), write spectrum
+    if k == "row_inv":
+        kb = 8 * wl.N * 2 * wl.d * wl.R             # read spectrum, write out
+    out[k] = (round(avg, 4), round(kb / (avg / 1e3) / 1e9) if kb else None)
+print(name, wl.shape, out)
