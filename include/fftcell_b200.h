@@ -70,6 +70,15 @@ int32_t fc_create(fc_ctx** out, int32_t dim, const int64_t* shape, const double*
                   int32_t device);
 void fc_destroy(fc_ctx* ctx);
 
+/* Slab-decomposed context: axis 0 split into nslabs (<= 8) uneven
+ * slabs, slab t on devices[t] (devices may repeat: several slabs on one GPU
+ * emulate ranks).  Every entry point below accepts it transparently: host
+ * arrays keep the full-grid layout, the library scatters / gathers slabs and
+ * runs two axis-0 exchanges (peer copies over NVLink) per operator
+ * application.  d = 3 with power-of-three axes (9 .. 2187). */
+int32_t fc_create_sharded(fc_ctx** out, int32_t dim, const int64_t* shape, const double* half_periods,
+                          int32_t nslabs, const int32_t* devices);
+
 /* CoefficientField upload (material.py:90-158): count = N (isotropic) or nsym*N (packed). */
 int32_t fc_set_coefficients(fc_ctx* ctx, int32_t kind, const double* host, int64_t count);
 

@@ -42,6 +42,8 @@ SIGNATURES = [
     ("fc_device_count", ctypes.c_int32, [ctypes.POINTER(ctypes.c_int32)]),
     ("fc_create", ctypes.c_int32,
      [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, _i64p, _dp, ctypes.c_int32]),
+    ("fc_create_sharded", ctypes.c_int32,
+     [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, _i64p, _dp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]),
     ("fc_destroy", None, [ctypes.c_void_p]),
     ("fc_set_coefficients", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, _dp, ctypes.c_int64]),
     ("fc_apply_A", ctypes.c_int32, [ctypes.c_void_p, _dp, _dp, ctypes.c_int32]),
@@ -115,7 +117,9 @@ def device_count():
 class Context:
     """One GridSpec bound to one GPU: coefficients, FFT plans and workspace in HBM."""
 
-    def __init__(self, spec, device_id: int = 0):
+    def __init__(self, spec, device_id: int = 0, slabs=None):
+        """``slabs``: None (one GPU) or a list of device ids, one per axis-0 slab
+        (SURVEY 8(e)); repeating a device emulates several ranks on it."""
         self.spec = spec
         self.device_id = device_id
         self.d = spec.dim
@@ -124,7 +128,13 @@ class Context:
         self._h = ctypes.c_void_p()
         shape = np.array(spec.shape, dtype=np.int64)
         Y = np.array(spec.half_periods, dtype=np.float64)
-        _check(lib().fc_create(ctypes.byref(self._h), spec.dim, shape.ctypes.data_as(_i64p), _ptr(Y), device_id))
+        if slabs is None:
+            _check(lib().fc_create(ctypes.byref(self._h), spec.dim, shape.ctypes.data_as(_i64p), _ptr(Y), device_id))
+        else:
+            dev = np.ascontiguousarray(slabs, dtype=np.int32)
+            _check(lib().fc_create_sharded(ctypes.byref(self._h), spec.dim, shape.ctypes.data_as(_i64p), _ptr(Y),
+                                           dev.size, dev.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
+        self.slabs = slabs
         self.isotropic = None
 
     def __del__(self):

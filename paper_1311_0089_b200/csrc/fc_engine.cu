@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <string>
 #include <vector>
@@ -161,7 +162,7 @@ struct fc_ctx {
     g.dim = dim;
     for (int a = 0; a < 3; ++a) g.n[a] = n[a];
     g.N = N;
-    g.invN = 1.0 / (double)N;
+    g.invN = 1.0 / (double)Ng;
     for (int a = 0; a < dim; ++a) g.xi[a] = xi + xi_off[a];
     return g;
   }
@@ -174,6 +175,42 @@ struct fc_ctx {
   int aniso_split = 1;      // packed coefficients: pointwise kernel + staged row FFT
   size_t smem_aniso_r = 0;
   size_t smem_row_r = 0, smem_row_inv_r = 0, smem_mid_r = 0, smem_outer_r = 0;
+
+  // slab decomposition along axis 0.  A plain context is the P = 1
+  // case.  A sharded context owns P slab contexts in `sub` (one per device; the
+  // same device may host several slabs, which emulates P ranks on one GPU).
+  int P = 1, me = 0;
+  int n0g = 0;             // global axis-0 length
+  int64_t Ng = 0;          // global voxel count
+  int s0[kMaxSlabs + 1] = {};  // axis-0 partition
+  int qs[kMaxSlabs + 1] = {};  // outer-pencil partition
+  double2* W2r = nullptr;  // received outer pencils (P > 1)
+  double* lsum = nullptr;  // slab-local reduction sums (2 x FC_MAX_RHS)
+  std::vector<fc_ctx*> sub;
+  cudaEvent_t sev[4] = {};  // phase events of this slab
+
+  SlabMap slabmap(int R) const {
+    SlabMap m{};
+    m.P = P;
+    m.me = me;
+    m.n0l = n[0];
+    for (int t = 0; t <= P; ++t) {
+      m.s0[t] = s0[t];
+      m.qs[t] = qs[t];
+    }
+    const int cdim = dim;
+    long long off = 0;
+    for (int t = 0; t < P; ++t) {  // send blocks: per destination t
+      m.doff[t] = off;
+      off += (long long)R * cdim * (qs[t + 1] - qs[t]) * n[0];
+    }
+    off = 0;
+    for (int t = 0; t < P; ++t) {  // receive segments: per source t
+      m.roff[t] = off;
+      off += (long long)R * cdim * (qs[me + 1] - qs[me]) * (s0[t + 1] - s0[t]);
+    }
+    return m;
+  }
 };
 
 namespace {
@@ -310,10 +347,10 @@ int choose_tiles(fc_ctx* c) {
   }
   {
     OuterGeo& og = c->og;
-    og.n0 = c->n[0];
+    og.n0 = c->n0g;
     og.n1 = d == 3 ? c->n[1] : 1;
     og.h_last = (c->n[d - 1] + 1) / 2;
-    og.Q = d == 3 ? og.h_last * c->n[1] : og.h_last;
+    og.Q = c->qs[c->me + 1] - c->qs[c->me];
     int best = 0;
     for (int QB = 32; QB >= 1; QB /= 2) {
       if (QB > og.Q && QB > 1) continue;
@@ -370,15 +407,15 @@ int choose_tiles(fc_ctx* c) {
     c->mid_bp = bp;
     c->smem_mid_r = (size_t)16 * bp * c->n[1];
   }
-  if (is_pow3_reg(c->n[0])) {
+  if (is_pow3_reg(c->n0g)) {
     OuterGeo& og = c->og;
-    const int TP = c->n[0] / 9;
+    const int TP = c->n0g / 9;
     int qb = std::max(1, std::min(32, std::min(env_int("FC_OUTER_THREADS", 256), kMaxBlockOuter) / TP));
     qb = std::min(qb, og.Q);
     og.QB = qb;
     og.nqb = (og.Q + qb - 1) / qb;
     c->outer_qb = qb;
-    c->smem_outer_r = (size_t)16 * d * qb * c->n[0];
+    c->smem_outer_r = (size_t)16 * d * qb * c->n0g;
   }
   return FC_OK;
 }
@@ -434,6 +471,12 @@ int ensure_workspace(fc_ctx* c, int R, int hcap) {
       int64_t spec = (int64_t)R * d * c->N / c->n[d - 1] * ((c->n[d - 1] + 1) / 2);
       CK(cudaMalloc(&c->W2, sizeof(double2) * spec));
       if (d == 3) CK(cudaMalloc(&c->W1, sizeof(double2) * spec));
+      if (c->P > 1) {
+        cudaFree(c->W2r);
+        c->W2r = nullptr;
+        const int64_t recv = (int64_t)R * d * (c->qs[c->me + 1] - c->qs[c->me]) * c->n0g;
+        CK(cudaMalloc(&c->W2r, sizeof(double2) * recv));
+      }
     }
     CK(cudaMalloc(&c->st, sizeof(RhsState) * R));
     c->Rcap = R;
@@ -461,13 +504,18 @@ int ensure_workspace(fc_ctx* c, int R, int hcap) {
 int64_t nslot_row(const fc_ctx* c) { return c->dim == 1 ? 1 : (int64_t)c->rg.no * c->rg.ntiles * c->dim; }
 int64_t nslot_vec(const fc_ctx* c) { return ((int64_t)c->dim * c->N + kVecTile - 1) / kVecTile; }
 
-// One operator application over R fields: first sweep (InArgs) ... last sweep (EpArgs).
-int run_operator(fc_ctx* c, int R, const InArgs& ia, EpArgs ea, int orth, const double M[3][3], const RhsState* st) {
+// One operator application over R fields, in three phases so a sharded run can
+// exchange spectra between them: 0 = first sweep (+ forward middle sweep),
+// 1 = outer sweep (Gamma_hat), 2 = inverse middle sweep + last sweep.
+enum Phase { PH_FWD = 1, PH_OUTER = 2, PH_INV = 4, PH_ALL = 7 };
+int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int orth, const double M[3][3],
+               const RhsState* st) {
   const Geo g = c->geo();
   const Coef C = c->coef();
   const int d = c->dim;
   cudaStream_t s = c->stream;
   if (ea.part != nullptr) ea.nslot = (int)nslot_row(c);
+  const SlabMap smap = c->slabmap(R);
   if (d == 1) {
     const FftPlan pl = c->plan(c->n[0]);
     const size_t sm = c->smem_line;
@@ -476,6 +524,26 @@ int run_operator(fc_ctx* c, int R, const InArgs& ia, EpArgs ea, int orth, const 
   const RowGeo rg = c->rg;
   const int64_t nrow_blocks = (int64_t)R * rg.no * rg.ntiles * d;
   double2* Wrow = d == 3 ? c->W1 : c->W2;
+  const MidGeo mg = c->mg;
+  const int64_t nmid = (int64_t)R * d * mg.h2 * mg.nib;
+  auto mid = [&](bool inv) -> int {
+    const double2* src = inv ? c->W2 : c->W1;
+    double2* dst = inv ? c->W1 : c->W2;
+    if (c->mid_bp) {
+      const int nt = c->mid_bp * (c->n[1] / 9);
+      const double2* tw = c->rtw(c->n[1]);
+      return launch(c, inv ? "mid_inv" : "mid_fwd", [&] {
+        if (inv) FC_POW3_SWITCH(c->n[1], (k_mid_r<LL, true><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, smap, st, tw, src, dst)))
+        else FC_POW3_SWITCH(c->n[1], (k_mid_r<LL, false><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, smap, st, tw, src, dst)))
+      });
+    }
+    const FftPlan pl1 = c->plan(c->n[1]);
+    return launch(c, inv ? "mid_inv" : "mid_fwd", [&] {
+      if (inv) k_mid<true><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, st, pl1, src, dst);
+      else k_mid<false><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, st, pl1, src, dst);
+    });
+  };
+  if (phases & PH_FWD) {
   if (C.kind == 1 && c->aniso_split && c->row_npen && ia.mode != IN_RAW) {
     // split variant: pointwise y = M(x) u (+ p') at streaming bandwidth, then the
     // staged row FFT on y.  y lives in the Ap buffer (free until the last sweep).
@@ -514,36 +582,20 @@ int run_operator(fc_ctx* c, int R, const InArgs& ia, EpArgs ea, int orth, const 
       k_row_fwd<<<(unsigned)nrow_blocks, kThreads, c->smem_row, s>>>(g, rg, C, ia, st, pl_last, Wrow);
     }));
   }
-  const MidGeo mg = c->mg;
-  const int64_t nmid = (int64_t)R * d * mg.h2 * mg.nib;
-  auto mid = [&](bool inv) -> int {
-    const double2* src = inv ? c->W2 : c->W1;
-    double2* dst = inv ? c->W1 : c->W2;
-    if (c->mid_bp) {
-      const int nt = c->mid_bp * (c->n[1] / 9);
-      const double2* tw = c->rtw(c->n[1]);
-      return launch(c, inv ? "mid_inv" : "mid_fwd", [&] {
-        if (inv) FC_POW3_SWITCH(c->n[1], (k_mid_r<LL, true><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, st, tw, src, dst)))
-        else FC_POW3_SWITCH(c->n[1], (k_mid_r<LL, false><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, st, tw, src, dst)))
-      });
-    }
-    const FftPlan pl1 = c->plan(c->n[1]);
-    return launch(c, inv ? "mid_inv" : "mid_fwd", [&] {
-      if (inv) k_mid<true><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, st, pl1, src, dst);
-      else k_mid<false><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, st, pl1, src, dst);
-    });
-  };
   if (d == 3) TRY(mid(false));
+  }
+  if (phases & PH_OUTER) {
   OuterGeo og = c->og;
   og.orth = orth;
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b) og.M[a][b] = M[a][b];
+  double2* Wout = c->P > 1 ? c->W2r : c->W2;
   if (c->outer_qb) {
-    const int nt = c->outer_qb * (c->n[0] / 9);
-    const double2* tw = c->rtw(c->n[0]);
+    const int nt = c->outer_qb * (c->n0g / 9);
+    const double2* tw = c->rtw(c->n0g);
     TRY(launch(c, "outer", [&] {
-      if (d == 2) FC_POW3_SWITCH(c->n[0], (k_outer_r<LL, 2><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, c->W2)))
-      else FC_POW3_SWITCH(c->n[0], (k_outer_r<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, c->W2)))
+      if (d == 2) FC_POW3_SWITCH(c->n0g, (k_outer_r<LL, 2><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, smap, st, tw, Wout)))
+      else FC_POW3_SWITCH(c->n0g, (k_outer_r<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, smap, st, tw, Wout)))
     }));
   } else {
     const FftPlan pl0 = c->plan(c->n[0]);
@@ -551,6 +603,8 @@ int run_operator(fc_ctx* c, int R, const InArgs& ia, EpArgs ea, int orth, const 
       k_outer<<<(unsigned)(R * og.nqb), kThreads, c->smem_outer, s>>>(g, og, st, pl0, c->W2);
     }));
   }
+  }
+  if (!(phases & PH_INV)) return FC_OK;
   if (d == 3) TRY(mid(true));
   if (c->row_npen) {
     const int nt = c->row_npen * (rg.nl / 9);
@@ -565,8 +619,16 @@ int run_operator(fc_ctx* c, int R, const InArgs& ia, EpArgs ea, int orth, const 
   });
 }
 
+int run_operator(fc_ctx* c, int R, const InArgs& ia, EpArgs ea, int orth, const double M[3][3], const RhsState* st) {
+  return run_phases(c, PH_ALL, R, ia, ea, orth, M, st);
+}
+
 int check_ctx(fc_ctx* c, bool need_coef) {
   if (c == nullptr) return set_err(FC_EINVAL, "null context");
+  if (!c->sub.empty()) {  // sharded parent: slabs carry the device state
+    if (need_coef && c->coef_kind < 0) return set_err(FC_EINVAL, "coefficients not set");
+    return FC_OK;
+  }
   if (need_coef && c->A == nullptr) return set_err(FC_EINVAL, "coefficients not set");
   CK(cudaSetDevice(c->device));
   return FC_OK;
@@ -615,6 +677,8 @@ FinArgs fin_args(fc_ctx* c, int mode, int R, int nslot, double tol, int max_iter
 
 }  // namespace
 
+#include "fc_shard.inc"
+
 // ===========================================================================
 // C ABI
 extern "C" {
@@ -633,28 +697,38 @@ int32_t fc_device_count(int32_t* count) {
   return FC_OK;
 }
 
-int32_t fc_create(fc_ctx** out, int32_t dim, const int64_t* shape, const double* half_periods, int32_t device) {
-  if (out == nullptr) return set_err(FC_EINVAL, "null output pointer");
+}  // extern "C"
+
+namespace {
+
+// One slab (or the whole grid when P = 1) on one device.  shape is GLOBAL; the
+// slab owns axis-0 planes [me n0 / P, (me + 1) n0 / P) and outer pencils
+// [me Q / P, (me + 1) Q / P).
+int create_slab(fc_ctx** out, int32_t dim, const int64_t* shape, const double* half_periods, int32_t device, int P,
+                int me) {
   *out = nullptr;
-  if (dim < 1 || dim > 3) return set_err(FC_ENOTSUP, "dimension %d not supported (1..3)", dim);
-  for (int a = 0; a < dim; ++a) {
-    if (shape[a] <= 0 || shape[a] % 2 == 0)
-      return set_err(FC_EINVAL, "grid shape must consist of positive odd integers");
-    if (!(half_periods[a] > 0)) return set_err(FC_EINVAL, "half_periods must be positive");
-    if (shape[a] > (1 << 20)) return set_err(FC_ENOTSUP, "axis length %lld too large", (long long)shape[a]);
-  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return set_err(FC_ECUDA, "no CUDA device available");
   if (device < 0 || device >= ndev) return set_err(FC_EINVAL, "device %d out of range (have %d)", device, ndev);
   fc_ctx* c = new fc_ctx();
   c->device = device;
   c->dim = dim;
-  c->N = 1;
+  c->P = P;
+  c->me = me;
+  c->n0g = (int)shape[0];
+  c->Ng = 1;
   for (int a = 0; a < dim; ++a) {
     c->n[a] = (int)shape[a];
     c->Y[a] = half_periods[a];
-    c->N *= shape[a];
+    c->Ng *= shape[a];
   }
+  const int Q = dim == 3 ? (int)(shape[1] * ((shape[2] + 1) / 2)) : (dim == 2 ? (int)((shape[1] + 1) / 2) : 1);
+  for (int t = 0; t <= P; ++t) {
+    c->s0[t] = (int)((int64_t)t * shape[0] / P);
+    c->qs[t] = (int)((int64_t)t * Q / P);
+  }
+  c->n[0] = c->s0[me + 1] - c->s0[me];
+  c->N = c->Ng / shape[0] * c->n[0];
   auto fail = [&](int rc) { fc_destroy(c); return rc; };
   if (cudaSetDevice(device) != cudaSuccess) return fail(set_err(FC_ECUDA, "cudaSetDevice(%d) failed", device));
   cudaDeviceProp prop;
@@ -665,23 +739,26 @@ int32_t fc_create(fc_ctx** out, int32_t dim, const int64_t* shape, const double*
   c->num_sms = prop.multiProcessorCount;
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(set_err(FC_ECUDA, "stream creation failed"));
-  for (int a = 0; a < dim; ++a) {
-    int rc = ensure_plan(c, c->n[a]);
-    if (rc) return fail(rc);
-  }
-  // per-axis frequency tables xi = k / Y (grid.py:131-146)
+  for (auto& e : c->sev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  int rc = ensure_plan(c, c->n0g);
+  for (int a = 1; a < dim && rc == FC_OK; ++a) rc = ensure_plan(c, c->n[a]);
+  if (rc) return fail(rc);
+  // per-axis frequency tables xi = k / Y (grid.py:131-146); axis 0 is global
   std::vector<double> xi;
   for (int a = 0; a < dim; ++a) {
     c->xi_off[a] = (int)xi.size();
-    for (int i = 0; i < c->n[a]; ++i) {
-      long long k = i <= (c->n[a] - 1) / 2 ? i : (long long)i - c->n[a];
+    const int na = a == 0 ? c->n0g : c->n[a];
+    for (int i = 0; i < na; ++i) {
+      long long k = i <= (na - 1) / 2 ? i : (long long)i - na;
       xi.push_back((double)k / c->Y[a]);
     }
   }
   if (cudaMalloc(&c->xi, sizeof(double) * xi.size()) != cudaSuccess) return fail(set_err(FC_ENOMEM, "xi alloc"));
   cudaMemcpy(c->xi, xi.data(), sizeof(double) * xi.size(), cudaMemcpyHostToDevice);
-  int rc = choose_tiles(c);
+  rc = choose_tiles(c);
   if (rc) return fail(rc);
+  if (P > 1 && (dim != 3 || !c->row_npen || !c->mid_bp || !c->outer_qb))
+    return fail(set_err(FC_ENOTSUP, "slab decomposition needs d = 3 and power-of-three axes (9..2187)"));
   const int mx = c->smem_optin;
   if ((rc = allow_smem(k_row_fwd, mx)) || (rc = allow_smem(k_row_inv, mx)) || (rc = allow_smem(k_mid<false>, mx)) ||
       (rc = allow_smem(k_mid<true>, mx)) || (rc = allow_smem(k_outer, mx)) || (rc = allow_smem(k_line, mx)) ||
@@ -690,6 +767,7 @@ int32_t fc_create(fc_ctx** out, int32_t dim, const int64_t* shape, const double*
   if (cudaMalloc(&c->any_active, sizeof(int)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "flag alloc"));
   if (cudaMalloc(&c->counter, sizeof(unsigned)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "counter alloc"));
   cudaMemset(c->counter, 0, sizeof(unsigned));
+  if (cudaMalloc(&c->lsum, sizeof(double) * 2 * FC_MAX_RHS) != cudaSuccess) return fail(set_err(FC_ENOMEM, "lsum alloc"));
   if (cudaMallocHost(&c->h_flag, 4 * sizeof(int)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "pinned alloc"));
   for (auto& e : c->flag_ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   if (cudaMalloc(&c->d_mat, sizeof(double) * FC_MAX_RHS * FC_MAX_RHS) != cudaSuccess)
@@ -698,8 +776,88 @@ int32_t fc_create(fc_ctx** out, int32_t dim, const int64_t* shape, const double*
   return FC_OK;
 }
 
+int check_shape(int32_t dim, const int64_t* shape, const double* half_periods) {
+  if (dim < 1 || dim > 3) return set_err(FC_ENOTSUP, "dimension %d not supported (1..3)", dim);
+  for (int a = 0; a < dim; ++a) {
+    if (shape[a] <= 0 || shape[a] % 2 == 0)
+      return set_err(FC_EINVAL, "grid shape must consist of positive odd integers");
+    if (!(half_periods[a] > 0)) return set_err(FC_EINVAL, "half_periods must be positive");
+    if (shape[a] > (1 << 20)) return set_err(FC_ENOTSUP, "axis length %lld too large", (long long)shape[a]);
+  }
+  return FC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t fc_create(fc_ctx** out, int32_t dim, const int64_t* shape, const double* half_periods, int32_t device) {
+  if (out == nullptr) return set_err(FC_EINVAL, "null output pointer");
+  *out = nullptr;
+  TRY(check_shape(dim, shape, half_periods));
+  return create_slab(out, dim, shape, half_periods, device, 1, 0);
+}
+
+int32_t fc_create_sharded(fc_ctx** out, int32_t dim, const int64_t* shape, const double* half_periods,
+                          int32_t nslabs, const int32_t* devices) {
+  if (out == nullptr) return set_err(FC_EINVAL, "null output pointer");
+  *out = nullptr;
+  TRY(check_shape(dim, shape, half_periods));
+  if (nslabs < 1 || nslabs > kMaxSlabs) return set_err(FC_EINVAL, "number of slabs must lie in [1, %d]", kMaxSlabs);
+  if (dim != 3) return set_err(FC_ENOTSUP, "slab decomposition is implemented for d = 3");
+  if (shape[0] < nslabs) return set_err(FC_EINVAL, "more slabs than axis-0 planes");
+  fc_ctx* c = new fc_ctx();
+  c->device = -1;  // parent: no device resources of its own
+  c->dim = dim;
+  c->P = nslabs;
+  c->n0g = (int)shape[0];
+  c->Ng = 1;
+  for (int a = 0; a < dim; ++a) {
+    c->n[a] = (int)shape[a];
+    c->Y[a] = half_periods[a];
+    c->Ng *= shape[a];
+  }
+  c->N = c->Ng;
+  for (int t = 0; t < nslabs; ++t) {
+    fc_ctx* sl = nullptr;
+    const int dev = devices ? devices[t] : 0;
+    int rc = create_slab(&sl, dim, shape, half_periods, dev, nslabs, t);
+    if (rc) {
+      fc_destroy(c);
+      return rc;
+    }
+    c->sub.push_back(sl);
+  }
+  // peer access between distinct devices (P2P loads of the slab sums, NVLink copies)
+  for (fc_ctx* a : c->sub)
+    for (fc_ctx* b : c->sub)
+      if (a->device != b->device) {
+        int ok = 0;
+        cudaDeviceCanAccessPeer(&ok, a->device, b->device);
+        if (!ok) {
+          fc_destroy(c);
+          return set_err(FC_ECUDA, "devices %d and %d cannot access each other", a->device, b->device);
+        }
+        cudaSetDevice(a->device);
+        cudaError_t e = cudaDeviceEnablePeerAccess(b->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+          fc_destroy(c);
+          return set_err(FC_ECUDA, "peer access %d -> %d: %s", a->device, b->device, cudaGetErrorString(e));
+        }
+        cudaGetLastError();
+      }
+  *out = c;
+  return FC_OK;
+}
+
 void fc_destroy(fc_ctx* c) {
   if (c == nullptr) return;
+  for (fc_ctx* sl : c->sub) fc_destroy(sl);
+  c->sub.clear();
+  if (c->device < 0) {  // sharded parent holds no device resources
+    delete c;
+    return;
+  }
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& kv : c->plans) {
@@ -712,6 +870,10 @@ void fc_destroy(fc_ctx* c) {
   cudaFree(c->st);
   cudaFree(c->any_active);
   cudaFree(c->counter);
+  cudaFree(c->lsum);
+  cudaFree(c->W2r);
+  for (auto& e : c->sev)
+    if (e) cudaEventDestroy(e);
   if (c->h_flag) cudaFreeHost(c->h_flag);
   for (auto& e : c->flag_ev)
     if (e) cudaEventDestroy(e);
@@ -727,6 +889,7 @@ void fc_destroy(fc_ctx* c) {
 }
 
 int32_t fc_set_coefficients(fc_ctx* c, int32_t kind, const double* host, int64_t count) {
+  if (c && !c->sub.empty()) return shard_set_coefficients(c, kind, host, count);
   TRY(check_ctx(c, false));
   const int d = c->dim;
   const int64_t nsym = (int64_t)d * (d + 1) / 2;
@@ -745,6 +908,10 @@ int32_t fc_set_coefficients(fc_ctx* c, int32_t kind, const double* host, int64_t
 }
 
 int32_t fc_apply_A(fc_ctx* c, const double* u, double* out, int32_t nf) {
+  if (c && !c->sub.empty()) {
+    TRY(check_R(nf));
+    return shard_field_op(c, 0, nullptr, u, out, nf);
+  }
   TRY(check_ctx(c, true));
   TRY(check_R(nf));
   TRY(ensure_workspace(c, nf, 2));
@@ -762,6 +929,7 @@ int32_t fc_project(fc_ctx* c, int32_t which, const double* ref, const double* u,
   TRY(check_R(nf));
   if (which != FC_PROJ_ORTHOGONAL && which != FC_PROJ_GAMMA_REF) return set_err(FC_EINVAL, "unknown projector %d", which);
   if (which == FC_PROJ_GAMMA_REF && ref == nullptr) return set_err(FC_EINVAL, "gamma_ref needs a reference matrix");
+  if (!c->sub.empty()) return shard_field_op(c, which == FC_PROJ_ORTHOGONAL ? 2 : 3, ref, u, out, nf);
   TRY(ensure_workspace(c, nf, 2));
   TRY(upload_fields(c, c->p[0], u, nf));
   InArgs ia{};
@@ -781,6 +949,10 @@ int32_t fc_project(fc_ctx* c, int32_t which, const double* ref, const double* u,
 }
 
 int32_t fc_apply_system(fc_ctx* c, const double* u, double* out, int32_t nf) {
+  if (c && !c->sub.empty()) {
+    TRY(check_R(nf));
+    return shard_field_op(c, 1, nullptr, u, out, nf);
+  }
   TRY(check_ctx(c, true));
   TRY(check_R(nf));
   TRY(ensure_workspace(c, nf, 2));
@@ -804,6 +976,11 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
   TRY(check_R(R));
   if (!(tol > 0 && tol < 1)) return set_err(FC_EINVAL, "tol must lie in (0, 1), got %g", tol);
   if (max_iter < 1) return set_err(FC_EINVAL, "max_iter must be positive");
+  if (!c->sub.empty()) {
+    if (iterates != nullptr) return set_err(FC_ENOTSUP, "record_iterates is not supported on a sharded context");
+    if (n_iterates) *n_iterates = 0;
+    return shard_solve_cg(c, R, E, tol, max_iter, lam, init, x_out, rep, hist);
+  }
   const int d = c->dim;
   TRY(ensure_workspace(c, R, max_iter + 1));
   cudaStream_t s = c->stream;
@@ -935,6 +1112,7 @@ int32_t fc_solve_fixed_point(fc_ctx* c, int32_t R, const double* E, double tol, 
   if (!(tol > 0 && tol < 1)) return set_err(FC_EINVAL, "tol must lie in (0, 1), got %g", tol);
   if (max_iter < 1) return set_err(FC_EINVAL, "max_iter must be positive");
   if (ref == nullptr || scale == nullptr) return set_err(FC_EINVAL, "reference matrix and scales are required");
+  if (!c->sub.empty()) return shard_solve_fp(c, R, E, tol, max_iter, ref, scale, x_out, rep, hist);
   const int d = c->dim;
   TRY(ensure_workspace(c, R, max_iter + 1));
   cudaStream_t s = c->stream;
@@ -1004,6 +1182,10 @@ int32_t fc_solve_fixed_point(fc_ctx* c, int32_t R, const double* E, double tol, 
 }
 
 int32_t fc_energy(fc_ctx* c, int32_t R, const double* E, const double* x, double* out) {
+  if (c && !c->sub.empty()) {
+    TRY(check_R(R));
+    return shard_energy(c, R, E, x, out);
+  }
   TRY(check_ctx(c, true));
   TRY(check_R(R));
   if (c->Rcap < R || c->x == nullptr) {
@@ -1027,6 +1209,12 @@ int32_t fc_energy(fc_ctx* c, int32_t R, const double* E, const double* x, double
 
 int32_t fc_generate_voronoi(fc_ctx* c, int32_t n_seeds, const double* seeds, const double* packed,
                             int32_t* labels_out) {
+  if (c && !c->sub.empty()) {
+    if (labels_out != nullptr) return set_err(FC_ENOTSUP, "labels are not gathered on a sharded context");
+    for (fc_ctx* sl : c->sub) TRY(fc_generate_voronoi(sl, n_seeds, seeds, packed, nullptr));
+    c->coef_kind = FC_COEF_PACKED;
+    return FC_OK;
+  }
   TRY(check_ctx(c, false));
   if (c->dim != 3) return set_err(FC_EINVAL, "the Voronoi generator is three-dimensional");
   if (n_seeds < 1 || n_seeds > 4096) return set_err(FC_EINVAL, "n_seeds must lie in [1, 4096]");
@@ -1050,8 +1238,8 @@ int32_t fc_generate_voronoi(fc_ctx* c, int32_t n_seeds, const double* seeds, con
   const size_t sm = sizeof(double) * 3 * n_seeds;
   CK(cudaFuncSetAttribute(k_gen_voronoi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   TRY(launch(c, "gen_voronoi", [&] {
-    k_gen_voronoi<<<blocks, 256, sm, c->stream>>>(c->n[0], c->n[1], c->n[2], n_seeds, d_seeds, d_packed, nsym, c->N,
-                                                  c->A, d_lab);
+    k_gen_voronoi<<<blocks, 256, sm, c->stream>>>(c->n0g, c->n[1], c->n[2], c->s0[c->me], n_seeds, d_seeds, d_packed,
+                                                  nsym, c->N, c->A, d_lab);
   }));
   if (labels_out) CK(cudaMemcpyAsync(labels_out, d_lab, sizeof(int) * c->N, cudaMemcpyDeviceToHost, c->stream));
   TRY(sync(c));
@@ -1063,6 +1251,10 @@ int32_t fc_generate_voronoi(fc_ctx* c, int32_t n_seeds, const double* seeds, con
 
 int32_t fc_set_profiling(fc_ctx* c, int32_t on) {
   if (c == nullptr) return set_err(FC_EINVAL, "null context");
+  if (!c->sub.empty()) {
+    for (fc_ctx* sl : c->sub) TRY(fc_set_profiling(sl, on));
+    return FC_OK;
+  }
   if (!on && c->prof_on) {
     cudaStreamSynchronize(c->stream);
     drain_profile(c);
@@ -1070,8 +1262,12 @@ int32_t fc_set_profiling(fc_ctx* c, int32_t on) {
   c->prof_on = on != 0;
   return FC_OK;
 }
-int32_t fc_profile_count(fc_ctx* c) { return c ? (int32_t)c->prof.size() : 0; }
+int32_t fc_profile_count(fc_ctx* c) {
+  if (c && !c->sub.empty()) return fc_profile_count(c->sub[0]);
+  return c ? (int32_t)c->prof.size() : 0;
+}
 int32_t fc_profile_get(fc_ctx* c, int32_t i, char* name, int32_t cap, int64_t* launches, double* ms) {
+  if (c && !c->sub.empty()) return fc_profile_get(c->sub[0], i, name, cap, launches, ms);
   if (c == nullptr || i < 0 || i >= (int)c->prof.size()) return set_err(FC_EINVAL, "bad profile index");
   std::snprintf(name, cap, "%s", c->prof[i].name.c_str());
   *launches = c->prof[i].launches;
@@ -1080,15 +1276,27 @@ int32_t fc_profile_get(fc_ctx* c, int32_t i, char* name, int32_t cap, int64_t* l
 }
 int32_t fc_profile_reset(fc_ctx* c) {
   if (c == nullptr) return set_err(FC_EINVAL, "null context");
+  if (!c->sub.empty()) {
+    for (fc_ctx* sl : c->sub) TRY(fc_profile_reset(sl));
+    return FC_OK;
+  }
   cudaStreamSynchronize(c->stream);
   drain_profile(c);
   c->prof.clear();
   c->prof_idx.clear();
   return FC_OK;
 }
-int64_t fc_launch_count(fc_ctx* c) { return c ? c->launches : 0; }
+int64_t fc_launch_count(fc_ctx* c) {
+  if (c && !c->sub.empty()) {
+    int64_t n = 0;
+    for (fc_ctx* sl : c->sub) n += sl->launches;
+    return n;
+  }
+  return c ? c->launches : 0;
+}
 
 int32_t fc_timer_mark(fc_ctx* c, int32_t slot) {
+  if (c && !c->sub.empty()) return fc_timer_mark(c->sub[0], slot);
   TRY(check_ctx(c, false));
   if (slot < 0 || slot >= 8) return set_err(FC_EINVAL, "timer slot %d out of range", slot);
   if (!c->timer_ev[slot]) CK(cudaEventCreate(&c->timer_ev[slot]));
@@ -1097,6 +1305,7 @@ int32_t fc_timer_mark(fc_ctx* c, int32_t slot) {
 }
 
 int32_t fc_timer_elapsed(fc_ctx* c, int32_t a, int32_t b, double* ms) {
+  if (c && !c->sub.empty()) return fc_timer_elapsed(c->sub[0], a, b, ms);
   TRY(check_ctx(c, false));
   if (a < 0 || a >= 8 || b < 0 || b >= 8 || !c->timer_ev[a] || !c->timer_ev[b])
     return set_err(FC_EINVAL, "timer slots not recorded");

@@ -56,6 +56,37 @@ struct Geo {
   const double* xi[3];  // xi[a][slot] = k(slot) / Y_a
 };
 
+// Slab decomposition along axis 0.  Each slab owns planes
+// [s0[me], s0[me+1]) of axis 0 and, for the outer sweep, the (k2, k1) pencils
+// q in [qs[me], qs[me+1]).  The middle sweep writes its spectrum in a
+// destination-blocked layout so the block for slab p is one contiguous chunk:
+//   send[doff[p] + ((r*c + a) * Q_p + (q - qs[p])) * n0l + i0_local]
+// and the outer sweep reads full axis-0 pencils from the received segments:
+//   recv[roff[p] + ((r*c + a) * Q_me + (q - qs[me])) * n0l(p) + (i0 - s0[p])].
+// P = 1 reduces both to the single-GPU layout W2[R][c][q][i0].
+constexpr int kMaxSlabs = 8;
+struct SlabMap {
+  int P, me, n0l;
+  int s0[kMaxSlabs + 1];
+  int qs[kMaxSlabs + 1];
+  long long doff[kMaxSlabs];
+  long long roff[kMaxSlabs];
+};
+
+__device__ __forceinline__ int slab_of(const int* bounds, int P, int x) {
+  int p = 0;
+#pragma unroll
+  for (int t = 1; t < kMaxSlabs; ++t)
+    if (t < P && x >= bounds[t]) p = t;
+  return p;
+}
+
+__device__ __forceinline__ int64_t send_index(const SlabMap& m, int rc, int q, int i0l) {
+  const int p = slab_of(m.qs, m.P, q);
+  const int Qp = m.qs[p + 1] - m.qs[p];
+  return m.doff[p] + ((int64_t)rc * Qp + (q - m.qs[p])) * m.n0l + i0l;
+}
+
 struct Coef {
   const double* A;   // iso: (N) ; packed: (nsym, N)
   int kind;          // 0 isotropic scalar, 1 packed symmetric
@@ -96,6 +127,7 @@ struct FinArgs {
   double invN;
   int* any_active;
   unsigned* counter;  // arrival counter, reset by the last CTA
+  double* lsum;       // slab-local mode: per-RHS sums go here, k_fin_global finishes
 };
 
 struct EpArgs {
@@ -532,15 +564,40 @@ __device__ void finish_block(const FinArgs& f, double* red) {
   for (int r = 0; r < f.R; ++r) {
     if (!init && !f.st[r].active) continue;
     const double sum = reduce_slots(f.part + (int64_t)r * f.nslot, f.nslot, red);
-    if (threadIdx.x == 0) fin_logic(f, r, sum);
+    if (threadIdx.x == 0) {
+      if (f.lsum) f.lsum[r] = sum;  // slab-local: the global finalize runs in k_fin_global
+      else fin_logic(f, r, sum);
+    }
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    int any = 0;
-    for (int r = 0; r < f.R; ++r) any |= f.st[r].active;
-    *f.any_active = any;
+    if (!f.lsum) {
+      int any = 0;
+      for (int r = 0; r < f.R; ++r) any |= f.st[r].active;
+      *f.any_active = any;
+    }
     *f.counter = 0u;
   }
+}
+
+// Sharded finalize: every slab sums the P slab-local sums in slab order (so all
+// slabs hold bit-identical scalars) and runs the same scalar logic.
+struct SlabSums {
+  const double* p[kMaxSlabs];
+  int P;
+};
+__global__ void k_fin_global(FinArgs f, SlabSums ss) {
+  if (threadIdx.x != 0) return;
+  const bool init = f.mode == FIN_INIT || f.mode == FIN_INIT2;
+  for (int r = 0; r < f.R; ++r) {
+    if (!init && !f.st[r].active) continue;
+    double sum = 0.0;
+    for (int q = 0; q < ss.P; ++q) sum += ss.p[q][r];
+    fin_logic(f, r, sum);
+  }
+  int any = 0;
+  for (int r = 0; r < f.R; ++r) any |= f.st[r].active;
+  *f.any_active = any;
 }
 
 // Row-sweep geometry: rows of length nl along the contiguous axis, grouped in
@@ -981,7 +1038,7 @@ namespace fc {
 // integer slot indices; squared distance accumulated axis 0, 1, 2 with
 // round-to-nearest ops (no FMA) and strict "<" so the first seed wins ties,
 // exactly as generators.voronoi_labels.  Writes the packed tensor of the grain.
-__global__ void k_gen_voronoi(int n0, int n1, int n2, int G, const double* __restrict__ seeds,
+__global__ void k_gen_voronoi(int n0, int n1, int n2, int i0_off, int G, const double* __restrict__ seeds,
                               const double* __restrict__ packed, int nsym, int64_t N, double* __restrict__ A,
                               int* __restrict__ labels) {
   extern __shared__ double sseeds[];
@@ -992,7 +1049,7 @@ __global__ void k_gen_voronoi(int n0, int n1, int n2, int G, const double* __res
     const int i2 = (int)(v % n2);
     const int64_t t = v / n2;
     const int i1 = (int)(t % n1);
-    const int i0 = (int)(t / n1);
+    const int i0 = (int)(t / n1) + i0_off;
     const double p0 = i0, p1 = i1, p2 = i2;
     double best = INFINITY;
     int lab = 0;

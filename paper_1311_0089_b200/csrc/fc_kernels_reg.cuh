@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
 // Middle sweep (d = 3), thread mapping pencil-fastest (t = j * BP + p) so the
 // transposed side is written / read in chunks of BP consecutive i0.
 template <int L, bool INV>
-__global__ void __launch_bounds__(kMaxBlock) k_mid_r(Geo g, MidGeo mg, const RhsState* st,
+__global__ void __launch_bounds__(kMaxBlock) k_mid_r(Geo g, MidGeo mg, SlabMap sm_, const RhsState* st,
                                                       const double2* __restrict__ tw,
                                                       const double2* __restrict__ src, double2* __restrict__ dst) {
   constexpr int TP = R9<L>::TP;
@@ -313,26 +313,25 @@ __global__ void __launch_bounds__(kMaxBlock) k_mid_r(Geo g, MidGeo mg, const Rhs
   const int p = threadIdx.x % BP;
   const int j = threadIdx.x / BP;
   const int i00 = ib * BP;
-  const bool live = i00 + p < mg.n0;
-  const int64_t rc = (int64_t)(r * c + a);
+  const bool live = i00 + p < mg.n0;   // mg.n0 = local planes of this slab
+  const int rc = r * c + a;
   double2 v[1][9];
   if (!INV) {
-    const double2* s0 = src + ((rc * mg.n0 + i00 + p) * mg.h2 + k2) * L;
+    const double2* s0 = src + (((int64_t)rc * mg.n0 + i00 + p) * mg.h2 + k2) * L;
 #pragma unroll
     for (int s = 0; s < 9; ++s) v[0][s] = live ? s0[j + s * TP] : make_double2(0.0, 0.0);
   } else {
-    const double2* s0 = src + (rc * mg.h2 + k2) * (int64_t)L * mg.n0 + i00 + p;
 #pragma unroll
-    for (int s = 0; s < 9; ++s) v[0][s] = live ? s0[(int64_t)(j + s * TP) * mg.n0] : make_double2(0.0, 0.0);
+    for (int s = 0; s < 9; ++s)
+      v[0][s] = live ? src[send_index(sm_, rc, k2 * L + j + s * TP, i00 + p)] : make_double2(0.0, 0.0);
   }
   fft_reg<L, 1, INV>(v, sm + (size_t)p * L, L, j, tw);
   if (!live) return;
   if (!INV) {
-    double2* d0 = dst + (rc * mg.h2 + k2) * (int64_t)L * mg.n0 + i00 + p;
 #pragma unroll
-    for (int s = 0; s < 9; ++s) d0[(int64_t)(j + s * TP) * mg.n0] = v[0][s];
+    for (int s = 0; s < 9; ++s) dst[send_index(sm_, rc, k2 * L + j + s * TP, i00 + p)] = v[0][s];
   } else {
-    double2* d0 = dst + ((rc * mg.n0 + i00 + p) * mg.h2 + k2) * L;
+    double2* d0 = dst + (((int64_t)rc * mg.n0 + i00 + p) * mg.h2 + k2) * L;
 #pragma unroll
     for (int s = 0; s < 9; ++s) d0[j + s * TP] = v[0][s];
   }
@@ -341,8 +340,10 @@ __global__ void __launch_bounds__(kMaxBlock) k_mid_r(Geo g, MidGeo mg, const Rhs
 // Outer sweep: each thread owns the C component pencils of one q so Gamma_hat
 // is applied in registers between the forward and inverse transforms.
 template <int L, int C>
-__global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Geo g, OuterGeo og, const RhsState* st,
-                                                        const double2* __restrict__ tw, double2* __restrict__ W) {
+__global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Geo g, OuterGeo og, SlabMap sm_,
+                                                                              const RhsState* st,
+                                                                              const double2* __restrict__ tw,
+                                                                              double2* __restrict__ W) {
   constexpr int TP = R9<L>::TP;
   extern __shared__ double2 sm[];
   const int qb = blockIdx.x % og.nqb;
@@ -350,20 +351,34 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
   if (!rhs_active(st, r)) return;
   const int qq = threadIdx.x / TP;
   const int j = threadIdx.x - qq * TP;
-  const int q = qb * og.QB + qq;
-  const bool live = q < og.Q;
+  const int ql = qb * og.QB + qq;         // pencil index within this slab's share
+  const bool live = ql < og.Q;
+  const int q = sm_.qs[sm_.me] + (live ? ql : 0);  // global (k2, k1) pencil index
+  // element offsets of this pencil's axis-0 entries in the received segments
+  int64_t eoff[9];
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+    const int i0 = j + s * TP;
+    const int p = slab_of(sm_.s0, sm_.P, i0);
+    const int n0p = sm_.s0[p + 1] - sm_.s0[p];
+    eoff[s] = sm_.roff[p] + (int64_t)ql * n0p + (i0 - sm_.s0[p]);
+  }
   double2 v[C][9];
 #pragma unroll
   for (int a = 0; a < C; ++a) {
-    const double2* s0 = W + (((int64_t)(r * C + a)) * og.Q + q) * L;
 #pragma unroll
-    for (int s = 0; s < 9; ++s) v[a][s] = live ? s0[j + s * TP] : make_double2(0.0, 0.0);
+    for (int s = 0; s < 9; ++s) {
+      const int i0 = j + s * TP;
+      const int p = slab_of(sm_.s0, sm_.P, i0);
+      const int n0p = sm_.s0[p + 1] - sm_.s0[p];
+      v[a][s] = live ? W[eoff[s] + (int64_t)(r * C + a) * og.Q * n0p] : make_double2(0.0, 0.0);
+    }
   }
   double2* smp = sm + (size_t)qq * C * L;
   fft_reg<L, C, false>(v, smp, L, j, tw);
   // Gamma_hat(k) v = xi (xi . v) / den ; 0 at k = 0
   double xi1 = 0.0, xi2 = 0.0;
-  bool qzero = q == 0;
+  bool qzero = live && q == 0;
   if (C == 2) {
     xi1 = g.xi[1][live ? q : 0];
   } else if (C == 3) {
@@ -407,9 +422,13 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
   if (!live) return;
 #pragma unroll
   for (int a = 0; a < C; ++a) {
-    double2* d0 = W + (((int64_t)(r * C + a)) * og.Q + q) * L;
 #pragma unroll
-    for (int s = 0; s < 9; ++s) d0[j + s * TP] = v[a][s];
+    for (int s = 0; s < 9; ++s) {
+      const int i0 = j + s * TP;
+      const int p = slab_of(sm_.s0, sm_.P, i0);
+      const int n0p = sm_.s0[p + 1] - sm_.s0[p];
+      W[eoff[s] + (int64_t)(r * C + a) * og.Q * n0p] = v[a][s];
+    }
   }
 }
 

@@ -1,0 +1,76 @@
+"""Slab decomposition checked on ONE GPU: P slabs of the same
+device emulate P ranks (no kernel ever waits on another).  Every result must
+match the single-slab run: identical iteration counts, fields to rounding."""
+
+import numpy as np
+import pytest
+
+from conftest import random_spd_packed, rel_l2
+from paper_1311_0089_b200 import _native, generators as gen
+from paper_1311_0089_b200.grid import GridSpec
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(spec, packed=None, iso=None, P=2):
+    one = _native.Context(spec)
+    many = _native.Context(spec, slabs=[0] * P)
+    for ctx in (one, many):
+        if iso is not None:
+            lib_kind, host = 0, np.ascontiguousarray(iso)
+        else:
+            lib_kind, host = 1, np.ascontiguousarray(packed)
+        _native._check(_native.lib().fc_set_coefficients(ctx._h, lib_kind, _native._ptr(host), host.size))
+    return one, many
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_sharded_operators_match_single(P, rng):
+    spec = GridSpec((1.0, 1.5, 0.75), (27, 9, 81))
+    packed = random_spd_packed(spec.shape, rng)
+    one, many = _pair(spec, packed=packed, P=P)
+    u = rng.standard_normal((2, 3) + spec.shape)
+    for f in ("apply_system", "apply_A"):
+        a, b = getattr(one, f)(u), getattr(many, f)(u)
+        assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(a))
+    A0 = np.array([[2.0, 0.3, 0.0], [0.3, 1.5, 0.1], [0.0, 0.1, 1.0]])
+    for which, ref in ((0, None), (1, A0)):
+        a, b = one.project(which, ref, u), many.project(which, ref, u)
+        assert np.max(np.abs(a - b)) <= 1e-13 * max(1.0, np.max(np.abs(a)))
+
+
+@pytest.mark.parametrize("P", [2, 3, 5])
+def test_sharded_cg_fixed_point_energy(P):
+    a = gen.cfg3_sphere(27)
+    one, many = _pair(a.spec, iso=a.isotropic_values, P=P)
+    E = np.array([[1.0, 0.0, 0.0], [0.2, -0.5, 1.0]])
+    r1, x1, _ = one.solve_cg(E, 1e-8, 500)
+    rP, xP, _ = many.solve_cg(E, 1e-8, 500)
+    for q1, qP in zip(r1, rP):
+        assert q1["iterations"] == qP["iterations"] and qP["converged"]
+        np.testing.assert_allclose(qP["history"], q1["history"], rtol=1e-9, atol=1e-12 * q1["history"][0])
+    assert rel_l2(xP, x1) <= 1e-12
+    np.testing.assert_allclose(many.energy(E), one.energy(E), rtol=1e-13)
+    lam = 0.5 * (1.0 + 50.0)
+    f1, e1 = one.solve_fixed_point(E[:1], 1e-6, 1000, lam * np.eye(3), [1.0])
+    fP, eP = many.solve_fixed_point(E[:1], 1e-6, 1000, lam * np.eye(3), [1.0])
+    assert f1[0]["iterations"] == fP[0]["iterations"] and fP[0]["converged"]
+    assert rel_l2(eP, e1) <= 1e-12
+
+
+def test_sharded_polycrystal_device_generator_and_warm_start():
+    n = 27
+    spec = GridSpec((1.0,) * 3, (n,) * 3)
+    seeds, packed = gen.cfg4_grains(512, gen.SEEDS["cfg4"], n)
+    one = _native.Context(spec)
+    many = _native.Context(spec, slabs=[0, 0, 0])
+    for ctx in (one, many):
+        ctx.generate_voronoi(seeds, packed)
+    E = np.array([[1.0, 0.0, 0.0]])
+    r1, x1, _ = one.solve_cg(E, 1e-8, 2000)
+    rP, xP, _ = many.solve_cg(E, 1e-8, 2000)
+    assert r1[0]["iterations"] == rP[0]["iterations"]
+    assert rel_l2(xP, x1) <= 1e-10   # CG amplifies rounding on this 400:1 case (see DESIGN 5)
+    w1, _, _ = one.solve_cg(E, 1e-8, 2000, init=x1)
+    wP, _, _ = many.solve_cg(E, 1e-8, 2000, init=x1)
+    assert w1[0]["iterations"] == wP[0]["iterations"] <= 2
