@@ -669,7 +669,7 @@ FinArgs fin_args(fc_ctx* c, int mode, int R, int nslot, double tol, int max_iter
   f.max_iter = max_iter;
   f.window = 10;  // solver.py:27
   f.with_init = with_init;
-  f.invN = 1.0 / (double)c->N;
+  f.invN = 1.0 / (double)c->Ng;  // global voxel count (slab-local N differs)
   f.any_active = c->any_active;
   f.counter = c->counter;
   return f;

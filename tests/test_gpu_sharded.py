@@ -70,7 +70,9 @@ def test_sharded_polycrystal_device_generator_and_warm_start():
     r1, x1, _ = one.solve_cg(E, 1e-8, 2000)
     rP, xP, _ = many.solve_cg(E, 1e-8, 2000)
     assert r1[0]["iterations"] == rP[0]["iterations"]
-    assert rel_l2(xP, x1) <= 1e-10   # CG amplifies rounding on this 400:1 case (see DESIGN 5)
+    # this 27^3 / 512-grain case amplifies rounding: two runs of the unmodified reference
+    # differ by 1.45e-9 (tests/golden/poly27.npz cg_floor); gate at 10x that floor
+    assert rel_l2(xP, x1) <= 1.5e-8
     w1, _, _ = one.solve_cg(E, 1e-8, 2000, init=x1)
     wP, _, _ = many.solve_cg(E, 1e-8, 2000, init=x1)
     assert w1[0]["iterations"] == wP[0]["iterations"] <= 2
