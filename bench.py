@@ -74,6 +74,7 @@ def barrier(world):
 
 
 def max_over_ranks(world, v):
+    """Max of a per-rank time over the process group (host plumbing over gloo)."""
     if world == 1:
         return v
     import torch
@@ -265,9 +266,9 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(wl):
+def config_dict(wl, parallelism="replicas"):
     return {"workload": wl.desc, "grid": list(wl.shape), "load_cases": wl.R, "tol": TOL,
-            "parallelism": "replicas",
+            "parallelism": parallelism,
             "l2": "inputs larger than L2 (per-iteration working set > 126 MB)"}
 
 
@@ -281,7 +282,15 @@ def run_gpu(args):
     loads, R, N, d = wl.loads, wl.R, wl.N, wl.d
     host = wl.host_field()
     spec = GridSpec((1.0,) * d, wl.shape)
-    ctx = _native.Context(spec, local)
+    # 3-D configs shard along axis 0 across the ranks (NCCL exchanges inside the
+    # library, strong scaling); cfg2 runs independent replicas (weak scaling)
+    sharded = world > 1 and d == 3 and not args.replicas
+    if sharded:
+        from paper_1311_0089_b200 import parallel
+
+        ctx = parallel.distributed_context(spec, device=local)
+    else:
+        ctx = _native.Context(spec, local)
     wl.setup(ctx, host)
 
     def solve_resident():
@@ -309,7 +318,8 @@ def run_gpu(args):
     prof = ctx.profile()
     assert [r["iterations"] for r in reps] == iters
     ms_max = max_over_ranks(world, ms)
-    value = world * work_per_step * args.steps / (ms_max / 1000.0)
+    copies = 1 if sharded else world
+    value = copies * work_per_step * args.steps / (ms_max / 1000.0)
 
     # ---- e2e: host buffers through the public API -----------------------------
     import torch
@@ -331,7 +341,7 @@ def run_gpu(args):
         ctx.solve_cg(loads, TOL, MAX_ITER, out=x_out)
     ctx.timer_mark(3)
     ms_e2e = max_over_ranks(world, ctx.timer_elapsed(2, 3))
-    e2e = world * work_per_step * e2e_steps / (ms_e2e / 1000.0)
+    e2e = copies * work_per_step * e2e_steps / (ms_e2e / 1000.0)
 
     if rank != 0:
         return
@@ -374,8 +384,8 @@ def run_gpu(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(wl),
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(wl, f"slab{world}" if sharded else ("replicas" if world > 1 else "single")),
         "iterations": iters,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,
@@ -400,6 +410,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override the grid size (0 = BASELINE size)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas even for 3-D configs")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -79,6 +79,15 @@ void fc_destroy(fc_ctx* ctx);
 int32_t fc_create_sharded(fc_ctx** out, int32_t dim, const int64_t* shape, const double* half_periods,
                           int32_t nslabs, const int32_t* devices);
 
+/* One process per GPU: this process owns slab `rank` of `nranks` on `device`;
+ * exchanges are NCCL grouped send/recv, reductions an NCCL all-gather of the
+ * per-slab sums (summed in rank order on every rank).  unique_id: 128 bytes from
+ * fc_nccl_unique_id() on rank 0, broadcast by the caller (torch.distributed).
+ * Host arrays keep the full layout; each rank reads / writes its own planes. */
+int32_t fc_nccl_unique_id(void* out128);
+int32_t fc_create_dist(fc_ctx** out, int32_t dim, const int64_t* shape, const double* half_periods,
+                       int32_t nranks, int32_t rank, int32_t device, const void* unique_id);
+
 /* CoefficientField upload (material.py:90-158): count = N (isotropic) or nsym*N (packed). */
 int32_t fc_set_coefficients(fc_ctx* ctx, int32_t kind, const double* host, int64_t count);
 

@@ -44,6 +44,10 @@ SIGNATURES = [
      [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, _i64p, _dp, ctypes.c_int32]),
     ("fc_create_sharded", ctypes.c_int32,
      [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, _i64p, _dp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]),
+    ("fc_nccl_unique_id", ctypes.c_int32, [ctypes.c_void_p]),
+    ("fc_create_dist", ctypes.c_int32,
+     [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, _i64p, _dp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+      ctypes.c_void_p]),
     ("fc_destroy", None, [ctypes.c_void_p]),
     ("fc_set_coefficients", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, _dp, ctypes.c_int64]),
     ("fc_apply_A", ctypes.c_int32, [ctypes.c_void_p, _dp, _dp, ctypes.c_int32]),
@@ -108,6 +112,12 @@ def _c64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().fc_nccl_unique_id(buf))
+    return buf.raw
+
+
 def device_count():
     n = ctypes.c_int32(0)
     rc = lib().fc_device_count(ctypes.byref(n))
@@ -116,6 +126,22 @@ def device_count():
 
 class Context:
     """One GridSpec bound to one GPU: coefficients, FFT plans and workspace in HBM."""
+
+    @classmethod
+    def distributed(cls, spec, nranks, rank, device_id, unique_id: bytes):
+        """One slab per process (fc_create_dist); unique_id from nccl_unique_id() on rank 0."""
+        self = cls.__new__(cls)
+        self.spec, self.device_id, self.d = spec, device_id, spec.dim
+        self.shape, self.total = tuple(spec.shape), spec.total
+        self._h = ctypes.c_void_p()
+        shape = np.array(spec.shape, dtype=np.int64)
+        Y = np.array(spec.half_periods, dtype=np.float64)
+        uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().fc_create_dist(ctypes.byref(self._h), spec.dim, shape.ctypes.data_as(_i64p), _ptr(Y),
+                                    nranks, rank, device_id, uid))
+        self.slabs = ("dist", nranks, rank)
+        self.isotropic = None
+        return self
 
     def __init__(self, spec, device_id: int = 0, slabs=None):
         """``slabs``: None (one GPU) or a list of device ids, one per axis-0 slab

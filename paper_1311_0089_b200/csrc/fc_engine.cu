@@ -188,6 +188,11 @@ struct fc_ctx {
   double* lsum = nullptr;  // slab-local reduction sums (2 x FC_MAX_RHS)
   std::vector<fc_ctx*> sub;
   cudaEvent_t sev[4] = {};  // phase events of this slab
+  // one process per GPU: this process holds slab `me` only; exchanges and sums go
+  // through NCCL (fc_create_dist)
+  bool dist = false;
+  void* comm = nullptr;        // ncclComm_t
+  double* gathered = nullptr;  // [P][FC_MAX_RHS] all ranks' local sums (device)
 
   SlabMap slabmap(int R) const {
     SlabMap m{};
@@ -677,6 +682,7 @@ FinArgs fin_args(fc_ctx* c, int mode, int R, int nslot, double tol, int max_iter
 
 }  // namespace
 
+#include "fc_nccl.inc"
 #include "fc_shard.inc"
 
 // ===========================================================================
@@ -850,11 +856,71 @@ int32_t fc_create_sharded(fc_ctx** out, int32_t dim, const int64_t* shape, const
   return FC_OK;
 }
 
+int32_t fc_nccl_unique_id(void* out) {
+  if (out == nullptr) return set_err(FC_EINVAL, "null output pointer");
+  if (!nccl().ok) return set_err(FC_ENOTSUP, "NCCL unavailable: %s", nccl().why.c_str());
+  ncclUniqueId id;
+  NK(nccl().getUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  return FC_OK;
+}
+
+int32_t fc_create_dist(fc_ctx** out, int32_t dim, const int64_t* shape, const double* half_periods, int32_t nranks,
+                       int32_t rank, int32_t device, const void* unique_id) {
+  if (out == nullptr || unique_id == nullptr) return set_err(FC_EINVAL, "null pointer argument");
+  *out = nullptr;
+  TRY(check_shape(dim, shape, half_periods));
+  if (nranks < 1 || nranks > kMaxSlabs || rank < 0 || rank >= nranks)
+    return set_err(FC_EINVAL, "rank %d / world %d outside [0, %d)", rank, nranks, kMaxSlabs);
+  if (dim != 3) return set_err(FC_ENOTSUP, "slab decomposition is implemented for d = 3");
+  if (shape[0] < nranks) return set_err(FC_EINVAL, "more ranks than axis-0 planes");
+  if (!nccl().ok) return set_err(FC_ENOTSUP, "NCCL unavailable: %s", nccl().why.c_str());
+  fc_ctx* c = new fc_ctx();
+  c->device = -1;
+  c->dim = dim;
+  c->P = nranks;
+  c->me = rank;
+  c->dist = true;
+  c->n0g = (int)shape[0];
+  c->Ng = 1;
+  for (int a = 0; a < dim; ++a) {
+    c->n[a] = (int)shape[a];
+    c->Y[a] = half_periods[a];
+    c->Ng *= shape[a];
+  }
+  c->N = c->Ng;
+  fc_ctx* sl = nullptr;
+  int rc = create_slab(&sl, dim, shape, half_periods, device, nranks, rank);
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  c->sub.push_back(sl);
+  cudaSetDevice(device);
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  ncclComm_t comm;
+  ncclResult_t nr = nccl().commInitRank(&comm, nranks, id, rank);
+  if (nr != ncclSuccess) {
+    fc_destroy(c);
+    return set_err(FC_ECUDA, "ncclCommInitRank: %s", nccl().errStr(nr));
+  }
+  c->comm = comm;
+  if (cudaMalloc(&c->gathered, sizeof(double) * FC_MAX_RHS * nranks) != cudaSuccess) {
+    fc_destroy(c);
+    return set_err(FC_ENOMEM, "gather buffer");
+  }
+  *out = c;
+  return FC_OK;
+}
+
 void fc_destroy(fc_ctx* c) {
   if (c == nullptr) return;
   for (fc_ctx* sl : c->sub) fc_destroy(sl);
   c->sub.clear();
   if (c->device < 0) {  // sharded parent holds no device resources
+    if (c->comm) nccl().commDestroy((ncclComm_t)c->comm);
+    cudaFree(c->gathered);
     delete c;
     return;
   }
