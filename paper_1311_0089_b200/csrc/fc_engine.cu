@@ -244,6 +244,11 @@ int launch(fc_ctx* c, const char* name, F&& f) {
   c->launches++;
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_err(FC_ECUDA, "launch of %s failed: %s", name, cudaGetErrorString(err));
+  static const bool sync_debug = getenv("FC_SYNC_DEBUG") != nullptr;
+  if (sync_debug) {
+    err = cudaStreamSynchronize(c->stream);
+    if (err != cudaSuccess) return set_err(FC_ECUDA, "kernel %s failed: %s", name, cudaGetErrorString(err));
+  }
   if (c->prof_on) {
     cudaEventRecord(e1, c->stream);
     auto it = c->prof_idx.find(name);

@@ -76,3 +76,21 @@ def test_sharded_polycrystal_device_generator_and_warm_start():
     w1, _, _ = one.solve_cg(E, 1e-8, 2000, init=x1)
     wP, _, _ = many.solve_cg(E, 1e-8, 2000, init=x1)
     assert w1[0]["iterations"] == wP[0]["iterations"] <= 2
+
+
+def test_nccl_slab_path_single_rank():
+    """fc_create_dist with one rank: the NCCL exchange (send/recv to self) and the
+    all-gather reduction run for real and must reproduce the plain context."""
+    import torch  # noqa: F401  (loads the NCCL the library resolves at run time)
+
+    a = gen.cfg3_sphere(27)
+    one = _native.Context(a.spec)
+    dist = _native.Context.distributed(a.spec, 1, 0, 0, _native.nccl_unique_id())
+    for ctx in (one, dist):
+        ctx.set_coefficients(a)
+    E = np.array([[1.0, 0.0, 0.0]])
+    r1, x1, _ = one.solve_cg(E, 1e-8, 500)
+    rD, xD, _ = dist.solve_cg(E, 1e-8, 500)
+    assert r1[0]["iterations"] == rD[0]["iterations"]
+    assert rel_l2(xD, x1) <= 1e-13
+    np.testing.assert_allclose(dist.energy(E), one.energy(E), rtol=1e-13)
