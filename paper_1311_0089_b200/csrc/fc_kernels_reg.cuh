@@ -51,7 +51,7 @@ constexpr int kMaxBlockOuter = 256;
 // pointwise input on the fly.  After the FFT the spectrum goes through shared
 // memory once more to split the two-for-one pairs and to store transposed.
 template <int L>
-__global__ void __launch_bounds__(kMaxBlock) k_row_fwd_r(Geo g, RowGeo rg, Coef C, InArgs ia, const RhsState* st,
+__global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, InArgs ia, const RhsState* st,
                                                           const double2* __restrict__ tw, double2* __restrict__ W) {
   constexpr int TP = R9<L>::TP;
   extern __shared__ double2 sm[];
@@ -76,10 +76,11 @@ __global__ void __launch_bounds__(kMaxBlock) k_row_fwd_r(Geo g, RowGeo rg, Coef 
   // off-diagonal entries (then (A - A0) e is diagonal, solver.py:253-255)
   const bool fp_diag = ev.mode != IN_FP ||
                        ((a == 0 || ev.R0 == 0.0) && (a == 1 || ev.R1 == 0.0) && (a == 2 || ev.R2 == 0.0));
-  if ((ev.kind == 0 || ev.mode == IN_RAW) && ev.mode != IN_CONST && fp_diag) {
+  const bool staged = (ev.kind == 0 || ev.mode == IN_RAW) && ev.mode != IN_CONST && fp_diag;
+  if (staged) {
     // isotropic: stage u (r / e / field), p_old and A for the whole row block in
-    // smem with cp.async, then evaluate from smem (the staging area is reused as
-    // the FFT exchange buffer afterwards)
+    // smem with cp.async, evaluate, store p' at once (no register array lives
+    // across the loop); the staging area is reused as the FFT exchange buffer
     const int stride = (rg.B * L + 3) & ~1;  // even, leaves room for the alignment shift
     double* st_u = reinterpret_cast<double*>(sm);
     double* st_p = st_u + stride;
@@ -94,10 +95,12 @@ __global__ void __launch_bounds__(kMaxBlock) k_row_fwd_r(Geo g, RowGeo rg, Coef 
     st_a += sa;
     cp_async_wait_all();
     __syncthreads();
+    double* pw = ia.p_new + ub;
+    const double A0aa = InEval::sel(a, ev.R0, ev.R1, ev.R2);
 #pragma unroll
     for (int s = 0; s < 9; ++s) {
       const int i = j + s * TP;
-      double y[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
+      double y[2] = {0.0, 0.0};
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int row = 2 * p + h;
@@ -106,18 +109,17 @@ __global__ void __launch_bounds__(kMaxBlock) k_row_fwd_r(Geo g, RowGeo rg, Coef 
           double x = st_u[e];
           if (ev.mode == IN_PNEW) {
             x = ev.first ? x : __dadd_rn(x, __dmul_rn(ev.beta, st_p[e]));
-            q[h] = x;
+            pw[e] = x;
           }
           double val;
           if (ev.mode == IN_RAW) val = x;
-          else if (ev.mode == IN_FP) val = __dmul_rn(__dsub_rn(st_a[e], InEval::sel(a, ev.R0, ev.R1, ev.R2)), x);
+          else if (ev.mode == IN_FP) val = __dmul_rn(__dsub_rn(st_a[e], A0aa), x);
           else val = __dmul_rn(st_a[e], x);
           if (ev.mode != IN_FP && ev.s != 1.0) val = __dmul_rn(ev.s, val);
           y[h] = val;
         }
       }
       v[0][s] = make_double2(y[0], y[1]);
-      pn[s] = make_double2(q[0], q[1]);
     }
   } else {
     with_in_mode(ev.mode, ev.kind, [&](auto M, auto K) {
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(kMaxBlock) k_row_fwd_r(Geo g, RowGeo rg, Coef 
       }
     });
   }
-  if (ev.mode == IN_PNEW) {  // p' = r + beta p, stored once by the CTA owning component a
+  if (ev.mode == IN_PNEW && !staged) {  // p' = r + beta p, stored once by the CTA owning component a
     double* pw = ia.p_new + ev.base + (int64_t)a * g.N + vbase;
 #pragma unroll
     for (int s = 0; s < 9; ++s) {
