@@ -173,6 +173,7 @@ struct fc_ctx {
   int row_npen = 0, mid_bp = 0, outer_qb = 0, inv_prefetch = 1;
   int aniso_npen = 0;       // all-components first sweep for packed coefficients (0 = off)
   int aniso_split = 1;      // packed coefficients: pointwise kernel + staged row FFT
+  int outer_persist = 0;    // persistent double-buffered outer sweep (FC_OUTER_PERSIST)
   size_t smem_aniso_r = 0;
   size_t smem_row_r = 0, smem_row_inv_r = 0, smem_mid_r = 0, smem_outer_r = 0;
 
@@ -426,6 +427,7 @@ int choose_tiles(fc_ctx* c) {
     og.nqb = (og.Q + qb - 1) / qb;
     c->outer_qb = qb;
     c->smem_outer_r = (size_t)16 * d * qb * c->n0g;
+    c->outer_persist = env_int("FC_OUTER_PERSIST", 0) && 2 * c->smem_outer_r <= (size_t)c->smem_optin - 2048;
   }
   return FC_OK;
 }
@@ -454,6 +456,8 @@ int allow_reg_smem(int mx) {
       al(k_mid_r<LL, true>);
       al(k_outer_r<LL, 2>);
       al(k_outer_r<LL, 3>);
+      al(k_outer_p<LL, 2>);
+      al(k_outer_p<LL, 3>);
     });
   }
   return rc;
@@ -600,7 +604,17 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b) og.M[a][b] = M[a][b];
   double2* Wout = c->P > 1 ? c->W2r : c->W2;
-  if (c->outer_qb) {
+  og.R = R;
+  if (c->outer_qb && c->outer_persist) {
+    const int nt = c->outer_qb * (c->n0g / 9);
+    const double2* tw = c->rtw(c->n0g);
+    const size_t smem = 2 * (size_t)16 * d * c->outer_qb * c->n0g;
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)R * og.nqb, c->num_sms);
+    TRY(launch(c, "outer", [&] {
+      if (d == 2) FC_POW3_SWITCH(c->n0g, (k_outer_p<LL, 2><<<grid, nt, smem, s>>>(g, og, smap, st, tw, Wout)))
+      else FC_POW3_SWITCH(c->n0g, (k_outer_p<LL, 3><<<grid, nt, smem, s>>>(g, og, smap, st, tw, Wout)))
+    }));
+  } else if (c->outer_qb) {
     const int nt = c->outer_qb * (c->n0g / 9);
     const double2* tw = c->rtw(c->n0g);
     TRY(launch(c, "outer", [&] {

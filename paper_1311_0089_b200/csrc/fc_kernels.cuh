@@ -768,6 +768,7 @@ __global__ void __launch_bounds__(kThreads) k_mid(Geo g, MidGeo mg, const RhsSta
 // (solver.py:98-110, green.py:81-92).
 struct OuterGeo {
   int n0, Q, QB, nqb;   // Q pencils per component, QB per CTA
+  int R;                // right-hand sides (persistent kernel tiles over R x nqb)
   int n1, h_last;       // d = 3: q = k2 * n1 + k1 ; d = 2: q = k1
   int orth;
   double M[kMaxDim][kMaxDim];

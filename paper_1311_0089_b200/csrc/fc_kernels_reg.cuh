@@ -551,3 +551,129 @@ __global__ void __launch_bounds__(kMaxBlock, 1) k_row_fwd_aniso_r(Geo g, RowGeo 
 }
 
 }  // namespace fc
+
+namespace fc {
+
+// Persistent outer sweep: one CTA per SM loops over pencil groups; the next
+// group is prefetched with cp.async into the second smem stage while the
+// current one is transformed, so HBM traffic overlaps the FFT arithmetic.
+// Stage layout: [a][qq][L] complex; the current stage doubles as the FFT
+// exchange buffer once its data sit in registers.
+template <int L, int C>
+__global__ void __launch_bounds__(kMaxBlockOuter, 1) k_outer_p(Geo g, OuterGeo og, SlabMap sm_, const RhsState* st,
+                                                               const double2* __restrict__ tw, double2* __restrict__ W) {
+  constexpr int TP = R9<L>::TP;
+  extern __shared__ double2 sm[];
+  const int stage = og.QB * C * L;
+  const int qq = threadIdx.x / TP;
+  const int j = threadIdx.x - qq * TP;
+  const int ntiles = og.nqb * gridDim.y;  // gridDim.y = R
+  (void)ntiles;
+  const int ntile = og.nqb * og.R;
+  auto tile_src = [&](int t, int a, int s, int& ok) -> int64_t {
+    const int qb = t % og.nqb;
+    const int r = t / og.nqb;
+    const int ql = qb * og.QB + qq;
+    ok = ql < og.Q;
+    const int i0 = j + s * TP;
+    const int p = slab_of(sm_.s0, sm_.P, i0);
+    const int n0p = sm_.s0[p + 1] - sm_.s0[p];
+    return sm_.roff[p] + (int64_t)(r * C + a) * og.Q * n0p + (int64_t)(ok ? ql : 0) * n0p + (i0 - sm_.s0[p]);
+  };
+  auto prefetch = [&](int t, int buf) {
+    const int r = t / og.nqb;
+    if (st != nullptr && !st[r].active) return;
+    double2* dst = sm + (size_t)buf * stage;
+#pragma unroll
+    for (int a = 0; a < C; ++a)
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+        int ok;
+        const int64_t off = tile_src(t, a, s, ok);
+        if (ok) cp_async16(dst + ((size_t)a * og.QB + qq) * L + j + s * TP, W + off);
+      }
+  };
+  int t = blockIdx.x;
+  int cur = 0;
+  if (t < ntile) prefetch(t, 0);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  for (; t < ntile; t += gridDim.x) {
+    const int tn = t + gridDim.x;
+    if (tn < ntile) prefetch(tn, cur ^ 1);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();
+    const int qb = t % og.nqb;
+    const int r = t / og.nqb;
+    const bool act = st == nullptr || st[r].active;
+    const int ql = qb * og.QB + qq;
+    const bool live = ql < og.Q;
+    double2* buf = sm + (size_t)cur * stage;
+    if (act) {
+      double2 v[C][9];
+#pragma unroll
+      for (int a = 0; a < C; ++a)
+#pragma unroll
+        for (int s = 0; s < 9; ++s)
+          v[a][s] = live ? buf[((size_t)a * og.QB + qq) * L + j + s * TP] : make_double2(0.0, 0.0);
+      double2* smp = buf + (size_t)qq * L;
+      fft_reg<L, C, false>(v, smp, og.QB * L, j, tw);
+      const int q = sm_.qs[sm_.me] + (live ? ql : 0);
+      double xi1 = 0.0, xi2 = 0.0;
+      if (C == 2) {
+        xi1 = g.xi[1][q];
+      } else {
+        const int k2 = q / og.n1, k1 = q - k2 * og.n1;
+        xi1 = g.xi[1][k1];
+        xi2 = g.xi[2][k2];
+      }
+      const bool qzero = live && q == 0;
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+        const int i0 = j + s * TP;
+        double xi[3] = {g.xi[0][i0], xi1, xi2};
+        if (qzero && i0 == 0) {
+#pragma unroll
+          for (int a = 0; a < C; ++a) v[a][s] = make_double2(0.0, 0.0);
+          continue;
+        }
+        double2 dots = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int a = 0; a < C; ++a) {
+          dots.x += xi[a] * v[a][s].x;
+          dots.y += xi[a] * v[a][s].y;
+        }
+        double den = 0.0;
+        if (og.orth) {
+#pragma unroll
+          for (int a = 0; a < C; ++a) den += xi[a] * xi[a];
+        } else {
+#pragma unroll
+          for (int a = 0; a < C; ++a)
+#pragma unroll
+            for (int b = 0; b < C; ++b) den += xi[a] * og.M[a][b] * xi[b];
+        }
+        const double inv = 1.0 / den;
+        const double2 qv = make_double2(dots.x * inv, dots.y * inv);
+#pragma unroll
+        for (int a = 0; a < C; ++a) v[a][s] = make_double2(xi[a] * qv.x, xi[a] * qv.y);
+      }
+      fft_reg<L, C, true>(v, smp, og.QB * L, j, tw);
+      if (live) {
+#pragma unroll
+        for (int a = 0; a < C; ++a)
+#pragma unroll
+          for (int s = 0; s < 9; ++s) {
+            int ok;
+            const int64_t off = tile_src(t, a, s, ok);
+            W[off] = v[a][s];
+          }
+      }
+    }
+    __syncthreads();  // this stage becomes the prefetch target of tile t + 2 gridDim.x
+    cur ^= 1;
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+}  // namespace fc
