@@ -139,6 +139,8 @@ struct fc_ctx {
   int* any_active = nullptr;
   unsigned* counter = nullptr;  // last-CTA arrival counter of the fused finalize
   int* h_flag = nullptr;  // pinned, 4 slots
+  int* h_mapped = nullptr;   // zero-copy "any RHS active" flag written by the finalizing CTA
+  int* d_mapped = nullptr;   // its device alias
   cudaEvent_t flag_ev[4] = {};
   double* d_mat = nullptr;
   cudaEvent_t timer_ev[8] = {};
@@ -694,7 +696,7 @@ FinArgs fin_args(fc_ctx* c, int mode, int R, int nslot, double tol, int max_iter
   f.window = 10;  // solver.py:27
   f.with_init = with_init;
   f.invN = 1.0 / (double)c->Ng;  // global voxel count (slab-local N differs)
-  f.any_active = c->any_active;
+  f.any_active = c->d_mapped;  // zero-copy: the host reads it after the iteration's event
   f.counter = c->counter;
   return f;
 }
@@ -794,6 +796,10 @@ int create_slab(fc_ctx** out, int32_t dim, const int64_t* shape, const double* h
   cudaMemset(c->counter, 0, sizeof(unsigned));
   if (cudaMalloc(&c->lsum, sizeof(double) * 2 * FC_MAX_RHS) != cudaSuccess) return fail(set_err(FC_ENOMEM, "lsum alloc"));
   if (cudaMallocHost(&c->h_flag, 4 * sizeof(int)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "pinned alloc"));
+  if (cudaHostAlloc(&c->h_mapped, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&c->d_mapped, c->h_mapped, 0) != cudaSuccess)
+    return fail(set_err(FC_ENOMEM, "mapped flag alloc"));
+  *c->h_mapped = 1;
   for (auto& e : c->flag_ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   if (cudaMalloc(&c->d_mat, sizeof(double) * FC_MAX_RHS * FC_MAX_RHS) != cudaSuccess)
     return fail(set_err(FC_ENOMEM, "matrix alloc"));
@@ -960,6 +966,7 @@ void fc_destroy(fc_ctx* c) {
   for (auto& e : c->sev)
     if (e) cudaEventDestroy(e);
   if (c->h_flag) cudaFreeHost(c->h_flag);
+  if (c->h_mapped) cudaFreeHost(c->h_mapped);
   for (auto& e : c->flag_ev)
     if (e) cudaEventDestroy(e);
   for (auto& pe : c->pending) {
@@ -1152,8 +1159,9 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
     TRY(launch(c, "cg_update", [&] {
       k_cg_update<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->st, c->x, c->r, pcur, c->Ap, c->part, nvec, fb);
     }));
+    // the flag is monotone (an inactive RHS never reactivates), so reading a
+    // later iteration's value is always a valid stop decision
     const int slot = it & 3;
-    CK(cudaMemcpyAsync(c->h_flag + slot, c->any_active, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaEventRecord(c->flag_ev[slot], s));
     if (record) {
       TRY(sync(c));
@@ -1162,11 +1170,11 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
         TRY(sync(c));
         ++nit;
       }
-      any = c->h_flag[slot] != 0;
+      any = *(volatile int*)c->h_mapped != 0;
     } else if (it >= 1) {
       const int prev = (it - 1) & 3;
       CK(cudaEventSynchronize(c->flag_ev[prev]));
-      if (c->h_flag[prev] == 0) any = false;
+      if (*(volatile int*)c->h_mapped == 0) any = false;
     }
   }
   TRY(sync(c));
@@ -1236,12 +1244,11 @@ int32_t fc_solve_fixed_point(fc_ctx* c, int32_t R, const double* E, double tol, 
   for (int it = 0; any && it < max_iter; ++it) {
     TRY(run_operator(c, R, ia, ea, 0, M, c->st));
     const int slot = it & 3;
-    CK(cudaMemcpyAsync(c->h_flag + slot, c->any_active, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaEventRecord(c->flag_ev[slot], s));
     if (it >= 1) {
       const int prev = (it - 1) & 3;
       CK(cudaEventSynchronize(c->flag_ev[prev]));
-      if (c->h_flag[prev] == 0) any = false;
+      if (*(volatile int*)c->h_mapped == 0) any = false;
     }
   }
   // solution = e - E_N in place (solver.py:293-294)

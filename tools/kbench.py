@@ -15,7 +15,11 @@ from paper_1311_0089_b200.grid import GridSpec  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+nrhs = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 wl = bench.Workload(name, n)
+if nrhs:
+    wl.loads = wl.loads[:nrhs]
+    wl.R = nrhs
 ctx = _native.Context(GridSpec((1.0,) * wl.d, wl.shape))
 wl.setup(ctx, wl.host_field())
 u = np.random.default_rng(0).standard_normal((wl.R, wl.d) + wl.shape)
