@@ -176,6 +176,7 @@ struct fc_ctx {
   int aniso_npen = 0;       // all-components first sweep for packed coefficients (0 = off)
   int aniso_split = 1;      // packed coefficients: pointwise kernel + staged row FFT
   int outer_persist = 0;    // persistent double-buffered outer sweep (FC_OUTER_PERSIST)
+  int outer_c1 = 0;         // one-component-per-thread outer sweep: pencil groups per CTA (0 = off)
   size_t smem_aniso_r = 0;
   size_t smem_row_r = 0, smem_row_inv_r = 0, smem_mid_r = 0, smem_outer_r = 0;
 
@@ -430,6 +431,15 @@ int choose_tiles(fc_ctx* c) {
     c->outer_qb = qb;
     c->smem_outer_r = (size_t)16 * d * qb * c->n0g;
     c->outer_persist = env_int("FC_OUTER_PERSIST", 0) && 2 * c->smem_outer_r <= (size_t)c->smem_optin - 2048;
+    {
+      // one component per thread: d * QB * TP threads (<= 512)
+      const int want = env_int(d == 3 ? "FC_OUTER_C1_3D" : "FC_OUTER_C1_2D", 0);
+      if (want) {
+        int qb1 = std::max(1, std::min(og.Q, 512 / (d * TP)));
+        while (qb1 > 1 && (size_t)16 * d * qb1 * c->n0g > (size_t)c->smem_optin - 2048) --qb1;
+        if (d * TP <= 512 && (size_t)16 * d * qb1 * c->n0g <= (size_t)c->smem_optin - 2048) c->outer_c1 = qb1;
+      }
+    }
   }
   return FC_OK;
 }
@@ -460,6 +470,8 @@ int allow_reg_smem(int mx) {
       al(k_outer_r<LL, 3>);
       al(k_outer_p<LL, 2>);
       al(k_outer_p<LL, 3>);
+      al(k_outer_c1<LL, 2>);
+      al(k_outer_c1<LL, 3>);
     });
   }
   return rc;
@@ -607,7 +619,18 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     for (int b = 0; b < 3; ++b) og.M[a][b] = M[a][b];
   double2* Wout = c->P > 1 ? c->W2r : c->W2;
   og.R = R;
-  if (c->outer_qb && c->outer_persist) {
+  if (c->outer_c1) {
+    OuterGeo o1 = og;
+    o1.QB = c->outer_c1;
+    o1.nqb = (og.Q + o1.QB - 1) / o1.QB;
+    const int nt = d * o1.QB * (c->n0g / 9);
+    const double2* tw = c->rtw(c->n0g);
+    const size_t smem = (size_t)16 * d * o1.QB * c->n0g;
+    TRY(launch(c, "outer", [&] {
+      if (d == 2) FC_POW3_SWITCH(c->n0g, (k_outer_c1<LL, 2><<<(unsigned)(R * o1.nqb), nt, smem, s>>>(g, o1, smap, st, tw, Wout)))
+      else FC_POW3_SWITCH(c->n0g, (k_outer_c1<LL, 3><<<(unsigned)(R * o1.nqb), nt, smem, s>>>(g, o1, smap, st, tw, Wout)))
+    }));
+  } else if (c->outer_qb && c->outer_persist) {
     const int nt = c->outer_qb * (c->n0g / 9);
     const double2* tw = c->rtw(c->n0g);
     const size_t smem = 2 * (size_t)16 * d * c->outer_qb * c->n0g;

@@ -322,6 +322,10 @@ __global__ void __launch_bounds__(kMaxBlock) k_mid_r(Geo g, MidGeo mg, SlabMap s
     const double2* s0 = src + (((int64_t)rc * mg.n0 + i00 + p) * mg.h2 + k2) * L;
 #pragma unroll
     for (int s = 0; s < 9; ++s) v[0][s] = live ? s0[j + s * TP] : make_double2(0.0, 0.0);
+  } else if (sm_.P == 1) {
+    const double2* s0 = src + (((int64_t)rc * mg.h2 + k2) * L) * sm_.n0l + i00 + p;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) v[0][s] = live ? s0[(int64_t)(j + s * TP) * sm_.n0l] : make_double2(0.0, 0.0);
   } else {
 #pragma unroll
     for (int s = 0; s < 9; ++s)
@@ -329,7 +333,11 @@ __global__ void __launch_bounds__(kMaxBlock) k_mid_r(Geo g, MidGeo mg, SlabMap s
   }
   fft_reg<L, 1, INV>(v, sm + (size_t)p * L, L, j, tw);
   if (!live) return;
-  if (!INV) {
+  if (!INV && sm_.P == 1) {
+    double2* d0 = dst + (((int64_t)rc * mg.h2 + k2) * L) * sm_.n0l + i00 + p;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) d0[(int64_t)(j + s * TP) * sm_.n0l] = v[0][s];
+  } else if (!INV) {
 #pragma unroll
     for (int s = 0; s < 9; ++s) dst[send_index(sm_, rc, k2 * L + j + s * TP, i00 + p)] = v[0][s];
   } else {
@@ -357,24 +365,31 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
   const bool live = ql < og.Q;
   const int q = sm_.qs[sm_.me] + (live ? ql : 0);  // global (k2, k1) pencil index
   // element offsets of this pencil's axis-0 entries in the received segments
-  int64_t eoff[9];
+  // element offsets of this pencil's axis-0 entries: one contiguous pencil for
+  // a single slab (uniform fast path), received segments otherwise
+  int64_t eoff[9], cstride[9];
+  if (sm_.P == 1) {
 #pragma unroll
-  for (int s = 0; s < 9; ++s) {
-    const int i0 = j + s * TP;
-    const int p = slab_of(sm_.s0, sm_.P, i0);
-    const int n0p = sm_.s0[p + 1] - sm_.s0[p];
-    eoff[s] = sm_.roff[p] + (int64_t)ql * n0p + (i0 - sm_.s0[p]);
-  }
-  double2 v[C][9];
-#pragma unroll
-  for (int a = 0; a < C; ++a) {
+    for (int s = 0; s < 9; ++s) {
+      eoff[s] = (int64_t)ql * L + j + s * TP;
+      cstride[s] = (int64_t)og.Q * L;
+    }
+  } else {
 #pragma unroll
     for (int s = 0; s < 9; ++s) {
       const int i0 = j + s * TP;
       const int p = slab_of(sm_.s0, sm_.P, i0);
       const int n0p = sm_.s0[p + 1] - sm_.s0[p];
-      v[a][s] = live ? W[eoff[s] + (int64_t)(r * C + a) * og.Q * n0p] : make_double2(0.0, 0.0);
+      eoff[s] = sm_.roff[p] + (int64_t)ql * n0p + (i0 - sm_.s0[p]);
+      cstride[s] = (int64_t)og.Q * n0p;
     }
+  }
+  double2 v[C][9];
+#pragma unroll
+  for (int a = 0; a < C; ++a) {
+#pragma unroll
+    for (int s = 0; s < 9; ++s)
+      v[a][s] = live ? W[eoff[s] + (int64_t)(r * C + a) * cstride[s]] : make_double2(0.0, 0.0);
   }
   double2* smp = sm + (size_t)qq * C * L;
   fft_reg<L, C, false>(v, smp, L, j, tw);
@@ -425,12 +440,7 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
 #pragma unroll
   for (int a = 0; a < C; ++a) {
 #pragma unroll
-    for (int s = 0; s < 9; ++s) {
-      const int i0 = j + s * TP;
-      const int p = slab_of(sm_.s0, sm_.P, i0);
-      const int n0p = sm_.s0[p + 1] - sm_.s0[p];
-      W[eoff[s] + (int64_t)(r * C + a) * og.Q * n0p] = v[a][s];
-    }
+    for (int s = 0; s < 9; ++s) W[eoff[s] + (int64_t)(r * C + a) * cstride[s]] = v[a][s];
   }
 }
 
@@ -674,6 +684,95 @@ __global__ void __launch_bounds__(kMaxBlockOuter, 1) k_outer_p(Geo g, OuterGeo o
     cur ^= 1;
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+}  // namespace fc
+
+namespace fc {
+
+// Outer sweep, one component per thread: thread (a, qq, j) transforms pencil
+// (a, q); Gamma_hat needs all components of a mode, so after the forward FFT
+// the spectra meet once in shared memory.  ~1/C of the registers of k_outer_r,
+// hence C times the resident warps, for one extra shared-memory exchange.
+template <int L, int C>
+__global__ void __launch_bounds__(512, 1) k_outer_c1(Geo g, OuterGeo og, SlabMap sm_, const RhsState* st,
+                                                     const double2* __restrict__ tw, double2* __restrict__ W) {
+  constexpr int TP = R9<L>::TP;
+  extern __shared__ double2 sm[];
+  const int qb = blockIdx.x % og.nqb;
+  const int r = blockIdx.x / og.nqb;
+  if (!rhs_active(st, r)) return;
+  const int per_a = og.QB * TP;
+  const int a = threadIdx.x / per_a;
+  const int rem = threadIdx.x - a * per_a;
+  const int qq = rem / TP;
+  const int j = rem - qq * TP;
+  const int ql = qb * og.QB + qq;
+  const bool live = ql < og.Q;
+  const int q = sm_.qs[sm_.me] + (live ? ql : 0);
+  int64_t eoff[9];
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+    const int i0 = j + s * TP;
+    const int p = slab_of(sm_.s0, sm_.P, i0);
+    const int n0p = sm_.s0[p + 1] - sm_.s0[p];
+    eoff[s] = sm_.roff[p] + (int64_t)(r * C + a) * og.Q * n0p + (int64_t)(live ? ql : 0) * n0p + (i0 - sm_.s0[p]);
+  }
+  double2 v[1][9];
+#pragma unroll
+  for (int s = 0; s < 9; ++s) v[0][s] = live ? W[eoff[s]] : make_double2(0.0, 0.0);
+  double2* smp = sm + (size_t)(a * og.QB + qq) * L;
+  fft_reg<L, 1, false>(v, smp, L, j, tw);
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 9; ++s) smp[j + s * TP] = v[0][s];
+  __syncthreads();
+  double xi1 = 0.0, xi2 = 0.0;
+  if (C == 2) {
+    xi1 = g.xi[1][q];
+  } else {
+    const int k2 = q / og.n1, k1 = q - k2 * og.n1;
+    xi1 = g.xi[1][k1];
+    xi2 = g.xi[2][k2];
+  }
+  const double xia = a == 0 ? 0.0 : (a == 1 ? xi1 : xi2);  // xi_a for a >= 1 (a = 0 uses xi0 below)
+  const bool qzero = live && q == 0;
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+    const int i0 = j + s * TP;
+    const double xi0 = g.xi[0][i0];
+    if (qzero && i0 == 0) {
+      v[0][s] = make_double2(0.0, 0.0);
+      continue;
+    }
+    double xi[3] = {xi0, xi1, xi2};
+    double2 vb[C];
+#pragma unroll
+    for (int b = 0; b < C; ++b) vb[b] = sm[(size_t)(b * og.QB + qq) * L + i0];
+    double2 dots = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int b = 0; b < C; ++b) {
+      dots.x += xi[b] * vb[b].x;
+      dots.y += xi[b] * vb[b].y;
+    }
+    double den = 0.0;
+    if (og.orth) {
+#pragma unroll
+      for (int b = 0; b < C; ++b) den += xi[b] * xi[b];
+    } else {
+#pragma unroll
+      for (int b = 0; b < C; ++b)
+#pragma unroll
+        for (int e = 0; e < C; ++e) den += xi[b] * og.M[b][e] * xi[e];
+    }
+    const double inv = 1.0 / den;
+    const double xa = a == 0 ? xi0 : xia;
+    v[0][s] = make_double2(xa * (dots.x * inv), xa * (dots.y * inv));
+  }
+  fft_reg<L, 1, true>(v, smp, L, j, tw);
+  if (!live) return;
+#pragma unroll
+  for (int s = 0; s < 9; ++s) W[eoff[s]] = v[0][s];
 }
 
 }  // namespace fc
