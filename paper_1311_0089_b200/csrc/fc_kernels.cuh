@@ -429,9 +429,24 @@ __device__ __forceinline__ void with_ep_mode(int mode, F&& f) {
   }
 }
 
+// Warp sum over the lanes that exist (the last warp of a 243-thread CTA is
+// partial; absent partners contribute nothing).  Fixed xor tree: deterministic.
+__device__ __forceinline__ double warp_sum(double v) {
+  const int lane = threadIdx.x & 31;
+  const int base = threadIdx.x & ~31;
+  const int nact = min(32, (int)blockDim.x - base);
+  const unsigned mask = nact == 32 ? 0xffffffffu : ((1u << nact) - 1u);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double other = __shfl_xor_sync(mask, v, o);
+    if ((lane ^ o) < nact) v += other;
+  }
+  return v;
+}
+
 // Deterministic block sum (fixed shuffle tree + fixed cross-warp order).
 __device__ __forceinline__ double block_sum(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  v = warp_sum(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   __syncthreads();
   if (l == 0) red[w] = v;
