@@ -22,6 +22,11 @@
 #include "../../include/fftcell_b200.h"
 #include "fc_kernels.cuh"
 #include "fc_kernels_reg.cuh"
+#include "fc_kernels_pipe.cuh"
+
+// Field allocations carry this many spare bytes: 16-byte-aligned bulk copies
+// (fc_tma.cuh) of a row block may read up to 8 bytes past its last element.
+constexpr size_t kFieldPad = 64;
 
 using namespace fc;
 
@@ -177,6 +182,9 @@ struct fc_ctx {
   int aniso_split = 1;      // packed coefficients: pointwise kernel + staged row FFT
   int outer_persist = 0;    // persistent double-buffered outer sweep (FC_OUTER_PERSIST)
   int outer_c1 = 0;         // one-component-per-thread outer sweep: pencil groups per CTA (0 = off)
+  int row_pipe = 0;         // persistent double-buffered first sweep (FC_ROW_PIPE)
+  int row_pipe_blocks = 0;  // its resident CTAs per SM
+  size_t smem_row_pp = 0;
   size_t smem_aniso_r = 0;
   size_t smem_row_r = 0, smem_row_inv_r = 0, smem_mid_r = 0, smem_outer_r = 0;
 
@@ -393,6 +401,8 @@ int choose_tiles(fc_ctx* c) {
     // doubles), last sweep p / e (2 npen L doubles)
     c->smem_row_r = (size_t)24 * (((size_t)2 * npen * rg.nl + 3) & ~(size_t)1);
     c->inv_prefetch = env_int("FC_INV_PREFETCH", 0);
+    c->row_pipe = env_int("FC_ROW_PIPE", 0) && rg.nl >= 81;
+    c->smem_row_pp = (size_t)2 * 3 * 8 * ((2 * rg.nl + 3) & ~1);
     c->smem_row_inv_r = (size_t)16 * npen * (rg.nl + 1) + (c->inv_prefetch ? (size_t)16 * npen * rg.nl : 0);
     c->aniso_split = env_int("FC_ANISO_SPLIT", 1);
     rg.exp_natural = env_int("FC_EXP_NATURAL_STORE", 0);
@@ -462,6 +472,7 @@ int allow_reg_smem(int mx) {
   for (int L : {9, 27, 81, 243, 729, 2187}) {
     FC_POW3_SWITCH(L, {
       al(k_row_fwd_r<LL>);
+      al(k_row_fwd_pp<LL>);
       al(k_row_fwd_aniso_r<LL>);
       al(k_row_inv_r<LL>);
       al(k_mid_r<LL, false>);
@@ -490,11 +501,11 @@ int ensure_workspace(fc_ctx* c, int R, int hcap) {
     c->st = nullptr;
     c->Rcap = 0;
     const size_t fb = sizeof(double) * field * R;
-    CK(cudaMalloc(&c->x, fb));
-    CK(cudaMalloc(&c->r, fb));
-    CK(cudaMalloc(&c->p[0], fb));
-    CK(cudaMalloc(&c->p[1], fb));
-    CK(cudaMalloc(&c->Ap, fb));
+    CK(cudaMalloc(&c->x, fb + kFieldPad));
+    CK(cudaMalloc(&c->r, fb + kFieldPad));
+    CK(cudaMalloc(&c->p[0], fb + kFieldPad));
+    CK(cudaMalloc(&c->p[1], fb + kFieldPad));
+    CK(cudaMalloc(&c->Ap, fb + kFieldPad));
     if (d >= 2) {
       int64_t spec = (int64_t)R * d * c->N / c->n[d - 1] * ((c->n[d - 1] + 1) / 2);
       CK(cudaMalloc(&c->W2, sizeof(double2) * spec));
@@ -531,6 +542,37 @@ int ensure_workspace(fc_ctx* c, int R, int hcap) {
 
 int64_t nslot_row(const fc_ctx* c) { return c->dim == 1 ? 1 : (int64_t)c->rg.no * c->rg.ntiles * c->dim; }
 int64_t nslot_vec(const fc_ctx* c) { return ((int64_t)c->dim * c->N + kVecTile - 1) / kVecTile; }
+
+// Persistent double-buffered first sweep (fc_kernels_pipe.cuh): only for
+// inputs that every tile stages (isotropic coefficients or raw fields; a
+// fixed-point reference without off-diagonal entries), as in k_row_fwd_r.
+bool row_pipe_ok(const fc_ctx* c, const InArgs& ia) {
+  if (c->row_pipe_blocks <= 0) return false;
+  if (ia.mode == IN_RAW) return true;
+  if (c->coef_kind != 0 || ia.mode == IN_CONST) return false;
+  if (ia.mode == IN_FP)
+    for (int a = 0; a < c->dim; ++a)
+      for (int b = 0; b < c->dim; ++b)
+        if (a != b && ia.A0[a][b] != 0.0) return false;
+  return true;
+}
+
+int launch_row_fwd_pp(fc_ctx* c, int R, const InArgs& ia, const RhsState* st, double2* Wrow) {
+  const Geo g = c->geo();
+  const Coef C = c->coef();
+  RowGeo rp = c->rg;
+  rp.B = 2;
+  rp.ntiles = (rp.np + 1) / 2;
+  const int64_t ntile = (int64_t)R * rp.no * rp.ntiles * c->dim;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntile, (int64_t)c->num_sms * c->row_pipe_blocks);
+  const int nt = rp.nl / 9;
+  const double2* tw = c->rtw(rp.nl);
+  const size_t smem = c->smem_row_pp;
+  cudaStream_t s = c->stream;
+  return launch(c, "row_fwd", [&] {
+    FC_POW3_SWITCH(rp.nl, (k_row_fwd_pp<LL><<<grid, nt, smem, s>>>(g, rp, C, ia, st, tw, Wrow, ntile)));
+  });
+}
 
 // One operator application over R fields, in three phases so a sharded run can
 // exchange spectra between them: 0 = first sweep (+ forward middle sweep),
@@ -584,9 +626,13 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     raw.u = y;
     const int nt = c->row_npen * (rg.nl / 9);
     const double2* tw = c->rtw(rg.nl);
-    TRY(launch(c, "row_fwd", [&] {
-      FC_POW3_SWITCH(rg.nl, (k_row_fwd_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, C, raw, st, tw, Wrow)));
-    }));
+    if (c->row_pipe && row_pipe_ok(c, raw)) {
+      TRY(launch_row_fwd_pp(c, R, raw, st, Wrow));
+    } else {
+      TRY(launch(c, "row_fwd", [&] {
+        FC_POW3_SWITCH(rg.nl, (k_row_fwd_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, C, raw, st, tw, Wrow)));
+      }));
+    }
   } else if (c->aniso_npen && C.kind == 1) {
     const int nt = d * c->aniso_npen * (rg.nl / 9);
     const double2* tw = c->rtw(rg.nl);
@@ -598,6 +644,8 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     TRY(launch(c, "row_fwd", [&] {
       FC_POW3_SWITCH(rg.nl, (k_row_fwd_aniso_r<LL><<<(unsigned)nb, nt, c->smem_aniso_r, s>>>(g, ra, C, ia, st, tw, Wrow, np_)));
     }));
+  } else if (c->row_npen && c->row_pipe && row_pipe_ok(c, ia)) {
+    TRY(launch_row_fwd_pp(c, R, ia, st, Wrow));
   } else if (c->row_npen) {
     const int nt = c->row_npen * (rg.nl / 9);
     const double2* tw = c->rtw(rg.nl);
@@ -814,6 +862,11 @@ int create_slab(fc_ctx** out, int32_t dim, const int64_t* shape, const double* h
       (rc = allow_smem(k_mid<true>, mx)) || (rc = allow_smem(k_outer, mx)) || (rc = allow_smem(k_line, mx)) ||
       (rc = allow_reg_smem(mx)))
     return fail(rc);
+  if (c->row_pipe) {
+    int nb = 0;
+    FC_POW3_SWITCH(c->rg.nl, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_row_fwd_pp<LL>, c->rg.nl / 9, c->smem_row_pp)));
+    c->row_pipe_blocks = nb;
+  }
   if (cudaMalloc(&c->any_active, sizeof(int)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "flag alloc"));
   if (cudaMalloc(&c->counter, sizeof(unsigned)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "counter alloc"));
   cudaMemset(c->counter, 0, sizeof(unsigned));
@@ -1014,7 +1067,7 @@ int32_t fc_set_coefficients(fc_ctx* c, int32_t kind, const double* host, int64_t
   if (c->A == nullptr || c->A_count != count) {
     cudaFree(c->A);
     c->A = nullptr;
-    CK(cudaMalloc(&c->A, sizeof(double) * count));
+    CK(cudaMalloc(&c->A, sizeof(double) * count + kFieldPad));
     c->A_count = count;
   }
   CK(cudaMemcpyAsync(c->A, host, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
@@ -1345,7 +1398,7 @@ int32_t fc_generate_voronoi(fc_ctx* c, int32_t n_seeds, const double* seeds, con
   if (c->A == nullptr || c->A_count != count) {
     cudaFree(c->A);
     c->A = nullptr;
-    CK(cudaMalloc(&c->A, sizeof(double) * count));
+    CK(cudaMalloc(&c->A, sizeof(double) * count + kFieldPad));
     c->A_count = count;
   }
   c->coef_kind = FC_COEF_PACKED;

@@ -4,6 +4,7 @@
 #pragma once
 #include "fc_fft_reg.cuh"
 #include "fc_kernels.cuh"
+#include "fc_tma.cuh"
 
 namespace fc {
 
@@ -87,14 +88,25 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, 
     double* st_a = st_p + stride;
     const int n = nrows * L;
     const int64_t ub = ev.base + (int64_t)a * g.N + vbase;
-    const int su = stage_doubles16(st_u, ev.u + ub, n);
-    const int sp = (ev.mode == IN_PNEW && !ev.first) ? stage_doubles16(st_p, ev.p_old + ub, n) : 0;
-    const int sa = ev.mode != IN_RAW ? stage_doubles16(st_a, ev.A + vbase, n) : 0;
+    // one thread stages the row block with bulk copies (TMA); the CTA waits on bar
+    __shared__ uint64_t bar;
+    const bool use_p = ev.mode == IN_PNEW && !ev.first;
+    const bool use_a = ev.mode != IN_RAW;
+    const int su = bulk_shift(ev.u + ub);
+    const int sp = use_p ? bulk_shift(ev.p_old + ub) : 0;
+    const int sa = use_a ? bulk_shift(ev.A + vbase) : 0;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_expect_tx(&bar, bulk_bytes(n, su) + (use_p ? bulk_bytes(n, sp) : 0u) + (use_a ? bulk_bytes(n, sa) : 0u));
+      bulk_g2s(st_u, ev.u + ub - su, bulk_bytes(n, su), &bar);
+      if (use_p) bulk_g2s(st_p, ev.p_old + ub - sp, bulk_bytes(n, sp), &bar);
+      if (use_a) bulk_g2s(st_a, ev.A + vbase - sa, bulk_bytes(n, sa), &bar);
+    }
     st_u += su;
     st_p += sp;
     st_a += sa;
-    cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();  // barrier initialised before anyone polls it
+    mbar_wait(&bar, 0);
     double* pw = ia.p_new + ub;
     const double A0aa = InEval::sel(a, ev.R0, ev.R1, ev.R2);
 #pragma unroll
