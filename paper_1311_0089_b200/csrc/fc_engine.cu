@@ -6,6 +6,8 @@
 // per-RHS scalars (alpha, beta, stop flags, histories) in device memory.  The
 // host only enqueues iterations and polls one pinned flag, one iteration
 // behind, so the stream never drains between iterations.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -183,6 +185,7 @@ struct fc_ctx {
   int outer_persist = 0;    // persistent double-buffered outer sweep (FC_OUTER_PERSIST)
   int outer_c1 = 0;         // one-component-per-thread outer sweep: pencil groups per CTA (0 = off)
   int row_pipe = 0;         // persistent double-buffered first sweep (FC_ROW_PIPE)
+  CUtensorMap tmW{};        // TMA view of the row-sweep spectrum (RowGeo::tma)
   int row_pipe_blocks = 0;  // its resident CTAs per SM
   size_t smem_row_pp = 0;
   size_t smem_aniso_r = 0;
@@ -403,7 +406,13 @@ int choose_tiles(fc_ctx* c) {
     c->inv_prefetch = env_int("FC_INV_PREFETCH", 0);
     c->row_pipe = env_int("FC_ROW_PIPE", 0) && rg.nl >= 81;
     c->smem_row_pp = (size_t)2 * 3 * 8 * ((2 * rg.nl + 3) & ~1);
-    c->smem_row_inv_r = (size_t)16 * npen * (rg.nl + 1) + (c->inv_prefetch ? (size_t)16 * npen * rg.nl : 0);
+    // TMA boxes of the transposed spectrum: nbox boxes of boxK modes x 2 npen rows
+    rg.nbox = (rg.hl + 255) / 256;
+    rg.boxK = ((rg.hl + rg.nbox - 1) / rg.nbox + 3) & ~3;  // boxes start 128-byte aligned in smem
+    const size_t ybytes = (size_t)16 * rg.nbox * rg.boxK * 2 * npen;
+    c->smem_row_r = std::max(c->smem_row_r, (size_t)16 * (((size_t)npen * rg.nl + 7) & ~(size_t)7) + ybytes);
+    c->smem_row_inv_r = std::max((size_t)16 * npen * (rg.nl + 1), ybytes) +
+                        (c->inv_prefetch ? (size_t)16 * npen * rg.nl : 0);
     c->aniso_split = env_int("FC_ANISO_SPLIT", 1);
     rg.exp_natural = env_int("FC_EXP_NATURAL_STORE", 0);
     // packed coefficients: one CTA per row block for all components (its own
@@ -488,6 +497,36 @@ int allow_reg_smem(int mx) {
   return rc;
 }
 
+// TMA tensor map over the row-sweep spectrum (d >= 2, register path): doubles
+// {2 np, hl, Rcap c no}, box {2B, boxK, 1} (fc_tma.cuh).  The driver entry point
+// is resolved through the runtime, so libcuda is not linked.  FC_ROW_TMA=0
+// keeps the per-thread transposed loads / stores.
+int make_row_tmap(fc_ctx* c) {
+  RowGeo& rg = c->rg;
+  rg.tma = 0;
+  const char* env = getenv("FC_ROW_TMA");
+  if (c->dim < 2 || !c->row_npen || rg.nbox == 0 || (env && atoi(env) == 0)) return FC_OK;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (encode == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return set_err(FC_ECUDA, "cuTensorMapEncodeTiled is unavailable");
+  }
+  void* base = c->dim == 3 ? (void*)c->W1 : (void*)c->W2;
+  const int B = 2 * c->row_npen;
+  cuuint64_t dims[3] = {(cuuint64_t)2 * rg.np, (cuuint64_t)rg.hl, (cuuint64_t)c->Rcap * c->dim * rg.no};
+  cuuint64_t strides[2] = {(cuuint64_t)16 * rg.np, (cuuint64_t)16 * rg.np * rg.hl};
+  cuuint32_t box[3] = {(cuuint32_t)(2 * B), (cuuint32_t)rg.boxK, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  const CUresult rc = encode(&c->tmW, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) return set_err(FC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)rc);
+  rg.tma = 1;
+  return FC_OK;
+}
+
 int ensure_workspace(fc_ctx* c, int R, int hcap) {
   const int d = c->dim;
   const int64_t field = (int64_t)d * c->N;
@@ -519,6 +558,7 @@ int ensure_workspace(fc_ctx* c, int R, int hcap) {
     }
     CK(cudaMalloc(&c->st, sizeof(RhsState) * R));
     c->Rcap = R;
+    TRY(make_row_tmap(c));
   }
   // partial-sum slots: max over row sweeps, vector tiles, energy chunks
   int64_t nslot_row = d == 1 ? 1 : (int64_t)c->rg.no * c->rg.ntiles * d;
@@ -630,7 +670,7 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
       TRY(launch_row_fwd_pp(c, R, raw, st, Wrow));
     } else {
       TRY(launch(c, "row_fwd", [&] {
-        FC_POW3_SWITCH(rg.nl, (k_row_fwd_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, C, raw, st, tw, Wrow)));
+        FC_POW3_SWITCH(rg.nl, (k_row_fwd_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, C, raw, st, tw, Wrow, c->tmW)));
       }));
     }
   } else if (c->aniso_npen && C.kind == 1) {
@@ -650,7 +690,7 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     const int nt = c->row_npen * (rg.nl / 9);
     const double2* tw = c->rtw(rg.nl);
     TRY(launch(c, "row_fwd", [&] {
-      FC_POW3_SWITCH(rg.nl, (k_row_fwd_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, C, ia, st, tw, Wrow)));
+      FC_POW3_SWITCH(rg.nl, (k_row_fwd_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, C, ia, st, tw, Wrow, c->tmW)));
     }));
   } else {
     const FftPlan pl_last = c->plan(rg.nl);
@@ -707,7 +747,7 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     const int nt = c->row_npen * (rg.nl / 9);
     const double2* tw = c->rtw(rg.nl);
     return launch(c, "row_inv", [&] {
-      FC_POW3_SWITCH(rg.nl, (k_row_inv_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_inv_r, s>>>(g, rg, ea, st, tw, Wrow, c->inv_prefetch)));
+      FC_POW3_SWITCH(rg.nl, (k_row_inv_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_inv_r, s>>>(g, rg, ea, st, tw, Wrow, c->inv_prefetch, c->tmW)));
     });
   }
   const FftPlan pl_last = c->plan(rg.nl);

@@ -53,9 +53,11 @@ constexpr int kMaxBlockOuter = 256;
 // memory once more to split the two-for-one pairs and to store transposed.
 template <int L>
 __global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, InArgs ia, const RhsState* st,
-                                                          const double2* __restrict__ tw, double2* __restrict__ W) {
+                                                          const double2* __restrict__ tw, double2* __restrict__ W,
+                                                          const __grid_constant__ CUtensorMap tmW) {
   constexpr int TP = R9<L>::TP;
-  extern __shared__ double2 sm[];
+  extern __shared__ __align__(128) unsigned char smraw[];  // TMA boxes need 128-byte alignment
+  double2* sm = reinterpret_cast<double2*>(smraw);
   const int c = g.dim;
   int64_t bid = blockIdx.x;
   const int a = bid % c; bid /= c;
@@ -176,8 +178,32 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, 
     }
     return;
   }
-  // split Z = Ye + i Yo into the two half spectra; one thread per (pair, k)
   const int npairs = (nrows + 1) >> 1;
+  if (rg.tma) {
+    // split into Y[k][row] (complex) behind the pencils, then TMA-store the boxes
+    // (the store clips rows >= np and modes >= hl)
+    const int B = rg.B;
+    double2* Y = sm + (((size_t)(B / 2) * L + 7) & ~(size_t)7);
+    for (int idx = threadIdx.x; idx < hl * npairs; idx += blockDim.x) {
+      const int k = idx / npairs;
+      const int pr = idx - k * npairs;
+      const double2* z = sm + (size_t)pr * L;
+      const double2 zk = z[k];
+      const double2 zm = z[k == 0 ? 0 : L - k];
+      Y[k * B + 2 * pr] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+      Y[k * B + 2 * pr + 1] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int c2 = (r * c + a) * rg.no + o;
+      for (int b = 0; b < rg.nbox; ++b) tma_store_3d(&tmW, 2 * row0, b * rg.boxK, c2, Y + (size_t)b * rg.boxK * B);
+      bulk_commit();
+      bulk_wait_read0();
+    }
+    return;
+  }
+  // split Z = Ye + i Yo into the two half spectra; one thread per (pair, k)
   for (int idx = threadIdx.x; idx < hl * npairs; idx += blockDim.x) {
     const int pr = idx / hl;
     const int k = idx - pr * hl;
@@ -195,10 +221,12 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, 
 template <int L>
 __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs ea, const RhsState* st,
                                                           const double2* __restrict__ tw,
-                                                          const double2* __restrict__ W, int prefetch) {
+                                                          const double2* __restrict__ W, int prefetch,
+                                                          const __grid_constant__ CUtensorMap tmW) {
   constexpr int TP = R9<L>::TP;
   constexpr int hl = (L + 1) / 2;
-  extern __shared__ double2 sm[];
+  extern __shared__ __align__(128) unsigned char smraw[];  // TMA boxes need 128-byte alignment
+  double2* sm = reinterpret_cast<double2*>(smraw);
   __shared__ double red[kMaxBlock / 32];
   const int c = g.dim;
   int64_t bid = blockIdx.x;
@@ -217,12 +245,25 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   const int64_t ebase = ((int64_t)r * c + a) * g.N + vbase;
   // epilogue input (p for EP_AP, e for EP_FP) prefetched with cp.async into the
   // area behind the exchange buffer; it lands while the spectrum is transformed
-  double* st_q = reinterpret_cast<double*>(sm + (size_t)(rg.B / 2) * (L + 1));
+  const size_t ystage = rg.tma ? (size_t)rg.nbox * rg.boxK * rg.B : 0;
+  double* st_q = reinterpret_cast<double*>(sm + max((size_t)(rg.B / 2) * (L + 1), ystage));
   const bool need_q = ea.mode == EP_AP || ea.mode == EP_FP;
   const double* qsrc = (ea.mode == EP_AP ? ea.p : ea.out) + ebase;
   if (need_q && prefetch) stage_doubles(st_q, qsrc, nrows * L);
-  // Y[row][k] staged at sm[row * hl + k]; one thread per (pair, k), 4 in flight
-  {
+  // Y staged at sm[k * yk + row * yr]: TMA boxes give [k][row], the fallback [row][k]
+  __shared__ uint64_t bar;
+  const int yk = rg.tma ? rg.B : 1;
+  const int yr = rg.tma ? 1 : hl;
+  if (rg.tma) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_expect_tx(&bar, (unsigned)(rg.nbox * rg.boxK * rg.B * 16));
+      const int c2 = (r * c + a) * rg.no + o;
+      for (int b = 0; b < rg.nbox; ++b) tma_load_3d(sm + (size_t)b * rg.boxK * rg.B, &tmW, 2 * row0, b * rg.boxK, c2, &bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+  } else {
     const int npairs = (nrows + 1) >> 1;
     const int total = hl * npairs;
     for (int base = 0; base < total; base += 4 * blockDim.x) {
@@ -258,8 +299,8 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   for (int s = 0; s < 9; ++s) {
     const int i = j + s * TP;
     const int k = i < hl ? i : L - i;
-    double2 ye = re < nrows ? sm[re * hl + k] : make_double2(0.0, 0.0);
-    double2 yo = has_o ? sm[ro * hl + k] : make_double2(0.0, 0.0);
+    double2 ye = re < nrows ? sm[k * yk + re * yr] : make_double2(0.0, 0.0);
+    double2 yo = has_o ? sm[k * yk + ro * yr] : make_double2(0.0, 0.0);
     if (i == 0) v[0][s] = make_double2(ye.x, yo.x);
     else if (i < hl) v[0][s] = make_double2(ye.x - yo.y, ye.y + yo.x);
     else v[0][s] = make_double2(ye.x + yo.y, yo.x - ye.y);

@@ -63,3 +63,34 @@ __device__ __forceinline__ int bulk_stage_doubles(double* dst, const double* src
 }
 
 }  // namespace fc
+
+// ---- tiled tensor copies (cuTensorMapEncodeTiled maps built on the host) ----
+#include <cuda.h>
+
+namespace fc {
+
+// 3-D box load global -> shared (coordinates innermost first), completes on bar
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+// 3-D box store shared -> global (out-of-range parts of the box are clipped)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+// wait until the smem sources of all committed bulk stores have been read
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+
+// Row-spectrum view for the tensor maps: the half spectrum of a row sweep is
+// stored transposed, W[(r*c + a)*no + o][k][row] (complex), i.e. a 3-D array of
+// doubles {2*np, hl, R*c*no}.  A box {4, kBoxK, 1} = rows (row0, row0+1) of
+// kBoxK consecutive modes; in shared memory it lands as [k][2] complex.
+constexpr int kBoxK = 256;
+
+}  // namespace fc
