@@ -405,14 +405,14 @@ int choose_tiles(fc_ctx* c) {
     c->smem_row_r = (size_t)24 * (((size_t)2 * npen * rg.nl + 3) & ~(size_t)1);
     c->inv_prefetch = env_int("FC_INV_PREFETCH", 0);
     c->row_pipe = env_int("FC_ROW_PIPE", 0) && rg.nl >= 81;
-    c->smem_row_pp = (size_t)2 * 3 * 8 * ((2 * rg.nl + 3) & ~1);
+    c->smem_row_pp = (size_t)2 * 8 * ((3 * ((2 * rg.nl + 3) & ~1) + 15) & ~15);
     // TMA boxes of the transposed spectrum: nbox boxes of boxK modes x 2 npen rows
     rg.nbox = (rg.hl + 255) / 256;
     rg.boxK = ((rg.hl + rg.nbox - 1) / rg.nbox + 3) & ~3;  // boxes start 128-byte aligned in smem
     const size_t ybytes = (size_t)16 * rg.nbox * rg.boxK * 2 * npen;
     c->smem_row_r = std::max(c->smem_row_r, (size_t)16 * (((size_t)npen * rg.nl + 7) & ~(size_t)7) + ybytes);
     c->smem_row_inv_r = std::max((size_t)16 * npen * (rg.nl + 1), ybytes) +
-                        (c->inv_prefetch ? (size_t)16 * npen * rg.nl : 0);
+                        (c->inv_prefetch ? (size_t)16 * npen * rg.nl + 16 : 0);
     c->aniso_split = env_int("FC_ANISO_SPLIT", 1);
     rg.exp_natural = env_int("FC_EXP_NATURAL_STORE", 0);
     // packed coefficients: one CTA per row block for all components (its own
@@ -587,7 +587,7 @@ int64_t nslot_vec(const fc_ctx* c) { return ((int64_t)c->dim * c->N + kVecTile -
 // inputs that every tile stages (isotropic coefficients or raw fields; a
 // fixed-point reference without off-diagonal entries), as in k_row_fwd_r.
 bool row_pipe_ok(const fc_ctx* c, const InArgs& ia) {
-  if (c->row_pipe_blocks <= 0) return false;
+  if (c->row_pipe_blocks <= 0 || !c->rg.tma || c->row_npen != 1) return false;
   if (ia.mode == IN_RAW) return true;
   if (c->coef_kind != 0 || ia.mode == IN_CONST) return false;
   if (ia.mode == IN_FP)
@@ -610,7 +610,7 @@ int launch_row_fwd_pp(fc_ctx* c, int R, const InArgs& ia, const RhsState* st, do
   const size_t smem = c->smem_row_pp;
   cudaStream_t s = c->stream;
   return launch(c, "row_fwd", [&] {
-    FC_POW3_SWITCH(rp.nl, (k_row_fwd_pp<LL><<<grid, nt, smem, s>>>(g, rp, C, ia, st, tw, Wrow, ntile)));
+    FC_POW3_SWITCH(rp.nl, (k_row_fwd_pp<LL><<<grid, nt, smem, s>>>(g, rp, C, ia, st, tw, ntile, c->tmW)));
   });
 }
 

@@ -52,11 +52,12 @@ template <bool INV>
 __device__ __forceinline__ void bfly3(double2& x0, double2& x1, double2& x2) {
   const double s = INV ? 0.86602540378443864676 : -0.86602540378443864676;
   double2 t1 = cadd(x1, x2);
-  double2 t2 = make_double2(x0.x - 0.5 * t1.x, x0.y - 0.5 * t1.y);
-  double2 t3 = cimul(s, csub(x1, x2));
+  double2 t2 = make_double2(fma(-0.5, t1.x, x0.x), fma(-0.5, t1.y, x0.y));
+  double2 d = csub(x1, x2);
   x0 = cadd(x0, t1);
-  x1 = cadd(t2, t3);
-  x2 = csub(t2, t3);
+  // t2 +- i s d as fused multiply-adds (constant input: d = 0, t2 = 0 exactly)
+  x1 = make_double2(fma(-s, d.y, t2.x), fma(s, d.x, t2.y));
+  x2 = make_double2(fma(s, d.y, t2.x), fma(-s, d.x, t2.y));
 }
 
 // ---- radix-5 -------------------------------------------------------------

@@ -331,13 +331,21 @@ __device__ __forceinline__ InEval make_eval(const InArgs& ia, const Geo& g, cons
   ev.kind = C.kind;
   ev.first = ia.mode == IN_PNEW ? st[r].first != 0 : true;
   ev.beta = ia.mode == IN_PNEW ? st[r].beta : 0.0;
-  ev.E0 = pick(ia.E, r, 0);
-  ev.E1 = pick(ia.E, r, 1);
-  ev.E2 = pick(ia.E, r, 2);
-  ev.Ea = pick(ia.E, r, a);
-  ev.R0 = pick3(ia.A0, a, 0);
-  ev.R1 = pick3(ia.A0, a, 1);
-  ev.R2 = pick3(ia.A0, a, 2);
+  // loads / reference rows only where the mode uses them (the static-index
+  // selections cost ~100 instructions per thread)
+  ev.E0 = ev.E1 = ev.E2 = ev.Ea = 0.0;
+  ev.R0 = ev.R1 = ev.R2 = 0.0;
+  if (ia.mode == IN_CONST) {
+    ev.E0 = pick(ia.E, r, 0);
+    ev.E1 = pick(ia.E, r, 1);
+    ev.E2 = pick(ia.E, r, 2);
+    ev.Ea = pick(ia.E, r, a);
+  }
+  if (ia.mode == IN_FP) {
+    ev.R0 = pick3(ia.A0, a, 0);
+    ev.R1 = pick3(ia.A0, a, 1);
+    ev.R2 = pick3(ia.A0, a, 2);
+  }
   return ev;
 }
 

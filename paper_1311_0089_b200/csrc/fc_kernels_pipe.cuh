@@ -1,0 +1,178 @@
+// Persistent, double-buffered first sweep for power-of-three contiguous axes.
+//
+// The one-shot row kernel (fc_kernels_reg.cuh: k_row_fwd_r) loads a row block,
+// transforms it and stores it, so HBM idles whenever both resident CTAs of an
+// SM transform at the same time.  Here one CTA per SM walks the row pairs
+// (tile t, t + G, t + 2G, ...) and keeps the next pair's inputs in flight while
+// the current pair is transformed: the TMA bulk loads of tile t + G land in
+// the second shared-memory stage during the FFT of tile t.
+//
+// Row block = one complex pencil (rows 2q, 2q+1).  Same layouts, modes and
+// rounding as the staged path of k_row_fwd_r; the transposed half spectrum is
+// written with TMA tensor boxes (RowGeo::tma).
+#pragma once
+#include "fc_kernels_reg.cuh"
+
+namespace fc {
+
+constexpr int FC_MAX_RHS_DEV = 8;  // = FC_MAX_RHS (include/fftcell_b200.h)
+
+// doubles per staged array of one row pair (even, room for the 16-byte phase shift)
+template <int L>
+__host__ __device__ constexpr int pipe_stride() { return (2 * L + 3) & ~1; }
+
+struct PipeTile {
+  int a, tile, o, r;
+};
+__device__ __forceinline__ PipeTile pipe_decode(int64_t t, int c, const RowGeo& rg) {
+  PipeTile q;
+  q.a = (int)(t % c); t /= c;
+  q.tile = (int)(t % rg.ntiles); t /= rg.ntiles;
+  q.o = (int)(t % rg.no);
+  q.r = (int)(t / rg.no);
+  return q;
+}
+
+// Stage layout (doubles): U[stride] P[stride] A[stride]; once the inputs sit in
+// registers the stage holds the FFT exchange buffer / spectrum z (L complex,
+// from offset 0) and the split half spectra Y[k][2] (from offset zoff).
+template <int L>
+__global__ void __launch_bounds__(256, 1) k_row_fwd_pp(Geo g, RowGeo rg, Coef C, InArgs ia, const RhsState* st,
+                                                       const double2* __restrict__ tw, int64_t ntile,
+                                                       const __grid_constant__ CUtensorMap tmW) {
+  constexpr int TP = R9<L>::TP;
+  constexpr int hl = (L + 1) / 2;
+  constexpr int stride = pipe_stride<L>();
+  constexpr int stage = (3 * stride + 15) & ~15;  // doubles; stages start 128-byte aligned
+  constexpr int zoff = (L + 7) & ~7;  // Y offset in complex (128-byte aligned boxes)
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* S = reinterpret_cast<double*>(smraw);
+  __shared__ uint64_t bar[2];
+  __shared__ double s_beta[FC_MAX_RHS_DEV];
+  __shared__ int s_flags[FC_MAX_RHS_DEV];  // bit 0 active, bit 1 first
+  const int c = g.dim;
+  const int j = threadIdx.x;  // one pencil per CTA: thread j = FFT lane
+  const int R = (int)(ntile / ((int64_t)c * rg.ntiles * rg.no));
+  if (threadIdx.x < R) {
+    const int r = threadIdx.x;
+    const bool act = rhs_active(st, r);
+    const bool first = ia.mode == IN_PNEW ? st[r].first != 0 : true;
+    s_flags[r] = (act ? 1 : 0) | (first ? 2 : 0);
+    s_beta[r] = ia.mode == IN_PNEW ? st[r].beta : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
+  __syncthreads();
+
+  // source pointers of tile t (u / p_old / A) and their 16-byte phases
+  struct Src {
+    const double *u, *p, *A;
+    int n;
+  };
+  auto sources = [&](const PipeTile& q) {
+    Src o;
+    const int row0 = q.tile * 2;
+    o.n = min(2, rg.np - row0) * L;
+    const int64_t vbase = ((int64_t)q.o * rg.np + row0) * L;
+    const int64_t ub = (int64_t)q.r * c * g.N + (int64_t)q.a * g.N + vbase;
+    const int fl = s_flags[q.r];
+    o.u = ia.u + ub;
+    o.p = (ia.mode == IN_PNEW && !(fl & 2)) ? ia.p_old + ub : nullptr;
+    o.A = ia.mode != IN_RAW ? C.A + vbase : nullptr;
+    return o;
+  };
+  // one thread issues the bulk loads of tile t into stage b
+  auto prefetch = [&](int64_t t, int b) {
+    if (t >= ntile) return;
+    const PipeTile q = pipe_decode(t, c, rg);
+    if (!(s_flags[q.r] & 1)) return;
+    const Src o = sources(q);
+    double* dst = S + b * stage;
+    const int su = bulk_shift(o.u), sp = o.p ? bulk_shift(o.p) : 0, sa = o.A ? bulk_shift(o.A) : 0;
+    mbar_expect_tx(&bar[b], bulk_bytes(o.n, su) + (o.p ? bulk_bytes(o.n, sp) : 0u) + (o.A ? bulk_bytes(o.n, sa) : 0u));
+    bulk_g2s(dst, o.u - su, bulk_bytes(o.n, su), &bar[b]);
+    if (o.p) bulk_g2s(dst + stride, o.p - sp, bulk_bytes(o.n, sp), &bar[b]);
+    if (o.A) bulk_g2s(dst + 2 * stride, o.A - sa, bulk_bytes(o.n, sa), &bar[b]);
+  };
+
+  int64_t t = blockIdx.x;
+  if (threadIdx.x == 0) {
+    prefetch(t, 0);
+    prefetch(t + gridDim.x, 1);
+  }
+  unsigned phase[2] = {0u, 0u};
+  int cur = 0;
+  for (; t < ntile; t += gridDim.x) {
+    const PipeTile q = pipe_decode(t, c, rg);
+    const int fl = s_flags[q.r];
+    double* base = S + cur * stage;
+    if (fl & 1) {
+      mbar_wait(&bar[cur], phase[cur]);
+      phase[cur] ^= 1u;
+      const int a = q.a, r = q.r;
+      const Src o = sources(q);
+      const int nrows = o.n / L;
+      const double* st_u = base + bulk_shift(o.u);
+      const double* st_p = base + stride + (o.p ? bulk_shift(o.p) : 0);
+      const double* st_a = base + 2 * stride + (o.A ? bulk_shift(o.A) : 0);
+      const bool pnew = ia.mode == IN_PNEW;
+      const bool first = (fl & 2) != 0;
+      const double beta = s_beta[r];
+      double* pw = pnew ? ia.p_new + (o.u - ia.u) : nullptr;
+      const double A0aa = ia.mode == IN_FP ? pick3(ia.A0, a, a) : 0.0;
+      double2 v[1][9];
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+        const int i = j + s * TP;
+        double y[2] = {0.0, 0.0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h < nrows) {
+            const int e = h * L + i;
+            double x = st_u[e];
+            if (pnew) {
+              x = first ? x : __dadd_rn(x, __dmul_rn(beta, st_p[e]));
+              pw[e] = x;
+            }
+            double val;
+            if (ia.mode == IN_RAW) val = x;
+            else if (ia.mode == IN_FP) val = __dmul_rn(__dsub_rn(st_a[e], A0aa), x);
+            else val = __dmul_rn(st_a[e], x);
+            if (ia.mode != IN_FP && ia.s != 1.0) val = __dmul_rn(ia.s, val);
+            y[h] = val;
+          }
+        }
+        v[0][s] = make_double2(y[0], y[1]);
+      }
+      double2* z = reinterpret_cast<double2*>(base);
+      fft_reg<L, 1, false>(v, z, L, j, tw);
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < 9; ++s) z[j + s * TP] = v[0][s];
+      __syncthreads();
+      // split Z = Ye + i Yo into the two half spectra Y[k][row]
+      double2* Y = z + zoff;
+      for (int k = threadIdx.x; k < hl; k += blockDim.x) {
+        const double2 zk = z[k];
+        const double2 zm = z[k == 0 ? 0 : L - k];
+        Y[2 * k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+        Y[2 * k + 1] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+      }
+      fence_proxy_async();  // generic writes of this stage before async-proxy use (store now, refill next)
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int c2 = (r * c + a) * rg.no + q.o;
+        for (int b = 0; b < rg.nbox; ++b) tma_store_3d(&tmW, 4 * q.tile, b * rg.boxK, c2, Y + (size_t)b * rg.boxK * 2);
+        bulk_commit();
+        bulk_wait_read0();  // the stage is refilled below
+      }
+    }
+    if (threadIdx.x == 0) prefetch(t + 2 * (int64_t)gridDim.x, cur);
+    cur ^= 1;
+  }
+  if (threadIdx.x == 0) bulk_wait_read0();
+}
+
+}  // namespace fc

@@ -249,9 +249,21 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   double* st_q = reinterpret_cast<double*>(sm + max((size_t)(rg.B / 2) * (L + 1), ystage));
   const bool need_q = ea.mode == EP_AP || ea.mode == EP_FP;
   const double* qsrc = (ea.mode == EP_AP ? ea.p : ea.out) + ebase;
-  if (need_q && prefetch) stage_doubles(st_q, qsrc, nrows * L);
+  __shared__ uint64_t bar, barq;
+  int qshift = 0;
+  if (need_q && prefetch) {
+    if (rg.tma) {  // one bulk copy on its own barrier, waited for only in the epilogue
+      qshift = bulk_shift(qsrc);
+      if (threadIdx.x == 0) {
+        mbar_init(&barq, 1);
+        mbar_expect_tx(&barq, bulk_bytes(nrows * L, qshift));
+        bulk_g2s(st_q, qsrc - qshift, bulk_bytes(nrows * L, qshift), &barq);
+      }
+    } else {
+      stage_doubles(st_q, qsrc, nrows * L);
+    }
+  }
   // Y staged at sm[k * yk + row * yr]: TMA boxes give [k][row], the fallback [row][k]
-  __shared__ uint64_t bar;
   const int yk = rg.tma ? rg.B : 1;
   const int yr = rg.tma ? 1 : hl;
   if (rg.tma) {
@@ -312,13 +324,18 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   const bool he = re < nrows;
   double2 q[9];
   if (need_q && prefetch) {
-    cp_async_wait_all();
-    __syncthreads();
+    if (rg.tma) {
+      mbar_wait(&barq, 0);
+    } else {
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    const double* sq = st_q + qshift;
 #pragma unroll
     for (int s = 0; s < 9; ++s) {
       const int i = j + s * TP;
-      q[s].x = he ? st_q[re * L + i] : 0.0;
-      q[s].y = has_o ? st_q[ro * L + i] : 0.0;
+      q[s].x = he ? sq[re * L + i] : 0.0;
+      q[s].y = has_o ? sq[ro * L + i] : 0.0;
     }
   } else if (need_q) {
 #pragma unroll
