@@ -449,6 +449,7 @@ int choose_tiles(fc_ctx* c) {
     og.nqb = (og.Q + qb - 1) / qb;
     c->outer_qb = qb;
     c->smem_outer_r = (size_t)16 * d * qb * c->n0g;
+    og.tma = env_int("FC_OUTER_TMA", 1);
     c->outer_persist = env_int("FC_OUTER_PERSIST", 0) && 2 * c->smem_outer_r <= (size_t)c->smem_optin - 2048;
     {
       // one component per thread: d * QB * TP threads (<= 512)

@@ -381,6 +381,25 @@ __device__ __forceinline__ double ep_store(const EpArgs& ea, int64_t e, double g
   }
 }
 
+// Same epilogue, value returned in o instead of stored (the caller stores it).
+template <int MODE>
+__device__ __forceinline__ double ep_value_t(double gval, double Ea, double q, double& o) {
+  if constexpr (MODE == EP_STORE) {
+    o = gval;
+    return 0.0;
+  } else if constexpr (MODE == EP_RHS) {
+    o = -gval;
+    return __dmul_rn(o, o);
+  } else if constexpr (MODE == EP_AP) {
+    o = gval;
+    return __dmul_rn(q, gval);
+  } else {
+    o = __dsub_rn(Ea, gval);
+    const double df = __dsub_rn(o, q);
+    return __dmul_rn(df, df);
+  }
+}
+
 template <int MODE>
 __device__ __forceinline__ double ep_store_t(double* __restrict__ out, int64_t e, double gval, double Ea, double q) {
   if constexpr (MODE == EP_STORE) {
@@ -570,8 +589,10 @@ __device__ void fin_logic(const FinArgs& f, int r, double sum) {
 // this CTA's partial.  The last CTA to arrive sums every RHS's slots in fixed
 // order and runs the finalize stage, so no separate finalize launch is needed.
 // Every CTA of the launch must call it exactly once (inactive RHS included).
-__device__ void finish_block(const FinArgs& f, double* red) {
-  if (f.mode == FIN_NONE) return;
+// Arrival half of finish_block: returns (uniformly) whether this CTA is the
+// last one; no barrier for FIN_NONE.
+__device__ bool arrive_block(const FinArgs& f) {
+  if (f.mode == FIN_NONE) return false;
   __shared__ int last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -581,7 +602,17 @@ __device__ void finish_block(const FinArgs& f, double* red) {
     last = prev == total - 1;
   }
   __syncthreads();
-  if (!last) return;
+  return last != 0;
+}
+
+__device__ void finalize_block(const FinArgs& f, double* red);
+
+__device__ void finish_block(const FinArgs& f, double* red) {
+  if (arrive_block(f)) finalize_block(f, red);
+}
+
+// Finalize half: the last CTA sums every RHS's slots and runs the scalar logic.
+__device__ void finalize_block(const FinArgs& f, double* red) {
   __threadfence();
   const bool init = f.mode == FIN_INIT || f.mode == FIN_INIT2;
   for (int r = 0; r < f.R; ++r) {
@@ -793,6 +824,7 @@ __global__ void __launch_bounds__(kThreads) k_mid(Geo g, MidGeo mg, const RhsSta
 // (solver.py:98-110, green.py:81-92).
 struct OuterGeo {
   int n0, Q, QB, nqb;   // Q pencils per component, QB per CTA
+  int tma = 0;          // single slab: bulk (TMA) pencil loads / stores in k_outer_r
   int R;                // right-hand sides (persistent kernel tiles over R x nqb)
   int n1, h_last;       // d = 3: q = k2 * n1 + k1 ; d = 2: q = k1
   int orth;

@@ -346,14 +346,15 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
     }
   }
   double acc = 0.0;
+  // epilogue values in registers first: the CTA's partial is published (and its
+  // arrival counted) before the output stores, so the arrival fence does not
+  // wait for them
   with_ep_mode(ea.mode, [&](auto M) {
     constexpr int MODE = decltype(M)::value;
-    double* __restrict__ out = ea.out;
 #pragma unroll
     for (int s = 0; s < 9; ++s) {
-      const int i = j + s * TP;
-      if (he) acc += ep_store_t<MODE>(out, ebase + (int64_t)re * L + i, v[0][s].x * g.invN, Ea, q[s].x);
-      if (has_o) acc += ep_store_t<MODE>(out, ebase + (int64_t)ro * L + i, v[0][s].y * g.invN, Ea, q[s].y);
+      if (he) acc += ep_value_t<MODE>(v[0][s].x * g.invN, Ea, q[s].x, v[0][s].x);
+      if (has_o) acc += ep_value_t<MODE>(v[0][s].y * g.invN, Ea, q[s].y, v[0][s].y);
     }
   });
   if (ea.part != nullptr) {
@@ -363,7 +364,17 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
       ea.part[(int64_t)r * ea.nslot + slot] = sum;
     }
   }
-  finish_block(ea.fin, red);
+  const bool last = arrive_block(ea.fin);
+  {
+    double* __restrict__ out = ea.out;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) {
+      const int i = j + s * TP;
+      if (he) out[ebase + (int64_t)re * L + i] = v[0][s].x;
+      if (has_o) out[ebase + (int64_t)ro * L + i] = v[0][s].y;
+    }
+  }
+  if (last) finalize_block(ea.fin, red);
 }
 
 // Middle sweep (d = 3), thread mapping pencil-fastest (t = j * BP + p) so the
@@ -425,7 +436,8 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
                                                                               const double2* __restrict__ tw,
                                                                               double2* __restrict__ W) {
   constexpr int TP = R9<L>::TP;
-  extern __shared__ double2 sm[];
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double2* sm = reinterpret_cast<double2*>(smraw);
   const int qb = blockIdx.x % og.nqb;
   const int r = blockIdx.x / og.nqb;
   if (!rhs_active(st, r)) return;
@@ -433,6 +445,22 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
   const int j = threadIdx.x - qq * TP;
   const int ql = qb * og.QB + qq;         // pencil index within this slab's share
   const bool live = ql < og.Q;
+  // single slab: the CTA's pencils of component a are one contiguous block
+  // W[r][a][q0 .. q0+nq)[n0]; bulk-load it to smem as [a][qq][L] (TMA)
+  const int nq = min(og.QB, og.Q - qb * og.QB);
+  const bool bulk = og.tma && sm_.P == 1;
+  __shared__ uint64_t bar;
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_expect_tx(&bar, (unsigned)(C * nq * L * 16));
+#pragma unroll
+      for (int a = 0; a < C; ++a)
+        bulk_g2s(sm + (size_t)a * og.QB * L, W + ((int64_t)(r * C + a) * og.Q + (int64_t)qb * og.QB) * L,
+                 (unsigned)(nq * L * 16), &bar);
+    }
+    __syncthreads();
+  }
   const int q = sm_.qs[sm_.me] + (live ? ql : 0);  // global (k2, k1) pencil index
   // element offsets of this pencil's axis-0 entries in the received segments
   // element offsets of this pencil's axis-0 entries: one contiguous pencil for
@@ -455,11 +483,20 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
     }
   }
   double2 v[C][9];
+  if (bulk) {
+    mbar_wait(&bar, 0);
 #pragma unroll
-  for (int a = 0; a < C; ++a) {
+    for (int a = 0; a < C; ++a)
 #pragma unroll
-    for (int s = 0; s < 9; ++s)
-      v[a][s] = live ? W[eoff[s] + (int64_t)(r * C + a) * cstride[s]] : make_double2(0.0, 0.0);
+      for (int s = 0; s < 9; ++s)
+        v[a][s] = live ? sm[((size_t)a * og.QB + qq) * L + j + s * TP] : make_double2(0.0, 0.0);
+  } else {
+#pragma unroll
+    for (int a = 0; a < C; ++a) {
+#pragma unroll
+      for (int s = 0; s < 9; ++s)
+        v[a][s] = live ? W[eoff[s] + (int64_t)(r * C + a) * cstride[s]] : make_double2(0.0, 0.0);
+    }
   }
   double2* smp = sm + (size_t)qq * C * L;
   fft_reg<L, C, false>(v, smp, L, j, tw);
@@ -506,6 +543,24 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
     for (int a = 0; a < C; ++a) v[a][s] = make_double2(xi[a] * qv.x, xi[a] * qv.y);
   }
   fft_reg<L, C, true>(v, smp, L, j, tw);
+  if (bulk) {  // back through smem ([a][qq][L]) and one bulk store per component
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < C; ++a)
+#pragma unroll
+      for (int s = 0; s < 9; ++s) sm[((size_t)a * og.QB + qq) * L + j + s * TP] = v[a][s];
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int a = 0; a < C; ++a)
+        bulk_s2g(W + ((int64_t)(r * C + a) * og.Q + (int64_t)qb * og.QB) * L, sm + (size_t)a * og.QB * L,
+                 (unsigned)(nq * L * 16));
+      bulk_commit();
+      bulk_wait_read0();
+    }
+    return;
+  }
   if (!live) return;
 #pragma unroll
   for (int a = 0; a < C; ++a) {

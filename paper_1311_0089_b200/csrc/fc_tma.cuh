@@ -83,6 +83,11 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int
                "r"(c1), "r"(c2), "r"(smem_u32(src))
                : "memory");
 }
+// shared -> global bulk store (bytes a multiple of 16, 16-byte aligned), bulk_group completion
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 // wait until the smem sources of all committed bulk stores have been read
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
