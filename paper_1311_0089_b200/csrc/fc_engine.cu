@@ -188,6 +188,9 @@ struct fc_ctx {
   CUtensorMap tmW{};        // TMA view of the row-sweep spectrum (RowGeo::tma)
   int row_pipe_blocks = 0;  // its resident CTAs per SM
   size_t smem_row_pp = 0;
+  int inv_pipe_blocks = 0;  // persistent double-buffered last sweep (FC_INV_PIPE): CTAs per SM
+  int inv_pipe_stage = 0;   // its stage size (complex)
+  int inv_pipe_nst = 2;     // its number of stages (FC_INV_STAGES, 2..4)
   size_t smem_aniso_r = 0;
   size_t smem_row_r = 0, smem_row_inv_r = 0, smem_mid_r = 0, smem_outer_r = 0;
 
@@ -476,6 +479,16 @@ int choose_tiles(fc_ctx* c) {
     default: break;                      \
   }
 
+int env_int_g(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+bool env_flag(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v ? atoi(v) : dflt) != 0;
+}
+
 int allow_reg_smem(int mx) {
   int rc = FC_OK;
   auto al = [&](auto k) { if (rc == FC_OK) rc = allow_smem(k, mx); };
@@ -744,6 +757,18 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
   }
   if (!(phases & PH_INV)) return FC_OK;
   if (d == 3) TRY(mid(true));
+  if (c->row_npen && c->rg.tma && c->inv_pipe_blocks > 0) {
+    const int nt = c->row_npen * (rg.nl / 9);
+    const double2* tw = c->rtw(rg.nl);
+    const int64_t ntile = nrow_blocks;
+    const unsigned grid = (unsigned)std::min<int64_t>(ntile, (int64_t)c->num_sms * c->inv_pipe_blocks);
+    const int stage_c = c->inv_pipe_stage;
+    const int nst = c->inv_pipe_nst;
+    const size_t smem = (size_t)nst * 16 * stage_c;
+    return launch(c, "row_inv", [&] {
+      FC_POW3_SWITCH(rg.nl, (k_row_inv_pp<LL><<<grid, nt, smem, s>>>(g, rg, ea, st, tw, ntile, stage_c, nst, c->tmW)));
+    });
+  }
   if (c->row_npen) {
     const int nt = c->row_npen * (rg.nl / 9);
     const double2* tw = c->rtw(rg.nl);
@@ -903,6 +928,23 @@ int create_slab(fc_ctx** out, int32_t dim, const int64_t* shape, const double* h
       (rc = allow_smem(k_mid<true>, mx)) || (rc = allow_smem(k_outer, mx)) || (rc = allow_smem(k_line, mx)) ||
       (rc = allow_reg_smem(mx)))
     return fail(rc);
+  // measured: faster for one pencil per block (L = 2187, cfg2), slower for the
+  // short rows of cfg3 / cfg4 (L = 243 / 729: many pencils per block)
+  if (c->row_npen && env_flag("FC_INV_PIPE", c->row_npen == 1)) {
+    const RowGeo& rg = c->rg;
+    const int B = 2 * c->row_npen;
+    c->inv_pipe_stage = (std::max(rg.nbox * rg.boxK * B, c->row_npen * (rg.nl + 1)) + 7) & ~7;
+    c->inv_pipe_nst = std::max(2, std::min(4, env_int_g("FC_INV_STAGES", 2)));
+    size_t smem = (size_t)c->inv_pipe_nst * 16 * c->inv_pipe_stage;
+    while (c->inv_pipe_nst > 2 && 2 * (smem + 2048) > (size_t)c->smem_optin) {  // keep 2 CTAs per SM
+      --c->inv_pipe_nst;
+      smem = (size_t)c->inv_pipe_nst * 16 * c->inv_pipe_stage;
+    }
+    int nb = 0;
+    FC_POW3_SWITCH(rg.nl, (allow_smem(k_row_inv_pp<LL>, mx),
+                           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_row_inv_pp<LL>, c->row_npen * (rg.nl / 9), smem)));
+    c->inv_pipe_blocks = nb;
+  }
   if (c->row_pipe) {
     int nb = 0;
     FC_POW3_SWITCH(c->rg.nl, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_row_fwd_pp<LL>, c->rg.nl / 9, c->smem_row_pp)));

@@ -102,15 +102,15 @@ __global__ void __launch_bounds__(256, 1) k_row_fwd_pp(Geo g, RowGeo rg, Coef C,
     prefetch(t, 0);
     prefetch(t + gridDim.x, 1);
   }
-  unsigned phase[2] = {0u, 0u};
+  unsigned phases = 0u;  // bit b: parity of stage b's next completion (no local array)
   int cur = 0;
   for (; t < ntile; t += gridDim.x) {
     const PipeTile q = pipe_decode(t, c, rg);
     const int fl = s_flags[q.r];
     double* base = S + cur * stage;
     if (fl & 1) {
-      mbar_wait(&bar[cur], phase[cur]);
-      phase[cur] ^= 1u;
+      mbar_wait(&bar[cur], (phases >> cur) & 1u);
+      phases ^= 1u << cur;
       const int a = q.a, r = q.r;
       const Src o = sources(q);
       const int nrows = o.n / L;
@@ -173,6 +173,111 @@ __global__ void __launch_bounds__(256, 1) k_row_fwd_pp(Geo g, RowGeo rg, Coef C,
     cur ^= 1;
   }
   if (threadIdx.x == 0) bulk_wait_read0();
+}
+
+// Persistent, multi-buffered last sweep (nst <= 4 stages): each CTA walks its
+// row blocks and keeps the TMA loads of the next nst - 1 blocks' transposed
+// half spectra in flight while it transforms the current one; the consumed stage
+// doubles as the FFT exchange buffer and is refilled once the block is done.
+// Same epilogues, partial-sum slots and finalize as k_row_inv_r (one arrival
+// per CTA at the end).
+template <int L>
+__global__ void __launch_bounds__(256, 2) k_row_inv_pp(Geo g, RowGeo rg, EpArgs ea, const RhsState* st,
+                                                       const double2* __restrict__ tw, int64_t ntile, int stage_c, int nst,
+                                                       const __grid_constant__ CUtensorMap tmW) {
+  constexpr int TP = R9<L>::TP;
+  constexpr int hl = (L + 1) / 2;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double2* S = reinterpret_cast<double2*>(smraw);
+  __shared__ double red[kMaxBlock / 32];
+  __shared__ uint64_t bar[4];
+  __shared__ int s_act[FC_MAX_RHS_DEV];
+  const int c = g.dim;
+  const int B = rg.B;
+  const int R = (int)(ntile / ((int64_t)c * rg.ntiles * rg.no));
+  if (threadIdx.x < R) s_act[threadIdx.x] = rhs_active(st, threadIdx.x) ? 1 : 0;
+  if (threadIdx.x == 0)
+    for (int b = 0; b < nst; ++b) mbar_init(&bar[b], 1);
+  __syncthreads();
+  auto issue = [&](int64_t t, int b) {
+    if (t >= ntile) return;
+    const PipeTile q = pipe_decode(t, c, rg);
+    if (!s_act[q.r]) return;
+    double2* dst = S + (size_t)b * stage_c;
+    mbar_expect_tx(&bar[b], (unsigned)(rg.nbox * rg.boxK * B * 16));
+    const int c2 = (q.r * c + q.a) * rg.no + q.o;
+    for (int bx = 0; bx < rg.nbox; ++bx)
+      tma_load_3d(dst + (size_t)bx * rg.boxK * B, &tmW, 2 * q.tile * B, bx * rg.boxK, c2, &bar[b]);
+  };
+  int64_t t = blockIdx.x;
+  if (threadIdx.x == 0)
+    for (int b = 0; b < nst; ++b) issue(t + (int64_t)b * gridDim.x, b);
+  const int p = threadIdx.x / TP;
+  const int j = threadIdx.x - p * TP;
+  const int re = 2 * p, ro = 2 * p + 1;
+  const bool need_q = ea.mode == EP_AP || ea.mode == EP_FP;
+  unsigned phases = 0u;  // bit b: parity of stage b's next completion (no local array)
+  int cur = 0;
+  for (; t < ntile; t += gridDim.x) {
+    const PipeTile q = pipe_decode(t, c, rg);
+    if (s_act[q.r]) {
+      const int a = q.a, r = q.r, o = q.o, tile = q.tile;
+      mbar_wait(&bar[cur], (phases >> cur) & 1u);
+      phases ^= 1u << cur;
+      double2* base = S + (size_t)cur * stage_c;
+      const int row0 = tile * B;
+      const int nrows = min(B, rg.np - row0);
+      const int64_t vbase = ((int64_t)o * rg.np + row0) * L;
+      const int64_t ebase = ((int64_t)r * c + a) * g.N + vbase;
+      const bool he = re < nrows, has_o = ro < nrows;
+      double2 v[1][9];
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+        const int i = j + s * TP;
+        const int k = i < hl ? i : L - i;
+        const double2 ye = he ? base[k * B + re] : make_double2(0.0, 0.0);
+        const double2 yo = has_o ? base[k * B + ro] : make_double2(0.0, 0.0);
+        if (i == 0) v[0][s] = make_double2(ye.x, yo.x);
+        else if (i < hl) v[0][s] = make_double2(ye.x - yo.y, ye.y + yo.x);
+        else v[0][s] = make_double2(ye.x + yo.y, yo.x - ye.y);
+      }
+      fft_reg<L, 1, true>(v, base + (size_t)p * L, L, j, tw);
+      const double Ea = ea.mode == EP_FP ? pick(ea.E, r, a) : 0.0;
+      const double* qsrc = (ea.mode == EP_AP ? ea.p : ea.out) + ebase;
+      double2 qv[9];
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+        const int i = j + s * TP;
+        qv[s].x = need_q && he ? __ldg(qsrc + re * L + i) : 0.0;
+        qv[s].y = need_q && has_o ? __ldg(qsrc + ro * L + i) : 0.0;
+      }
+      double acc = 0.0;
+      with_ep_mode(ea.mode, [&](auto M) {
+        constexpr int MODE = decltype(M)::value;
+#pragma unroll
+        for (int s = 0; s < 9; ++s) {
+          if (he) acc += ep_value_t<MODE>(v[0][s].x * g.invN, Ea, qv[s].x, v[0][s].x);
+          if (has_o) acc += ep_value_t<MODE>(v[0][s].y * g.invN, Ea, qv[s].y, v[0][s].y);
+        }
+      });
+      if (ea.part != nullptr) {
+        const double sum = block_sum(acc, red);
+        if (threadIdx.x == 0) ea.part[(int64_t)r * ea.nslot + (o * rg.ntiles + tile) * c + a] = sum;
+      }
+      double* __restrict__ out = ea.out;
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+        const int i = j + s * TP;
+        if (he) out[ebase + (int64_t)re * L + i] = v[0][s].x;
+        if (has_o) out[ebase + (int64_t)ro * L + i] = v[0][s].y;
+      }
+      fence_proxy_async();  // the exchange writes precede the refill of this stage
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) issue(t + (int64_t)nst * gridDim.x, cur);
+    cur = cur + 1 == nst ? 0 : cur + 1;
+  }
+  finish_block(ea.fin, red);
 }
 
 }  // namespace fc

@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   // the exchange buffer overlaps the Y staging area: fft_reg syncs before its first write
   double2* smp = sm + (size_t)p * L;
   fft_reg<L, 1, true>(v, smp, L, j, tw);
-  const double Ea = pick(ea.E, r, a);
+  const double Ea = ea.mode == EP_FP ? pick(ea.E, r, a) : 0.0;
   const bool he = re < nrows;
   double2 q[9];
   if (need_q && prefetch) {
