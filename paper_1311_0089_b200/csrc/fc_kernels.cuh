@@ -964,12 +964,25 @@ __global__ void __launch_bounds__(kThreads) k_cg_update(int64_t len, RhsState* s
   const int64_t t0 = (int64_t)blockIdx.x * kVecTile;
   const int64_t t1 = min(len, t0 + kVecTile);
   double acc = 0.0;
-  if ((len & 1) == 0) {
-    double2* x2 = reinterpret_cast<double2*>(x + base);
-    double2* r2 = reinterpret_cast<double2*>(rr + base);
-    const double2* p2 = reinterpret_cast<const double2*>(p + base);
-    const double2* a2 = reinterpret_cast<const double2*>(Ap + base);
-    const int64_t h0 = t0 >> 1, h1 = t1 >> 1;
+  // 16-byte accesses for any length: the buffers are 16-byte aligned and every
+  // tile starts at an even offset, so a tile starting at an odd element (odd
+  // per-RHS length, r odd) peels one element; an odd tail is done scalar
+  auto upd1 = [&](int64_t e) {
+    x[e] = __dadd_rn(x[e], __dmul_rn(alpha, p[e]));
+    const double rn = __dsub_rn(rr[e], __dmul_rn(alpha, Ap[e]));
+    rr[e] = rn;
+    return __dmul_rn(rn, rn);
+  };
+  const int64_t g0 = base + t0, g1 = base + t1;  // global element range of this tile
+  const int64_t v0 = (g0 + 1) & ~(int64_t)1;     // first even element
+  const int64_t v1 = g1 & ~(int64_t)1;           // end of the pair range
+  if (threadIdx.x == 0 && g0 < v0) acc += upd1(g0);
+  {
+    double2* x2 = reinterpret_cast<double2*>(x);
+    double2* r2 = reinterpret_cast<double2*>(rr);
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    const double2* a2 = reinterpret_cast<const double2*>(Ap);
+    const int64_t h0 = v0 >> 1, h1 = v1 >> 1;
 #pragma unroll 4
     for (int64_t i = h0 + threadIdx.x; i < h1; i += blockDim.x) {
       const double2 xv = x2[i], rv = r2[i], pv = __ldg(p2 + i), av = __ldg(a2 + i);
@@ -979,15 +992,8 @@ __global__ void __launch_bounds__(kThreads) k_cg_update(int64_t len, RhsState* s
       acc += __dmul_rn(rn.x, rn.x);
       acc += __dmul_rn(rn.y, rn.y);
     }
-  } else {
-    for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
-      const int64_t e = base + i;
-      x[e] = __dadd_rn(x[e], __dmul_rn(alpha, p[e]));
-      const double rn = __dsub_rn(rr[e], __dmul_rn(alpha, Ap[e]));
-      rr[e] = rn;
-      acc += __dmul_rn(rn, rn);
-    }
   }
+  if (threadIdx.x == blockDim.x - 1 && v1 < g1 && v1 >= v0) acc += upd1(v1);
   double s = block_sum(acc, red);
   if (threadIdx.x == 0) part[(int64_t)r * nslot + blockIdx.x] = s;
   finish_block(fin, red);

@@ -1,0 +1,89 @@
+"""GPU: every kernel variant of the row / outer sweeps gives the same CG solve.
+
+The sweeps have alternative implementations selected by environment switches
+read when a context is created (fc_engine.cu): TMA tensor boxes for the
+transposed half spectrum (FC_ROW_TMA), bulk pencil copies in the outer sweep
+(FC_OUTER_TMA), the persistent double-buffered last sweep (FC_INV_PIPE) and
+first sweep (FC_ROW_PIPE).  They perform the same arithmetic in the same order,
+so the batched solve must agree to the last bit with the default path; the
+default path itself is checked against the CPU oracle.  A 243 x 2187 grid has
+one-pencil row blocks (rows of 2187), the case the persistent kernels handle.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from oracle import fftcell_oracle as orc
+from paper_1311_0089_b200 import _native
+from paper_1311_0089_b200.grid import GridSpec
+
+pytestmark = pytest.mark.gpu
+
+SHAPE = (243, 2187)
+LOADS = np.array([[1.0, 0.0], [0.6, 0.8]])
+
+
+def _medium():
+    rng = np.random.default_rng(243)
+    noise = rng.standard_normal(SHAPE)
+    f0 = np.fft.fftfreq(SHAPE[0])[:, None]
+    f1 = np.fft.fftfreq(SHAPE[1])[None, :]
+    smooth = np.fft.ifft2(np.fft.fft2(noise) * np.exp(-2 * np.pi**2 * 9.0 * (f0**2 + f1**2))).real
+    return np.where(smooth > np.quantile(smooth, 0.6), 100.0, 1.0)
+
+
+def _solve(a, env):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        ctx = _native.Context(GridSpec((1.0, 1.0), SHAPE))
+        ctx.set_coefficients(_field(a))
+        reps, x, _ = ctx.solve_cg(LOADS, 1e-8, 1000)
+        return [r["iterations"] for r in reps], x
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _field(a):
+    from paper_1311_0089_b200 import CoefficientField
+
+    return CoefficientField.isotropic(GridSpec((1.0, 1.0), SHAPE), a)
+
+
+@pytest.fixture(scope="module")
+def medium():
+    return _medium()
+
+
+@pytest.fixture(scope="module")
+def default_solve(medium):
+    return _solve(medium, {})
+
+
+def test_default_path_matches_oracle(medium, default_solve):
+    its, x = default_solve
+    full = orc.isotropic_full(medium, 2)
+    ref = orc.solve_cg(full, tuple(LOADS[0]), SHAPE, (1.0, 1.0), 1e-8, 1000)
+    assert its[0] == ref["iterations"]
+    assert rel_l2(x[0], ref["solution"]) < 1e-9
+
+
+@pytest.mark.parametrize("env", [
+    {"FC_ROW_TMA": "0"},
+    {"FC_OUTER_TMA": "0"},
+    {"FC_INV_PIPE": "0"},
+    {"FC_ROW_PIPE": "1"},
+    {"FC_ROW_PIPE": "1", "FC_INV_STAGES": "3"},
+], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_variant_is_bitwise_identical(medium, default_solve, env):
+    its0, x0 = default_solve
+    its, x = _solve(medium, env)
+    assert its == its0
+    assert np.array_equal(x, x0), rel_l2(x, x0)
