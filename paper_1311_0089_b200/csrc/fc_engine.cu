@@ -186,6 +186,7 @@ struct fc_ctx {
   int outer_c1 = 0;         // one-component-per-thread outer sweep: pencil groups per CTA (0 = off)
   int row_pipe = 0;         // persistent double-buffered first sweep (FC_ROW_PIPE)
   CUtensorMap tmW{};        // TMA view of the row-sweep spectrum (RowGeo::tma)
+  CUtensorMap tmM{};        // TMA view of the middle sweep's transposed side (MidGeo::tma)
   int row_pipe_blocks = 0;  // its resident CTAs per SM
   size_t smem_row_pp = 0;
   int inv_pipe_blocks = 0;  // persistent double-buffered last sweep (FC_INV_PIPE): CTAs per SM
@@ -441,12 +442,22 @@ int choose_tiles(fc_ctx* c) {
     mg.B = bp;
     mg.nib = (mg.n0 + bp - 1) / bp;
     c->mid_bp = bp;
-    c->smem_mid_r = (size_t)16 * bp * c->n[1];
+    // TMA boxes on the transposed side: rows * bp a multiple of 8 (128-byte boxes)
+    const int L1 = c->n[1];
+    mg.nbox = (L1 + 255) / 256;
+    int rows = (L1 + mg.nbox - 1) / mg.nbox;
+    while ((rows * bp) % 8) ++rows;
+    if (rows > 256) mg.nbox = 0;  // no box shape: per-thread path
+    mg.rows = rows;
+    c->smem_mid_r = (size_t)16 * std::max(bp * L1, mg.nbox * rows * bp);
   }
   if (is_pow3_reg(c->n0g)) {
     OuterGeo& og = c->og;
     const int TP = c->n0g / 9;
-    int qb = std::max(1, std::min(32, std::min(env_int("FC_OUTER_THREADS", 256), kMaxBlockOuter) / TP));
+    // d = 3 holds 3 x 9 complex per thread: short pencils (TP <= 32) run best
+    // as small CTAs (measured at 243^3: 2 pencils, 54 threads, -22 %)
+    const int outer_dflt = (d == 3 && TP <= 32) ? 2 * TP : 256;
+    int qb = std::max(1, std::min(32, std::min(env_int("FC_OUTER_THREADS", outer_dflt), kMaxBlockOuter) / TP));
     qb = std::min(qb, og.Q);
     og.QB = qb;
     og.nqb = (og.Q + qb - 1) / qb;
@@ -500,6 +511,7 @@ int allow_reg_smem(int mx) {
       al(k_row_inv_r<LL>);
       al(k_mid_r<LL, false>);
       al(k_mid_r<LL, true>);
+      al(k_mid_tma<LL, true>);
       al(k_outer_r<LL, 2>);
       al(k_outer_r<LL, 3>);
       al(k_outer_p<LL, 2>);
@@ -538,6 +550,20 @@ int make_row_tmap(fc_ctx* c) {
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rc != CUDA_SUCCESS) return set_err(FC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)rc);
   rg.tma = 1;
+  // middle sweep (d = 3, one slab): W2[rc][k2][k1][i0] as doubles {2 n0, n1, R c h2}
+  MidGeo& mg = c->mg;
+  mg.tma = 0;
+  const char* envm = getenv("FC_MID_TMA");
+  if (c->dim == 3 && c->mid_bp && c->P == 1 && mg.nbox > 0 && !(envm && atoi(envm) == 0)) {
+    cuuint64_t md[3] = {(cuuint64_t)2 * mg.n0, (cuuint64_t)mg.n1, (cuuint64_t)c->Rcap * c->dim * mg.h2};
+    cuuint64_t ms[2] = {(cuuint64_t)16 * mg.n0, (cuuint64_t)16 * mg.n0 * mg.n1};
+    cuuint32_t mb[3] = {(cuuint32_t)(2 * mg.B), (cuuint32_t)mg.rows, 1};
+    const CUresult rm = encode(&c->tmM, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->W2, md, ms, mb, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rm != CUDA_SUCCESS) return set_err(FC_ECUDA, "cuTensorMapEncodeTiled (middle sweep) failed (%d)", (int)rm);
+    mg.tma = 1;
+  }
   return FC_OK;
 }
 
@@ -657,7 +683,10 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
       const int nt = c->mid_bp * (c->n[1] / 9);
       const double2* tw = c->rtw(c->n[1]);
       return launch(c, inv ? "mid_inv" : "mid_fwd", [&] {
-        if (inv) FC_POW3_SWITCH(c->n[1], (k_mid_r<LL, true><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, smap, st, tw, src, dst)))
+        // TMA variant for the inverse direction only (measured: the forward one,
+        // whose transposed side is the store, is not faster than per-thread stores)
+        if (inv && mg.tma) FC_POW3_SWITCH(c->n[1], (k_mid_tma<LL, true><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, st, tw, src, dst, c->tmM)))
+        else if (inv) FC_POW3_SWITCH(c->n[1], (k_mid_r<LL, true><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, smap, st, tw, src, dst)))
         else FC_POW3_SWITCH(c->n[1], (k_mid_r<LL, false><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, smap, st, tw, src, dst)))
       });
     }

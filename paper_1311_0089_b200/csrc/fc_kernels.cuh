@@ -772,6 +772,8 @@ __global__ void __launch_bounds__(kThreads) k_row_inv(Geo g, RowGeo rg, EpArgs e
 // Middle sweep (d = 3): W1[r][a][i0][k2][i1] <-> W2[r][a][k2][k1][i0].
 struct MidGeo {
   int n0, n1, h2, B, nib;
+  int tma = 0;          // single slab: bulk pencil copies + TMA boxes on the transposed side
+  int rows = 0, nbox = 0;  // box {2B doubles, rows modes}, nbox boxes per CTA
 };
 
 template <bool INV>

@@ -377,6 +377,80 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   if (last) finalize_block(ea.fin, red);
 }
 
+// Middle sweep through TMA (one slab).  Pencil side (W1[rc][i0][k2][:], one
+// contiguous row of L modes per i0): one bulk copy per pencil.  Transposed side
+// (W2[rc][k2][k1][i0]): tensor boxes {2 BP doubles, rows modes} = BP consecutive
+// i0 for rows consecutive k1, landing in smem as [k1][p].
+template <int L, bool INV>
+__device__ __forceinline__ void mid_tma(const Geo& g, const MidGeo& mg, const RhsState* st,
+                                        const double2* __restrict__ tw, const double2* __restrict__ src,
+                                        double2* __restrict__ dst, const CUtensorMap& tmM, double2* sm) {
+  constexpr int TP = R9<L>::TP;
+  const int c = g.dim;
+  int64_t bid = blockIdx.x;
+  const int ib = bid % mg.nib; bid /= mg.nib;
+  const int k2 = bid % mg.h2; bid /= mg.h2;
+  const int a = bid % c;
+  const int r = (int)(bid / c);
+  if (!rhs_active(st, r)) return;
+  const int BP = mg.B;
+  const int p = threadIdx.x % BP;
+  const int j = threadIdx.x / BP;
+  const int i00 = ib * BP;
+  const int np_ = min(BP, mg.n0 - i00);  // live pencils
+  const int rc = r * c + a;
+  const int cz = rc * mg.h2 + k2;        // tensor coordinate of the (rc, k2) plane
+  const double2* pen = (INV ? dst : src) + (((int64_t)rc * mg.n0 + i00) * mg.h2 + k2) * L;  // pencil p at + p*h2*L
+  const int64_t pstride = (int64_t)mg.h2 * L;
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    if (!INV) {
+      mbar_expect_tx(&bar, (unsigned)(np_ * L * 16));
+      for (int q = 0; q < np_; ++q) bulk_g2s(sm + (size_t)q * L, pen + q * pstride, (unsigned)(L * 16), &bar);
+    } else {
+      mbar_expect_tx(&bar, (unsigned)(mg.nbox * mg.rows * BP * 16));
+      for (int b = 0; b < mg.nbox; ++b)
+        tma_load_3d(sm + (size_t)b * mg.rows * BP, &tmM, 2 * i00, b * mg.rows, cz, &bar);
+    }
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  double2 v[1][9];
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+    const int i = j + s * TP;
+    v[0][s] = INV ? sm[(size_t)i * BP + p] : sm[(size_t)p * L + i];
+  }
+  fft_reg<L, 1, INV>(v, sm + (size_t)p * L, L, j, tw);
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+    const int i = j + s * TP;
+    if (INV) sm[(size_t)p * L + i] = v[0][s];
+    else sm[(size_t)i * BP + p] = v[0][s];
+  }
+  fence_proxy_async();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (INV) {
+      for (int q = 0; q < np_; ++q) bulk_s2g(const_cast<double2*>(pen) + q * pstride, sm + (size_t)q * L, (unsigned)(L * 16));
+    } else {
+      for (int b = 0; b < mg.nbox; ++b) tma_store_3d(&tmM, 2 * i00, b * mg.rows, cz, sm + (size_t)b * mg.rows * BP);
+    }
+    bulk_commit();
+    bulk_wait_read0();
+  }
+}
+
+template <int L, bool INV>
+__global__ void __launch_bounds__(kMaxBlock) k_mid_tma(Geo g, MidGeo mg, const RhsState* st,
+                                                        const double2* __restrict__ tw, const double2* __restrict__ src,
+                                                        double2* __restrict__ dst, const __grid_constant__ CUtensorMap tmM) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  mid_tma<L, INV>(g, mg, st, tw, src, dst, tmM, reinterpret_cast<double2*>(smraw));
+}
+
 // Middle sweep (d = 3), thread mapping pencil-fastest (t = j * BP + p) so the
 // transposed side is written / read in chunks of BP consecutive i0.
 template <int L, bool INV>

@@ -87,3 +87,36 @@ def test_variant_is_bitwise_identical(medium, default_solve, env):
     its, x = _solve(medium, env)
     assert its == its0
     assert np.array_equal(x, x0), rel_l2(x, x0)
+
+
+def test_mid_sweep_variants_3d():
+    """3-D: the TMA middle sweep (FC_MID_TMA) and the outer CTA size
+    (FC_OUTER_THREADS) give a bitwise-identical CG solve."""
+    from paper_1311_0089_b200 import CoefficientField
+
+    shape = (81, 81, 81)
+    spec = GridSpec((1.0, 1.0, 1.0), shape)
+    rng = np.random.default_rng(81)
+    a = np.where(rng.random(shape) < 0.3, 50.0, 1.0)
+    coef = CoefficientField.isotropic(spec, a)
+
+    def run(env):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            ctx = _native.Context(spec)
+            ctx.set_coefficients(coef)
+            reps, x, _ = ctx.solve_cg(np.array([[1.0, 0.0, 0.0]]), 1e-8, 1000)
+            return reps[0]["iterations"], x
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+
+    it0, x0 = run({})
+    for env in ({"FC_MID_TMA": "0"}, {"FC_OUTER_THREADS": "256"}, {"FC_OUTER_TMA": "0"}):
+        it, x = run(env)
+        assert it == it0, env
+        assert np.array_equal(x, x0), (env, rel_l2(x, x0))
