@@ -192,6 +192,7 @@ struct fc_ctx {
   int inv_pipe_blocks = 0;  // persistent double-buffered last sweep (FC_INV_PIPE): CTAs per SM
   int inv_pipe_stage = 0;   // its stage size (complex)
   int inv_pipe_nst = 2;     // its number of stages (FC_INV_STAGES, 2..4)
+  int inv_pipe_qbuf = 1;    // bulk-load the epilogue input per block (FC_INV_QBUF)
   size_t smem_aniso_r = 0;
   size_t smem_row_r = 0, smem_row_inv_r = 0, smem_mid_r = 0, smem_outer_r = 0;
 
@@ -793,9 +794,10 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     const unsigned grid = (unsigned)std::min<int64_t>(ntile, (int64_t)c->num_sms * c->inv_pipe_blocks);
     const int stage_c = c->inv_pipe_stage;
     const int nst = c->inv_pipe_nst;
-    const size_t smem = (size_t)nst * 16 * stage_c;
+    const int qbuf = c->inv_pipe_qbuf;
+    const size_t smem = (size_t)nst * 16 * stage_c + (qbuf ? (size_t)8 * (2 * c->row_npen * rg.nl + 2) : 0);
     return launch(c, "row_inv", [&] {
-      FC_POW3_SWITCH(rg.nl, (k_row_inv_pp<LL><<<grid, nt, smem, s>>>(g, rg, ea, st, tw, ntile, stage_c, nst, c->tmW)));
+      FC_POW3_SWITCH(rg.nl, (k_row_inv_pp<LL><<<grid, nt, smem, s>>>(g, rg, ea, st, tw, ntile, stage_c, nst, qbuf, c->tmW)));
     });
   }
   if (c->row_npen) {
@@ -964,10 +966,12 @@ int create_slab(fc_ctx** out, int32_t dim, const int64_t* shape, const double* h
     const int B = 2 * c->row_npen;
     c->inv_pipe_stage = (std::max(rg.nbox * rg.boxK * B, c->row_npen * (rg.nl + 1)) + 7) & ~7;
     c->inv_pipe_nst = std::max(2, std::min(4, env_int_g("FC_INV_STAGES", 2)));
-    size_t smem = (size_t)c->inv_pipe_nst * 16 * c->inv_pipe_stage;
+    c->inv_pipe_qbuf = env_int_g("FC_INV_QBUF", 1) != 0;
+    const size_t qbytes = c->inv_pipe_qbuf ? (size_t)8 * (2 * c->row_npen * rg.nl + 2) : 0;
+    size_t smem = (size_t)c->inv_pipe_nst * 16 * c->inv_pipe_stage + qbytes;
     while (c->inv_pipe_nst > 2 && 2 * (smem + 2048) > (size_t)c->smem_optin) {  // keep 2 CTAs per SM
       --c->inv_pipe_nst;
-      smem = (size_t)c->inv_pipe_nst * 16 * c->inv_pipe_stage;
+      smem = (size_t)c->inv_pipe_nst * 16 * c->inv_pipe_stage + qbytes;
     }
     int nb = 0;
     FC_POW3_SWITCH(rg.nl, (allow_smem(k_row_inv_pp<LL>, mx),

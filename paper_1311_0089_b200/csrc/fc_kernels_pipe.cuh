@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(256, 1) k_row_fwd_pp(Geo g, RowGeo rg, Coef C,
 template <int L>
 __global__ void __launch_bounds__(256, 2) k_row_inv_pp(Geo g, RowGeo rg, EpArgs ea, const RhsState* st,
                                                        const double2* __restrict__ tw, int64_t ntile, int stage_c, int nst,
+                                                       int qbuf,
                                                        const __grid_constant__ CUtensorMap tmW) {
   constexpr int TP = R9<L>::TP;
   constexpr int hl = (L + 1) / 2;
@@ -191,13 +192,18 @@ __global__ void __launch_bounds__(256, 2) k_row_inv_pp(Geo g, RowGeo rg, EpArgs 
   double2* S = reinterpret_cast<double2*>(smraw);
   __shared__ double red[kMaxBlock / 32];
   __shared__ uint64_t bar[4];
+  __shared__ uint64_t barq;  // epilogue input (p / e) of the current block, qbuf != 0
   __shared__ int s_act[FC_MAX_RHS_DEV];
   const int c = g.dim;
   const int B = rg.B;
   const int R = (int)(ntile / ((int64_t)c * rg.ntiles * rg.no));
   if (threadIdx.x < R) s_act[threadIdx.x] = rhs_active(st, threadIdx.x) ? 1 : 0;
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
     for (int b = 0; b < nst; ++b) mbar_init(&bar[b], 1);
+    mbar_init(&barq, 1);
+  }
+  double* Q = reinterpret_cast<double*>(S + (size_t)nst * stage_c);  // qbuf: one row block of doubles (+2)
+  unsigned qphase = 0u;
   __syncthreads();
   auto issue = [&](int64_t t, int b) {
     if (t >= ntile) return;
@@ -230,6 +236,13 @@ __global__ void __launch_bounds__(256, 2) k_row_inv_pp(Geo g, RowGeo rg, EpArgs 
       const int64_t vbase = ((int64_t)o * rg.np + row0) * L;
       const int64_t ebase = ((int64_t)r * c + a) * g.N + vbase;
       const bool he = re < nrows, has_o = ro < nrows;
+      const double* qsrc = (ea.mode == EP_AP ? ea.p : ea.out) + ebase;
+      const bool qb = need_q && qbuf;
+      const int qsh = qb ? bulk_shift(qsrc) : 0;
+      if (qb && threadIdx.x == 0) {  // lands during the transform
+        mbar_expect_tx(&barq, bulk_bytes(nrows * L, qsh));
+        bulk_g2s(Q, qsrc - qsh, bulk_bytes(nrows * L, qsh), &barq);
+      }
       double2 v[1][9];
 #pragma unroll
       for (int s = 0; s < 9; ++s) {
@@ -243,13 +256,24 @@ __global__ void __launch_bounds__(256, 2) k_row_inv_pp(Geo g, RowGeo rg, EpArgs 
       }
       fft_reg<L, 1, true>(v, base + (size_t)p * L, L, j, tw);
       const double Ea = ea.mode == EP_FP ? pick(ea.E, r, a) : 0.0;
-      const double* qsrc = (ea.mode == EP_AP ? ea.p : ea.out) + ebase;
       double2 qv[9];
+      if (qb) {
+        mbar_wait(&barq, qphase);
+        qphase ^= 1u;
+        const double* sq = Q + qsh;
 #pragma unroll
-      for (int s = 0; s < 9; ++s) {
-        const int i = j + s * TP;
-        qv[s].x = need_q && he ? __ldg(qsrc + re * L + i) : 0.0;
-        qv[s].y = need_q && has_o ? __ldg(qsrc + ro * L + i) : 0.0;
+        for (int s = 0; s < 9; ++s) {
+          const int i = j + s * TP;
+          qv[s].x = he ? sq[re * L + i] : 0.0;
+          qv[s].y = has_o ? sq[ro * L + i] : 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < 9; ++s) {
+          const int i = j + s * TP;
+          qv[s].x = need_q && he ? __ldg(qsrc + re * L + i) : 0.0;
+          qv[s].y = need_q && has_o ? __ldg(qsrc + ro * L + i) : 0.0;
+        }
       }
       double acc = 0.0;
       with_ep_mode(ea.mode, [&](auto M) {
