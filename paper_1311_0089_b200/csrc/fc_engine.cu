@@ -410,10 +410,13 @@ int choose_tiles(fc_ctx* c) {
     c->smem_row_r = (size_t)24 * (((size_t)2 * npen * rg.nl + 3) & ~(size_t)1);
     c->inv_prefetch = env_int("FC_INV_PREFETCH", 0);
     c->row_pipe = env_int("FC_ROW_PIPE", 0) && rg.nl >= 81;
-    c->smem_row_pp = (size_t)2 * 8 * ((3 * ((2 * rg.nl + 3) & ~1) + 15) & ~15);
     // TMA boxes of the transposed spectrum: nbox boxes of boxK modes x 2 npen rows
     rg.nbox = (rg.hl + 255) / 256;
     rg.boxK = ((rg.hl + rg.nbox - 1) / rg.nbox + 3) & ~3;  // boxes start 128-byte aligned in smem
+    // persistent first sweep: stage U, P (2 x stride doubles, 128-byte rounded) +
+    // spectrum buffer (L complex for the FFT, nbox boxK 2 complex for the split)
+    c->smem_row_pp = (size_t)8 * ((2 * ((2 * rg.nl + 3) & ~1) + 15) & ~15) +
+                     (size_t)16 * std::max(rg.nl, rg.nbox * rg.boxK * 2);
     const size_t ybytes = (size_t)16 * rg.nbox * rg.boxK * 2 * npen;
     c->smem_row_r = std::max(c->smem_row_r, (size_t)16 * (((size_t)npen * rg.nl + 7) & ~(size_t)7) + ybytes);
     c->smem_row_inv_r = std::max((size_t)16 * npen * (rg.nl + 1), ybytes) +

@@ -33,21 +33,25 @@ __device__ __forceinline__ PipeTile pipe_decode(int64_t t, int c, const RowGeo& 
   return q;
 }
 
-// Stage layout (doubles): U[stride] P[stride] A[stride]; once the inputs sit in
-// registers the stage holds the FFT exchange buffer / spectrum z (L complex,
-// from offset 0) and the split half spectra Y[k][2] (from offset zoff).
+// Persistent first sweep, 2 CTAs per SM.  Shared memory: one input stage
+// U[stride] P[stride] (r / p_old, or the raw field) and one spectrum buffer Z
+// (the FFT exchange, then the split half spectra Y[k][2] written in place).
+// A is read straight from global memory (issued before the stage wait).  As
+// soon as the pointwise step has moved the inputs into registers the stage is
+// refilled with block t + G by TMA, so those loads overlap this block's FFT,
+// split and store.
 template <int L>
-__global__ void __launch_bounds__(256, 1) k_row_fwd_pp(Geo g, RowGeo rg, Coef C, InArgs ia, const RhsState* st,
+__global__ void __launch_bounds__(256, 2) k_row_fwd_pp(Geo g, RowGeo rg, Coef C, InArgs ia, const RhsState* st,
                                                        const double2* __restrict__ tw, int64_t ntile,
                                                        const __grid_constant__ CUtensorMap tmW) {
   constexpr int TP = R9<L>::TP;
   constexpr int hl = (L + 1) / 2;
   constexpr int stride = pipe_stride<L>();
-  constexpr int stage = (3 * stride + 15) & ~15;  // doubles; stages start 128-byte aligned
-  constexpr int zoff = (L + 7) & ~7;  // Y offset in complex (128-byte aligned boxes)
+  constexpr int zoff = (2 * stride + 15) & ~15;  // doubles: Z starts 128-byte aligned
   extern __shared__ __align__(128) unsigned char smraw[];
   double* S = reinterpret_cast<double*>(smraw);
-  __shared__ uint64_t bar[2];
+  double2* Z = reinterpret_cast<double2*>(S + zoff);
+  __shared__ uint64_t bar;
   __shared__ double s_beta[FC_MAX_RHS_DEV];
   __shared__ int s_flags[FC_MAX_RHS_DEV];  // bit 0 active, bit 1 first
   const int c = g.dim;
@@ -60,13 +64,9 @@ __global__ void __launch_bounds__(256, 1) k_row_fwd_pp(Geo g, RowGeo rg, Coef C,
     s_flags[r] = (act ? 1 : 0) | (first ? 2 : 0);
     s_beta[r] = ia.mode == IN_PNEW ? st[r].beta : 0.0;
   }
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-  }
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
   __syncthreads();
 
-  // source pointers of tile t (u / p_old / A) and their 16-byte phases
   struct Src {
     const double *u, *p, *A;
     int n;
@@ -77,100 +77,110 @@ __global__ void __launch_bounds__(256, 1) k_row_fwd_pp(Geo g, RowGeo rg, Coef C,
     o.n = min(2, rg.np - row0) * L;
     const int64_t vbase = ((int64_t)q.o * rg.np + row0) * L;
     const int64_t ub = (int64_t)q.r * c * g.N + (int64_t)q.a * g.N + vbase;
-    const int fl = s_flags[q.r];
     o.u = ia.u + ub;
-    o.p = (ia.mode == IN_PNEW && !(fl & 2)) ? ia.p_old + ub : nullptr;
+    o.p = (ia.mode == IN_PNEW && !(s_flags[q.r] & 2)) ? ia.p_old + ub : nullptr;
     o.A = ia.mode != IN_RAW ? C.A + vbase : nullptr;
     return o;
   };
-  // one thread issues the bulk loads of tile t into stage b
-  auto prefetch = [&](int64_t t, int b) {
-    if (t >= ntile) return;
-    const PipeTile q = pipe_decode(t, c, rg);
-    if (!(s_flags[q.r] & 1)) return;
-    const Src o = sources(q);
-    double* dst = S + b * stage;
-    const int su = bulk_shift(o.u), sp = o.p ? bulk_shift(o.p) : 0, sa = o.A ? bulk_shift(o.A) : 0;
-    mbar_expect_tx(&bar[b], bulk_bytes(o.n, su) + (o.p ? bulk_bytes(o.n, sp) : 0u) + (o.A ? bulk_bytes(o.n, sa) : 0u));
-    bulk_g2s(dst, o.u - su, bulk_bytes(o.n, su), &bar[b]);
-    if (o.p) bulk_g2s(dst + stride, o.p - sp, bulk_bytes(o.n, sp), &bar[b]);
-    if (o.A) bulk_g2s(dst + 2 * stride, o.A - sa, bulk_bytes(o.n, sa), &bar[b]);
+  // first active block at or after t (inactive right-hand sides are skipped)
+  auto next_active = [&](int64_t t) {
+    while (t < ntile && !(s_flags[pipe_decode(t, c, rg).r] & 1)) t += gridDim.x;
+    return t;
   };
-
-  int64_t t = blockIdx.x;
-  if (threadIdx.x == 0) {
-    prefetch(t, 0);
-    prefetch(t + gridDim.x, 1);
-  }
-  unsigned phases = 0u;  // bit b: parity of stage b's next completion (no local array)
-  int cur = 0;
-  for (; t < ntile; t += gridDim.x) {
+  auto prefetch = [&](int64_t t) {  // thread 0
+    if (t >= ntile) return;
+    const Src o = sources(pipe_decode(t, c, rg));
+    const int su = bulk_shift(o.u), sp = o.p ? bulk_shift(o.p) : 0;
+    mbar_expect_tx(&bar, bulk_bytes(o.n, su) + (o.p ? bulk_bytes(o.n, sp) : 0u));
+    bulk_g2s(S, o.u - su, bulk_bytes(o.n, su), &bar);
+    if (o.p) bulk_g2s(S + stride, o.p - sp, bulk_bytes(o.n, sp), &bar);
+  };
+  int64_t t = next_active(blockIdx.x);
+  if (threadIdx.x == 0) prefetch(t);
+  unsigned phase = 0u;
+  for (; t < ntile;) {
     const PipeTile q = pipe_decode(t, c, rg);
-    const int fl = s_flags[q.r];
-    double* base = S + cur * stage;
-    if (fl & 1) {
-      mbar_wait(&bar[cur], (phases >> cur) & 1u);
-      phases ^= 1u << cur;
-      const int a = q.a, r = q.r;
-      const Src o = sources(q);
-      const int nrows = o.n / L;
-      const double* st_u = base + bulk_shift(o.u);
-      const double* st_p = base + stride + (o.p ? bulk_shift(o.p) : 0);
-      const double* st_a = base + 2 * stride + (o.A ? bulk_shift(o.A) : 0);
-      const bool pnew = ia.mode == IN_PNEW;
-      const bool first = (fl & 2) != 0;
-      const double beta = s_beta[r];
-      double* pw = pnew ? ia.p_new + (o.u - ia.u) : nullptr;
-      const double A0aa = ia.mode == IN_FP ? pick3(ia.A0, a, a) : 0.0;
-      double2 v[1][9];
+    const int a = q.a, r = q.r;
+    const Src o = sources(q);
+    const int nrows = o.n / L;
+    const bool pnew = ia.mode == IN_PNEW;
+    const bool first = (s_flags[r] & 2) != 0;
+    const double beta = s_beta[r];
+    // coefficient values straight from global memory, issued before the wait
+    double av[2][9];
 #pragma unroll
-      for (int s = 0; s < 9; ++s) {
-        const int i = j + s * TP;
-        double y[2] = {0.0, 0.0};
+    for (int s = 0; s < 9; ++s)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (h < nrows) {
-            const int e = h * L + i;
-            double x = st_u[e];
-            if (pnew) {
-              x = first ? x : __dadd_rn(x, __dmul_rn(beta, st_p[e]));
-              pw[e] = x;
-            }
-            double val;
-            if (ia.mode == IN_RAW) val = x;
-            else if (ia.mode == IN_FP) val = __dmul_rn(__dsub_rn(st_a[e], A0aa), x);
-            else val = __dmul_rn(st_a[e], x);
-            if (ia.mode != IN_FP && ia.s != 1.0) val = __dmul_rn(ia.s, val);
-            y[h] = val;
+      for (int h = 0; h < 2; ++h) av[h][s] = (o.A && h < nrows) ? __ldg(o.A + h * L + j + s * TP) : 0.0;
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+    const double* st_u = S + bulk_shift(o.u);
+    const double* st_p = S + stride + (o.p ? bulk_shift(o.p) : 0);
+    double* pw = pnew ? ia.p_new + (o.u - ia.u) : nullptr;
+    const double A0aa = ia.mode == IN_FP ? pick3(ia.A0, a, a) : 0.0;
+    double2 v[1][9];
+#pragma unroll
+    for (int s = 0; s < 9; ++s) {
+      const int i = j + s * TP;
+      double y[2] = {0.0, 0.0};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h < nrows) {
+          const int e = h * L + i;
+          double x = st_u[e];
+          if (pnew) {
+            x = first ? x : __dadd_rn(x, __dmul_rn(beta, st_p[e]));
+            pw[e] = x;
           }
+          double val;
+          if (ia.mode == IN_RAW) val = x;
+          else if (ia.mode == IN_FP) val = __dmul_rn(__dsub_rn(av[h][s], A0aa), x);
+          else val = __dmul_rn(av[h][s], x);
+          if (ia.mode != IN_FP && ia.s != 1.0) val = __dmul_rn(ia.s, val);
+          y[h] = val;
         }
-        v[0][s] = make_double2(y[0], y[1]);
       }
-      double2* z = reinterpret_cast<double2*>(base);
-      fft_reg<L, 1, false>(v, z, L, j, tw);
-      __syncthreads();
+      v[0][s] = make_double2(y[0], y[1]);
+    }
+    const int64_t tn = next_active(t + gridDim.x);
+    __syncthreads();  // the stage has been read: refill it with the next block
+    if (threadIdx.x == 0) {
+      bulk_wait_read0();  // the previous block's spectrum store has left Z
+      prefetch(tn);
+    }
+    fft_reg<L, 1, false>(v, Z, L, j, tw);
+    __syncthreads();
 #pragma unroll
-      for (int s = 0; s < 9; ++s) z[j + s * TP] = v[0][s];
-      __syncthreads();
-      // split Z = Ye + i Yo into the two half spectra Y[k][row]
-      double2* Y = z + zoff;
-      for (int k = threadIdx.x; k < hl; k += blockDim.x) {
-        const double2 zk = z[k];
-        const double2 zm = z[k == 0 ? 0 : L - k];
-        Y[2 * k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-        Y[2 * k + 1] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
-      }
-      fence_proxy_async();  // generic writes of this stage before async-proxy use (store now, refill next)
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const int c2 = (r * c + a) * rg.no + q.o;
-        for (int b = 0; b < rg.nbox; ++b) tma_store_3d(&tmW, 4 * q.tile, b * rg.boxK, c2, Y + (size_t)b * rg.boxK * 2);
-        bulk_commit();
-        bulk_wait_read0();  // the stage is refilled below
+    for (int s = 0; s < 9; ++s) Z[j + s * TP] = v[0][s];
+    __syncthreads();
+    // split in place: gather (z_k, z_{L-k}) for this thread's modes, then write Y[k][2]
+    constexpr int KP = (hl + TP - 1) / TP;
+    double2 zk[KP], zm[KP];
+#pragma unroll
+    for (int m = 0; m < KP; ++m) {
+      const int k = j + m * TP;
+      if (k < hl) {
+        zk[m] = Z[k];
+        zm[m] = Z[k == 0 ? 0 : L - k];
       }
     }
-    if (threadIdx.x == 0) prefetch(t + 2 * (int64_t)gridDim.x, cur);
-    cur ^= 1;
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < KP; ++m) {
+      const int k = j + m * TP;
+      if (k < hl) {
+        Z[2 * k] = make_double2(0.5 * (zk[m].x + zm[m].x), 0.5 * (zk[m].y - zm[m].y));
+        Z[2 * k + 1] = make_double2(0.5 * (zk[m].y + zm[m].y), 0.5 * (zm[m].x - zk[m].x));
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int c2 = (r * c + a) * rg.no + q.o;
+      for (int b = 0; b < rg.nbox; ++b) tma_store_3d(&tmW, 4 * q.tile, b * rg.boxK, c2, Z + (size_t)b * rg.boxK * 2);
+      bulk_commit();
+    }
+    t = tn;
   }
   if (threadIdx.x == 0) bulk_wait_read0();
 }
