@@ -696,8 +696,8 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     }
     const FftPlan pl1 = c->plan(c->n[1]);
     return launch(c, inv ? "mid_inv" : "mid_fwd", [&] {
-      if (inv) k_mid<true><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, st, pl1, src, dst);
-      else k_mid<false><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, st, pl1, src, dst);
+      if (inv) k_mid<true><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, smap, st, pl1, src, dst);
+      else k_mid<false><<<(unsigned)nmid, kThreads, c->smem_mid, s>>>(g, mg, smap, st, pl1, src, dst);
     });
   };
   if (phases & PH_FWD) {
@@ -782,9 +782,9 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
       else FC_POW3_SWITCH(c->n0g, (k_outer_r<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, smap, st, tw, Wout)))
     }));
   } else {
-    const FftPlan pl0 = c->plan(c->n[0]);
+    const FftPlan pl0 = c->plan(c->n0g);  // outer axis: global length (a slab holds n[0] < n0g planes)
     TRY(launch(c, "outer", [&] {
-      k_outer<<<(unsigned)(R * og.nqb), kThreads, c->smem_outer, s>>>(g, og, st, pl0, c->W2);
+      k_outer<<<(unsigned)(R * og.nqb), kThreads, c->smem_outer, s>>>(g, og, smap, st, pl0, Wout);
     }));
   }
   }
@@ -955,8 +955,7 @@ int create_slab(fc_ctx** out, int32_t dim, const int64_t* shape, const double* h
   cudaMemcpy(c->xi, xi.data(), sizeof(double) * xi.size(), cudaMemcpyHostToDevice);
   rc = choose_tiles(c);
   if (rc) return fail(rc);
-  if (P > 1 && (dim != 3 || !c->row_npen || !c->mid_bp || !c->outer_qb))
-    return fail(set_err(FC_ENOTSUP, "slab decomposition needs d = 3 and power-of-three axes (9..2187)"));
+  if (P > 1 && dim != 3) return fail(set_err(FC_ENOTSUP, "slab decomposition needs d = 3"));
   const int mx = c->smem_optin;
   if ((rc = allow_smem(k_row_fwd, mx)) || (rc = allow_smem(k_row_inv, mx)) || (rc = allow_smem(k_mid<false>, mx)) ||
       (rc = allow_smem(k_mid<true>, mx)) || (rc = allow_smem(k_outer, mx)) || (rc = allow_smem(k_line, mx)) ||

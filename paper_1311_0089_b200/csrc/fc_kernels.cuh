@@ -777,7 +777,7 @@ struct MidGeo {
 };
 
 template <bool INV>
-__global__ void __launch_bounds__(kThreads) k_mid(Geo g, MidGeo mg, const RhsState* st, FftPlan pl,
+__global__ void __launch_bounds__(kThreads) k_mid(Geo g, MidGeo mg, SlabMap sm_, const RhsState* st, FftPlan pl,
                                                    const double2* __restrict__ src, double2* __restrict__ dst) {
   extern __shared__ double2 sm[];
   const int c = g.dim;
@@ -794,7 +794,8 @@ __global__ void __launch_bounds__(kThreads) k_mid(Geo g, MidGeo mg, const RhsSta
   double2* buf1 = sm + (size_t)nr * ld;
   const int64_t rc = (int64_t)(r * c + a);
   // W1 offset of (i0, k2, i1): ((rc*n0 + i0)*h2 + k2)*n1 + i1
-  // W2 offset of (k2, k1, i0): ((rc*h2 + k2)*n1 + k1)*n0 + i0
+  // W2 offset of (k2, k1, i0): send_index(rc, k2*n1 + k1, i0) (= ((rc*h2 + k2)*n1 + k1)*n0 + i0
+  // for one slab; destination-blocked for P slabs, SlabMap)
   if (!INV) {
     for (int idx = threadIdx.x; idx < nr * mg.n1; idx += blockDim.x) {
       const int row = idx / mg.n1, i1 = idx - row * mg.n1;
@@ -803,7 +804,7 @@ __global__ void __launch_bounds__(kThreads) k_mid(Geo g, MidGeo mg, const RhsSta
   } else {
     for (int idx = threadIdx.x; idx < nr * mg.n1; idx += blockDim.x) {
       const int k1 = idx / nr, row = idx - k1 * nr;
-      buf0[(size_t)row * ld + k1] = src[((rc * mg.h2 + k2) * mg.n1 + k1) * mg.n0 + i00 + row];
+      buf0[(size_t)row * ld + k1] = src[send_index(sm_, (int)rc, k2 * mg.n1 + k1, i00 + row)];
     }
   }
   __syncthreads();
@@ -811,7 +812,7 @@ __global__ void __launch_bounds__(kThreads) k_mid(Geo g, MidGeo mg, const RhsSta
   if (!INV) {
     for (int idx = threadIdx.x; idx < nr * mg.n1; idx += blockDim.x) {
       const int k1 = idx / nr, row = idx - k1 * nr;
-      dst[((rc * mg.h2 + k2) * mg.n1 + k1) * mg.n0 + i00 + row] = res[(size_t)row * ld + k1];
+      dst[send_index(sm_, (int)rc, k2 * mg.n1 + k1, i00 + row)] = res[(size_t)row * ld + k1];
     }
   } else {
     for (int idx = threadIdx.x; idx < nr * mg.n1; idx += blockDim.x) {
@@ -833,7 +834,15 @@ struct OuterGeo {
   double M[kMaxDim][kMaxDim];
 };
 
-__global__ void __launch_bounds__(kThreads) k_outer(Geo g, OuterGeo og, const RhsState* st, FftPlan pl,
+// Element (a, local pencil ql, i0) of the outer sweep's input: the received
+// segment of the slab owning plane i0 (P = 1: W2[r][a][ql][i0]).
+__device__ __forceinline__ int64_t outer_index(const SlabMap& m, int Q, int rc, int ql, int i0) {
+  const int p = slab_of(m.s0, m.P, i0);
+  const int n0p = m.s0[p + 1] - m.s0[p];
+  return m.roff[p] + ((int64_t)rc * Q + ql) * n0p + (i0 - m.s0[p]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_outer(Geo g, OuterGeo og, SlabMap sm_, const RhsState* st, FftPlan pl,
                                                      double2* __restrict__ W) {
   extern __shared__ double2 sm[];
   const int c = g.dim;
@@ -847,16 +856,18 @@ __global__ void __launch_bounds__(kThreads) k_outer(Geo g, OuterGeo og, const Rh
   double2* buf0 = sm;
   double2* buf1 = sm + (size_t)P * ld;
   for (int a = 0; a < c; ++a) {
-    const double2* s = W + (((int64_t)(r * c + a)) * og.Q + q0) * og.n0;
     double2* d = buf0 + (size_t)a * nq * ld;
-    for (int idx = threadIdx.x; idx < nq * og.n0; idx += blockDim.x) d[idx] = s[idx];
+    for (int idx = threadIdx.x; idx < nq * og.n0; idx += blockDim.x) {
+      const int qq = idx / og.n0, i0 = idx - qq * og.n0;
+      d[idx] = W[outer_index(sm_, og.Q, r * c + a, q0 + qq, i0)];
+    }
   }
   __syncthreads();
   double2* res = smem_fft<false>(buf0, buf1, P, ld, pl);
   double2* other = res == buf0 ? buf1 : buf0;
   for (int idx = threadIdx.x; idx < nq * og.n0; idx += blockDim.x) {
     const int qq = idx / og.n0, i0 = idx - qq * og.n0;
-    const int q = q0 + qq;
+    const int q = sm_.qs[sm_.me] + q0 + qq;  // global (k2, k1) pencil index
     double xi[kMaxDim];
     xi[0] = g.xi[0][i0];
     bool zero_mode = (i0 == 0);
@@ -895,9 +906,11 @@ __global__ void __launch_bounds__(kThreads) k_outer(Geo g, OuterGeo og, const Rh
   __syncthreads();
   double2* res2 = smem_fft<true>(other, res, P, ld, pl);
   for (int a = 0; a < c; ++a) {
-    double2* d = W + (((int64_t)(r * c + a)) * og.Q + q0) * og.n0;
     const double2* s = res2 + (size_t)a * nq * ld;
-    for (int idx = threadIdx.x; idx < nq * og.n0; idx += blockDim.x) d[idx] = s[idx];
+    for (int idx = threadIdx.x; idx < nq * og.n0; idx += blockDim.x) {
+      const int qq = idx / og.n0, i0 = idx - qq * og.n0;
+      W[outer_index(sm_, og.Q, r * c + a, q0 + qq, i0)] = s[idx];
+    }
   }
 }
 

@@ -94,3 +94,46 @@ def test_nccl_slab_path_single_rank():
     assert r1[0]["iterations"] == rD[0]["iterations"]
     assert rel_l2(xD, x1) <= 1e-13
     np.testing.assert_allclose(dist.energy(E), one.energy(E), rtol=1e-13)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_sharded_generic_lengths(P, rng):
+    """Axes that are not powers of three (the cfg5 grid 1215 = 3^5 5 class) run
+    the shared-memory Stockham kernels, which take the same slab maps: a 45 x 25
+    x 15 grid on P slabs matches the single slab, and the single slab matches
+    the CPU oracle."""
+    import os
+
+    from oracle import fftcell_oracle as orc
+
+    shape = (45, 25, 15)
+    spec = GridSpec((1.0, 1.0, 1.0), shape)
+    a = np.where(rng.random(shape) < 0.3, 20.0, 1.0)
+    one, many = _pair(spec, iso=a, P=P)
+    u = rng.standard_normal((2, 3) + shape)
+    s1, sP = one.apply_system(u), many.apply_system(u)
+    assert np.max(np.abs(s1 - sP)) <= 1e-13 * np.max(np.abs(s1))
+    E = np.array([[1.0, 0.0, 0.0], [0.0, 0.6, 0.8]])
+    r1, x1, _ = one.solve_cg(E, 1e-8, 500)
+    rP, xP, _ = many.solve_cg(E, 1e-8, 500)
+    assert [q["iterations"] for q in r1] == [q["iterations"] for q in rP]
+    assert rel_l2(xP, x1) <= 1e-12
+    ref = orc.solve_cg(orc.isotropic_full(a, 3), tuple(E[0]), shape, (1.0, 1.0, 1.0), 1e-8, 500)
+    assert r1[0]["iterations"] == ref["iterations"]
+    assert rel_l2(x1[0], ref["solution"]) < 1e-9
+
+
+def test_sharded_forced_generic_matches_register_path(monkeypatch):
+    """FC_FORCE_GENERIC=1 routes a power-of-three grid through the Stockham
+    kernels; sharded over 3 slabs it must reproduce the register-path solve."""
+    a = gen.cfg3_sphere(27)
+    E = np.array([[1.0, 0.0, 0.0]])
+    reg = _native.Context(a.spec)
+    reg.set_coefficients(a)
+    r0, x0, _ = reg.solve_cg(E, 1e-8, 500)
+    monkeypatch.setenv("FC_FORCE_GENERIC", "1")
+    gen_many = _native.Context(a.spec, slabs=[0, 0, 0])
+    gen_many.set_coefficients(a)
+    r1, x1, _ = gen_many.solve_cg(E, 1e-8, 500)
+    assert r0[0]["iterations"] == r1[0]["iterations"]
+    assert rel_l2(x1, x0) <= 1e-12
