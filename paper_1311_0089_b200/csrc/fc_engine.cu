@@ -234,8 +234,23 @@ struct fc_ctx {
       m.roff[t] = off;
       off += (long long)R * cdim * (qs[me + 1] - qs[me]) * (s0[t + 1] - s0[t]);
     }
+    if (fused && sibs != nullptr) {  // peer destinations of the fused exchange (SlabMap::fused)
+      m.fused = 1;
+      for (int t = 0; t < P; ++t) {
+        const fc_ctx* o = (*sibs)[t];
+        long long rf = 0, rt = 0;
+        for (int u = 0; u < me; ++u) {
+          rf += (long long)R * cdim * (qs[t + 1] - qs[t]) * (s0[u + 1] - s0[u]);  // o's receive offset of source me
+          rt += (long long)R * cdim * (qs[u + 1] - qs[u]) * (s0[t + 1] - s0[t]);  // o's send offset of destination me
+        }
+        m.fwd[t] = o->W2r + rf;
+        m.ret[t] = o->W2 + rt;
+      }
+    }
     return m;
   }
+  int fused = 0;                                 // fused peer-store exchange (in-process slabs)
+  const std::vector<fc_ctx*>* sibs = nullptr;    // all slabs of the parent (fused exchange)
 };
 
 namespace {
@@ -1071,6 +1086,14 @@ int32_t fc_create_sharded(fc_ctx** out, int32_t dim, const int64_t* shape, const
         }
         cudaGetLastError();
       }
+  // fused exchange: the sweeps store into the other slabs' buffers directly
+  // (FC_FUSED_EXCHANGE=0 keeps the copy-engine exchange)
+  const char* fx = getenv("FC_FUSED_EXCHANGE");
+  const bool fuse = nslabs > 1 && !(fx && atoi(fx) == 0);
+  for (fc_ctx* sl : c->sub) {
+    sl->sibs = &c->sub;
+    sl->fused = fuse && !sl->outer_c1 && !sl->outer_persist;
+  }
   *out = c;
   return FC_OK;
 }

@@ -71,6 +71,14 @@ struct SlabMap {
   int qs[kMaxSlabs + 1];
   long long doff[kMaxSlabs];
   long long roff[kMaxSlabs];
+  // Fused exchange (in-process slabs with peer access): the forward middle
+  // sweep stores block t straight into slab t's receive buffer (fwd[t] = its
+  // segment for this sender) and the outer sweep stores segment t straight
+  // back into slab t's send buffer (ret[t]), over NVLink for slabs on other
+  // GPUs; no copy pass, the transfer overlaps the sweep's arithmetic.
+  int fused;
+  double2* fwd[kMaxSlabs];
+  double2* ret[kMaxSlabs];
 };
 
 __device__ __forceinline__ int slab_of(const int* bounds, int P, int x) {
@@ -85,6 +93,14 @@ __device__ __forceinline__ int64_t send_index(const SlabMap& m, int rc, int q, i
   const int p = slab_of(m.qs, m.P, q);
   const int Qp = m.qs[p + 1] - m.qs[p];
   return m.doff[p] + ((int64_t)rc * Qp + (q - m.qs[p])) * m.n0l + i0l;
+}
+// Destination of a forward-middle-sweep store: the local send block, or (fused)
+// the destination slab's receive segment for this sender.
+__device__ __forceinline__ double2* send_dst(const SlabMap& m, double2* base, int rc, int q, int i0l) {
+  const int p = slab_of(m.qs, m.P, q);
+  const int Qp = m.qs[p + 1] - m.qs[p];
+  const int64_t inner = ((int64_t)rc * Qp + (q - m.qs[p])) * m.n0l + i0l;
+  return (m.fused ? m.fwd[p] : base + m.doff[p]) + inner;
 }
 
 struct Coef {
@@ -812,7 +828,7 @@ __global__ void __launch_bounds__(kThreads) k_mid(Geo g, MidGeo mg, SlabMap sm_,
   if (!INV) {
     for (int idx = threadIdx.x; idx < nr * mg.n1; idx += blockDim.x) {
       const int k1 = idx / nr, row = idx - k1 * nr;
-      dst[send_index(sm_, (int)rc, k2 * mg.n1 + k1, i00 + row)] = res[(size_t)row * ld + k1];
+      *send_dst(sm_, dst, (int)rc, k2 * mg.n1 + k1, i00 + row) = res[(size_t)row * ld + k1];
     }
   } else {
     for (int idx = threadIdx.x; idx < nr * mg.n1; idx += blockDim.x) {
@@ -840,6 +856,14 @@ __device__ __forceinline__ int64_t outer_index(const SlabMap& m, int Q, int rc, 
   const int p = slab_of(m.s0, m.P, i0);
   const int n0p = m.s0[p + 1] - m.s0[p];
   return m.roff[p] + ((int64_t)rc * Q + ql) * n0p + (i0 - m.s0[p]);
+}
+// Destination of an outer-sweep result: in place, or (fused) the owning slab's
+// send block for this slab.
+__device__ __forceinline__ double2* outer_dst(const SlabMap& m, double2* W, int Q, int rc, int ql, int i0) {
+  if (!m.fused) return W + outer_index(m, Q, rc, ql, i0);
+  const int p = slab_of(m.s0, m.P, i0);
+  const int n0p = m.s0[p + 1] - m.s0[p];
+  return m.ret[p] + ((int64_t)rc * Q + ql) * n0p + (i0 - m.s0[p]);
 }
 
 __global__ void __launch_bounds__(kThreads) k_outer(Geo g, OuterGeo og, SlabMap sm_, const RhsState* st, FftPlan pl,
@@ -909,7 +933,7 @@ __global__ void __launch_bounds__(kThreads) k_outer(Geo g, OuterGeo og, SlabMap 
     const double2* s = res2 + (size_t)a * nq * ld;
     for (int idx = threadIdx.x; idx < nq * og.n0; idx += blockDim.x) {
       const int qq = idx / og.n0, i0 = idx - qq * og.n0;
-      W[outer_index(sm_, og.Q, r * c + a, q0 + qq, i0)] = s[idx];
+      *outer_dst(sm_, W, og.Q, r * c + a, q0 + qq, i0) = s[idx];
     }
   }
 }

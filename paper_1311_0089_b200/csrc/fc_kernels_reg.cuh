@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(kMaxBlock) k_mid_r(Geo g, MidGeo mg, SlabMap s
     for (int s = 0; s < 9; ++s) d0[(int64_t)(j + s * TP) * sm_.n0l] = v[0][s];
   } else if (!INV) {
 #pragma unroll
-    for (int s = 0; s < 9; ++s) dst[send_index(sm_, rc, k2 * L + j + s * TP, i00 + p)] = v[0][s];
+    for (int s = 0; s < 9; ++s) *send_dst(sm_, dst, rc, k2 * L + j + s * TP, i00 + p) = v[0][s];
   } else {
     double2* d0 = dst + (((int64_t)rc * mg.n0 + i00 + p) * mg.h2 + k2) * L;
 #pragma unroll
@@ -639,7 +639,10 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
 #pragma unroll
   for (int a = 0; a < C; ++a) {
 #pragma unroll
-    for (int s = 0; s < 9; ++s) W[eoff[s] + (int64_t)(r * C + a) * cstride[s]] = v[a][s];
+    for (int s = 0; s < 9; ++s) {
+      if (sm_.fused) *outer_dst(sm_, W, og.Q, r * C + a, ql, j + s * TP) = v[a][s];
+      else W[eoff[s] + (int64_t)(r * C + a) * cstride[s]] = v[a][s];
+    }
   }
 }
 

@@ -137,3 +137,22 @@ def test_sharded_forced_generic_matches_register_path(monkeypatch):
     r1, x1, _ = gen_many.solve_cg(E, 1e-8, 500)
     assert r0[0]["iterations"] == r1[0]["iterations"]
     assert rel_l2(x1, x0) <= 1e-12
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_fused_exchange_matches_copy_exchange(P, monkeypatch):
+    """Fused exchange (the sweeps store straight into the other slabs' buffers)
+    against the copy-engine exchange: same arithmetic, bitwise-identical solve."""
+    a = gen.cfg3_sphere(27)
+    E = np.array([[1.0, 0.0, 0.0], [0.0, 1.0, 0.0]])
+    fused = _native.Context(a.spec, slabs=[0] * P)
+    fused.set_coefficients(a)
+    rf, xf, _ = fused.solve_cg(E, 1e-8, 500)
+    monkeypatch.setenv("FC_FUSED_EXCHANGE", "0")
+    copy = _native.Context(a.spec, slabs=[0] * P)
+    copy.set_coefficients(a)
+    rc, xc, _ = copy.solve_cg(E, 1e-8, 500)
+    assert [q["iterations"] for q in rf] == [q["iterations"] for q in rc]
+    assert np.array_equal(xf, xc)
+    u = np.random.default_rng(5).standard_normal((2, 3) + a.spec.shape)
+    assert np.array_equal(fused.apply_system(u), copy.apply_system(u))
