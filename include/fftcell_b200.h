@@ -134,6 +134,19 @@ int32_t fc_energy(fc_ctx* ctx, int32_t nrhs, const double* E, const double* x, d
 int32_t fc_generate_voronoi(fc_ctx* ctx, int32_t n_seeds, const double* seeds, const double* packed,
                             int32_t* labels_out);
 
+/* Device generator for the BASELINE cfg5 medium (generators.py:
+ * cfg5_sphere_centres / cfg5_two_phase): balls {|o|^2 < radius^2, o integer,
+ * |o_a| <= ceil(radius)} around integer centres on the periodic grid.
+ * fc_spheres_stamp marks the balls of n centres ((n, 3) int32 voxel indices, in
+ * the caller's drawing order) in a device coverage bitmap (allocated and cleared
+ * by the first stamp after fc_spheres_finish or context creation) and returns in
+ * *covered the number of covered voxels of this context (a slab's planes only;
+ * the caller sums over ranks).  fc_spheres_finish turns the bitmap into the
+ * isotropic coefficient field (inside: high, outside: low) and frees it.  The
+ * result is bit-identical to the host generator for the same centre list. */
+int32_t fc_spheres_stamp(fc_ctx* ctx, int32_t n, const int32_t* centres, double radius, int64_t* covered);
+int32_t fc_spheres_finish(fc_ctx* ctx, double high, double low);
+
 /* Instrumentation used by bench.py: per-kernel CUDA-event timing and a launch counter. */
 int32_t fc_set_profiling(fc_ctx* ctx, int32_t on);
 int32_t fc_profile_count(fc_ctx* ctx);

@@ -62,6 +62,9 @@ SIGNATURES = [
     ("fc_energy", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, _dp, _dp, _dp]),
     ("fc_generate_voronoi", ctypes.c_int32,
      [ctypes.c_void_p, ctypes.c_int32, _dp, _dp, ctypes.POINTER(ctypes.c_int32)]),
+    ("fc_spheres_stamp", ctypes.c_int32,
+     [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_double, _i64p]),
+    ("fc_spheres_finish", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_double, ctypes.c_double]),
     ("fc_set_profiling", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32]),
     ("fc_profile_count", ctypes.c_int32, [ctypes.c_void_p]),
     ("fc_profile_get", ctypes.c_int32,
@@ -189,6 +192,19 @@ class Context:
         _check(lib().fc_generate_voronoi(self._h, seeds.shape[0], _ptr(seeds), _ptr(packed), lp))
         self.isotropic = False
         return labels
+
+    def spheres_stamp(self, centres, radius):
+        """Mark the balls of integer ``centres`` ((n, 3)); returns covered voxels."""
+        cen = np.ascontiguousarray(np.asarray(centres, dtype=np.int32).reshape(-1, 3))
+        cov = ctypes.c_int64(0)
+        _check(lib().fc_spheres_stamp(self._h, cen.shape[0], cen.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                      float(radius), ctypes.byref(cov)))
+        return cov.value
+
+    def spheres_finish(self, high, low):
+        """Coverage bitmap -> isotropic coefficient field (high inside, low outside)."""
+        _check(lib().fc_spheres_finish(self._h, float(high), float(low)))
+        self.isotropic = True
 
     # -- batched field operators ------------------------------------------
     def _batched(self, fn, u, *extra):

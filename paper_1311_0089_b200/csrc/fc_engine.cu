@@ -249,6 +249,8 @@ struct fc_ctx {
     }
     return m;
   }
+  unsigned* sphere_bits = nullptr;               // cfg5 generator coverage bitmap (fc_spheres_stamp)
+  unsigned long long* sphere_count = nullptr;
   int fused = 0;                                 // fused peer-store exchange (in-process slabs)
   const std::vector<fc_ctx*>* sibs = nullptr;    // all slabs of the parent (fused exchange)
 };
@@ -1180,6 +1182,8 @@ void fc_destroy(fc_ctx* c) {
   cudaFree(c->counter);
   cudaFree(c->lsum);
   cudaFree(c->W2r);
+  cudaFree(c->sphere_bits);
+  cudaFree(c->sphere_count);
   for (auto& e : c->sev)
     if (e) cudaEventDestroy(e);
   if (c->h_flag) cudaFreeHost(c->h_flag);
@@ -1555,6 +1559,74 @@ int32_t fc_generate_voronoi(fc_ctx* c, int32_t n_seeds, const double* seeds, con
   cudaFree(d_seeds);
   cudaFree(d_packed);
   cudaFree(d_lab);
+  return FC_OK;
+}
+
+int32_t fc_spheres_stamp(fc_ctx* c, int32_t n, const int32_t* centres, double radius, int64_t* covered) {
+  if (covered == nullptr || (n > 0 && centres == nullptr)) return set_err(FC_EINVAL, "null argument");
+  if (c && !c->sub.empty()) {
+    int64_t tot = 0;
+    for (fc_ctx* sl : c->sub) {
+      int64_t k = 0;
+      TRY(fc_spheres_stamp(sl, n, centres, radius, &k));
+      tot += k;
+    }
+    *covered = tot;
+    return FC_OK;
+  }
+  TRY(check_ctx(c, false));
+  if (c->dim != 3) return set_err(FC_EINVAL, "the sphere generator is three-dimensional");
+  if (!(radius > 0) || radius > 512) return set_err(FC_EINVAL, "radius must lie in (0, 512]");
+  if (n < 0) return set_err(FC_EINVAL, "negative number of centres");
+  if (c->sphere_bits == nullptr) {
+    const size_t words = (size_t)((c->N + 31) / 32);
+    CK(cudaMalloc(&c->sphere_bits, sizeof(unsigned) * words));
+    CK(cudaMalloc(&c->sphere_count, sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(c->sphere_bits, 0, sizeof(unsigned) * words, c->stream));
+    CK(cudaMemsetAsync(c->sphere_count, 0, sizeof(unsigned long long), c->stream));
+  }
+  if (n > 0) {
+    int* d_c = nullptr;
+    CK(cudaMalloc(&d_c, sizeof(int) * 3 * n));
+    CK(cudaMemcpyAsync(d_c, centres, sizeof(int) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    const int rad = (int)std::ceil(radius);
+    const unsigned grid = (unsigned)((int64_t)n * (2 * rad + 1));
+    TRY(launch(c, "stamp_spheres", [&] {
+      k_stamp_spheres<<<grid, 256, 0, c->stream>>>(c->n0g, c->n[1], c->n[2], c->s0[c->me], c->n[0], d_c, n, rad,
+                                                   radius * radius, c->sphere_bits, c->sphere_count);
+    }));
+    TRY(sync(c));
+    cudaFree(d_c);
+  }
+  unsigned long long k = 0;
+  CK(cudaMemcpy(&k, c->sphere_count, sizeof(k), cudaMemcpyDeviceToHost));
+  *covered = (int64_t)k;
+  return FC_OK;
+}
+
+int32_t fc_spheres_finish(fc_ctx* c, double high, double low) {
+  if (c && !c->sub.empty()) {
+    for (fc_ctx* sl : c->sub) TRY(fc_spheres_finish(sl, high, low));
+    c->coef_kind = FC_COEF_ISOTROPIC;
+    return FC_OK;
+  }
+  TRY(check_ctx(c, false));
+  if (c->sphere_bits == nullptr) return set_err(FC_EINVAL, "no spheres stamped");
+  if (c->A == nullptr || c->A_count != c->N) {
+    cudaFree(c->A);
+    c->A = nullptr;
+    CK(cudaMalloc(&c->A, sizeof(double) * c->N + kFieldPad));
+    c->A_count = c->N;
+  }
+  c->coef_kind = FC_COEF_ISOTROPIC;
+  TRY(launch(c, "spheres_field", [&] {
+    k_spheres_field<<<c->num_sms * 8, 256, 0, c->stream>>>(c->N, c->sphere_bits, high, low, c->A);
+  }));
+  TRY(sync(c));
+  cudaFree(c->sphere_bits);
+  cudaFree(c->sphere_count);
+  c->sphere_bits = nullptr;
+  c->sphere_count = nullptr;
   return FC_OK;
 }
 

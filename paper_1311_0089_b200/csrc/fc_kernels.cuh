@@ -1141,6 +1141,44 @@ namespace fc {
 // integer slot indices; squared distance accumulated axis 0, 1, 2 with
 // round-to-nearest ops (no FMA) and strict "<" so the first seed wins ties,
 // exactly as generators.voronoi_labels.  Writes the packed tensor of the grain.
+// cfg5 generator: one CTA per (centre, z offset) slice of the ball; each thread
+// marks voxels (y, x offsets) of that slice in the slab's coverage bitmap and
+// counts the bits it newly set (atomicOr's old value), warp-aggregated.
+__global__ void __launch_bounds__(256) k_stamp_spheres(int n0g, int n1, int n2, int i0_off, int n0l,
+                                                        const int* __restrict__ centres, int ncent, int rad,
+                                                        double r2, unsigned* __restrict__ bits,
+                                                        unsigned long long* __restrict__ count) {
+  const int span = 2 * rad + 1;
+  const int cz = blockIdx.x / span;
+  const int dz = blockIdx.x % span - rad;
+  if (cz >= ncent) return;
+  const int z = ((centres[3 * cz] + dz) % n0g + n0g) % n0g;
+  const int zl = z - i0_off;
+  unsigned long long mine = 0;
+  if (zl >= 0 && zl < n0l) {
+    const int cy = centres[3 * cz + 1], cx = centres[3 * cz + 2];
+    for (int t = threadIdx.x; t < span * span; t += blockDim.x) {
+      const int dy = t / span - rad, dx = t % span - rad;
+      if ((double)(dz * dz + dy * dy + dx * dx) < r2) {
+        const int y = ((cy + dy) % n1 + n1) % n1;
+        const int x = ((cx + dx) % n2 + n2) % n2;
+        const int64_t v = ((int64_t)zl * n1 + y) * n2 + x;
+        const unsigned bit = 1u << (v & 31);
+        const unsigned old = atomicOr(bits + (v >> 5), bit);
+        mine += (old & bit) ? 0 : 1;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(count, mine);
+}
+
+__global__ void k_spheres_field(int64_t N, const unsigned* __restrict__ bits, double high, double low,
+                                double* __restrict__ A) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < N; v += (int64_t)gridDim.x * blockDim.x)
+    A[v] = (bits[v >> 5] >> (v & 31)) & 1u ? high : low;
+}
+
 __global__ void k_gen_voronoi(int n0, int n1, int n2, int i0_off, int G, const double* __restrict__ seeds,
                               const double* __restrict__ packed, int nsym, int64_t N, double* __restrict__ A,
                               int* __restrict__ labels) {

@@ -166,4 +166,27 @@ def cfg5_two_phase(n=1215, seed=SEEDS["cfg5"], radius=None, high=1000.0, low=1.0
     return CoefficientField.isotropic(spec, np.where(covered, high, low))
 
 
+def cfg5_device(ctx, n=1215, seed=SEEDS["cfg5"], radius=None, fraction=0.30, high=1000.0, low=1.0, batch=64,
+                count_fn=None):
+    """cfg5 built on the device (fc_spheres_stamp): the same centre stream and
+    stopping rule as ``cfg5_sphere_centres`` (coverage checked every 16 centres),
+    so the field is bit-identical to ``cfg5_two_phase``.  ``count_fn`` sums the
+    covered-voxel count over ranks (one slab per process); returns the centres used."""
+    radius = 20.0 * n / 1215.0 if radius is None else radius
+    rng = np.random.default_rng(seed)
+    target = fraction * n**3
+    used = []
+    while True:
+        cs = np.floor(rng.uniform(0.0, float(n), size=(batch, 3))).astype(np.int64)
+        for g in range(0, batch, 16):
+            grp = cs[g:g + 16]
+            cov = ctx.spheres_stamp(grp, radius)
+            if count_fn is not None:
+                cov = count_fn(cov)
+            used.append(grp)
+            if cov >= target:
+                ctx.spheres_finish(high, low)
+                return np.concatenate(used).astype(np.float64)
+
+
 CFG5_LOAD = (1.0 / np.sqrt(3.0),) * 3

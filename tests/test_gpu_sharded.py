@@ -156,3 +156,28 @@ def test_fused_exchange_matches_copy_exchange(P, monkeypatch):
     assert np.array_equal(xf, xc)
     u = np.random.default_rng(5).standard_normal((2, 3) + a.spec.shape)
     assert np.array_equal(fused.apply_system(u), copy.apply_system(u))
+
+
+def test_cfg5_device_generator_matches_host():
+    """fc_spheres_stamp / fc_spheres_finish (device cfg5) against the host
+    generator at 81^3 (radius 20 x 81 / 1215): same centre count, and the CG
+    solve on the device-built field equals the one on the uploaded host field
+    bit for bit (same coefficients); also built across 3 slabs."""
+    n = 81
+    spec = GridSpec((1.0,) * 3, (n,) * 3)
+    centres, covered = gen.cfg5_sphere_centres(n, gen.SEEDS["cfg5"], 20.0 * n / 1215.0)
+    host = _native.Context(spec)
+    host.set_coefficients(gen.cfg5_two_phase(n))
+    dev = _native.Context(spec)
+    used = gen.cfg5_device(dev, n)
+    assert used.shape == centres.shape and np.array_equal(used, centres)
+    E = np.array([gen.CFG5_LOAD])
+    r0, x0, _ = host.solve_cg(E, 1e-8, 1000)
+    r1, x1, _ = dev.solve_cg(E, 1e-8, 1000)
+    assert r0[0]["iterations"] == r1[0]["iterations"]
+    assert np.array_equal(x0, x1)
+    many = _native.Context(spec, slabs=[0, 0, 0])
+    gen.cfg5_device(many, n)
+    r2, x2, _ = many.solve_cg(E, 1e-8, 1000)
+    assert r2[0]["iterations"] == r0[0]["iterations"]
+    assert rel_l2(x2, x0) <= 1e-12
