@@ -81,6 +81,9 @@ def test_default_path_matches_oracle(medium, default_solve):
     {"FC_INV_PIPE": "0"},
     {"FC_ROW_PIPE": "1"},
     {"FC_ROW_PIPE": "1", "FC_INV_STAGES": "3"},
+    {"FC_INV_QBUF": "0"},
+    {"FC_OUTER_PERSIST": "1"},
+    {"FC_OUTER_C1_2D": "1"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_variant_is_bitwise_identical(medium, default_solve, env):
     its0, x0 = default_solve
@@ -120,3 +123,36 @@ def test_mid_sweep_variants_3d():
         it, x = run(env)
         assert it == it0, env
         assert np.array_equal(x, x0), (env, rel_l2(x, x0))
+
+
+def test_anisotropic_first_sweep_variants():
+    """Packed coefficients: the split first sweep (pointwise kernel + staged row
+    FFT, default) and the all-components fused first sweep (FC_ANISO_SPLIT=0)
+    give a bitwise-identical CG solve."""
+    from conftest import random_spd_packed
+    from paper_1311_0089_b200 import CoefficientField
+
+    shape = (27, 27, 81)
+    spec = GridSpec((1.0, 1.0, 1.0), shape)
+    packed = random_spd_packed(shape, np.random.default_rng(27))
+    coef = CoefficientField(spec, packed)
+
+    def run(env):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            ctx = _native.Context(spec)
+            ctx.set_coefficients(coef)
+            reps, x, _ = ctx.solve_cg(np.array([[1.0, 0.0, 0.0], [0.0, 0.0, 1.0]]), 1e-8, 1000)
+            return [r["iterations"] for r in reps], x
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+
+    it0, x0 = run({})
+    it1, x1 = run({"FC_ANISO_SPLIT": "0"})
+    assert it0 == it1
+    assert np.array_equal(x0, x1), rel_l2(x1, x0)
