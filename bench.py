@@ -355,6 +355,10 @@ def run_gpu(args):
     if rank != 0:
         return
     peak, peak_kind = peaks()
+    # sharded: rank 0's kernels process its slab only (planes [0, n0/P))
+    local = (wl.shape[0] // world) / wl.shape[0] if sharded else 1.0
+    kbytes = wl.kernel_bytes
+    wl.kernel_bytes = lambda k: None if kbytes(k) is None else kbytes(k) * local
     kern = {k: v for k, v in prof.items() if wl.kernel_bytes(k) is not None}
     top = max(kern, key=lambda k: kern[k][1])
     avg_ms = kern[top][1] / kern[top][0]
@@ -378,9 +382,19 @@ def run_gpu(args):
         avg = v[1] / max(v[0], 1)
         kb = wl.kernel_bytes(k)
         per_kernel[k] = {"launches": v[0], "avg_ms": avg, "GBps": kb / (avg / 1000) / 1e9 if kb else None}
-    iteration = {"bytes": wl.iter_bytes(), "ms": step_ms / n_iter,
-                 "GBps": wl.iter_bytes() / (step_ms / n_iter / 1000) / 1e9}
+    ib = wl.iter_bytes() * local  # per GPU
+    iteration = {"bytes": ib, "ms": step_ms / n_iter, "GBps": ib / (step_ms / n_iter / 1000) / 1e9}
     iteration["frac"] = iteration["GBps"] / peak
+    exchange = None
+    if "exchange" in prof:  # spectrum transposes between ranks, broken out
+        from paper_1311_0089_b200 import parallel
+
+        cnt, tot = prof["exchange"]
+        sent = 16 * sum(int(v) for p, v in enumerate(parallel.exchange_counts(wl.shape, R, world)[rank]) if p != rank)
+        exchange = {"per_exchange_ms": tot / cnt, "exchanges_per_iteration": 2,
+                    "share_of_step": tot / ms_prof, "bytes_sent_per_gpu": sent,
+                    "GBps_per_gpu": sent / (tot / cnt / 1000) / 1e9,
+                    "transport": "NCCL send/recv over NVLink (one process per GPU)"}
     op_names = [k for k in ("row_fwd", "mid_fwd", "outer", "mid_inv", "row_inv") if k in prof]
     op_ms = sum(per_kernel[k]["avg_ms"] for k in op_names)
     op_bytes = sum(wl.kernel_bytes(k) for k in op_names)
@@ -405,6 +419,7 @@ def run_gpu(args):
         "iteration_roofline": iteration,
         "operator_roofline": operator,
         "kernels": per_kernel,
+        "exchange": exchange,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }

@@ -268,6 +268,35 @@ cudaEvent_t take_event(fc_ctx* c) {
   return e;
 }
 
+// Profiling span on the context's stream (no launch counted): bench.py reads
+// it like a kernel, e.g. the NCCL / copy-engine exchanges ("exchange").
+struct ProfSpan {
+  cudaEvent_t e0 = nullptr;
+};
+ProfSpan prof_begin(fc_ctx* c) {
+  ProfSpan sp;
+  if (c->prof_on) {
+    sp.e0 = take_event(c);
+    cudaEventRecord(sp.e0, c->stream);
+  }
+  return sp;
+}
+void prof_end(fc_ctx* c, const char* name, const ProfSpan& sp) {
+  if (!c->prof_on || sp.e0 == nullptr) return;
+  cudaEvent_t e1 = take_event(c);
+  cudaEventRecord(e1, c->stream);
+  auto it = c->prof_idx.find(name);
+  int idx;
+  if (it == c->prof_idx.end()) {
+    idx = (int)c->prof.size();
+    c->prof_idx[name] = idx;
+    c->prof.push_back(Prof{name, 0, 0.0});
+  } else {
+    idx = it->second;
+  }
+  c->pending.push_back({idx, {sp.e0, e1}});
+}
+
 // Launch wrapper: counts launches and (when profiling) brackets with events.
 template <typename F>
 int launch(fc_ctx* c, const char* name, F&& f) {
