@@ -66,12 +66,23 @@ struct DevPlan {
   double2* rtw = nullptr;  // register-FFT twiddle table (L = 3^k only)
 };
 
-bool is_pow3_reg(int L) { return L == 9 || L == 27 || L == 81 || L == 243 || L == 729 || L == 2187; }
+// register-path lengths (fc_fft_reg.cuh): 3^k for 9..2187 and 5 * 3^k for 45..1215
+bool is_pow3_reg(int L) { return fc::is_reg_len(L); }
 
 // Twiddle table of fc_fft_reg.cuh for L = 3^k: for radix-9 pass S >= 1 (Ns = 9^S)
 // tw[off9(S) + (r-1) Ns + k] = w_L^{k r L/(9 Ns)}, r = 1..8, k < Ns; tail block
 // tw[offT + (r-1) L/3 + b] = w_L^{b r}, r = 1, 2, b < L/3.
 std::vector<double2> reg_twiddles(int L, const std::vector<double2>& roots) {
+  if (!fc::is_pow3(L)) {  // L = 5 M: M's table (roots of M = roots of L at multiples of 5) + w_L^{r k2}
+    const int M = L / 5;
+    std::vector<double2> rm(M);
+    for (int t = 0; t < M; ++t) rm[t] = roots[(int64_t)5 * t];
+    std::vector<double2> tw = reg_twiddles(M, rm);
+    if (tw.size() == 1 && fc::R9<9>::table == 0 && M == 9) tw.clear();  // M = 9: no inner table
+    for (int r = 1; r < 5; ++r)
+      for (int k2 = 0; k2 < M; ++k2) tw.push_back(roots[(int64_t)r * k2 % L]);
+    return tw;
+  }
   int K = 0;
   for (int t = L; t > 1; t /= 3) ++K;
   const int NP9 = K / 2;
@@ -537,6 +548,10 @@ int choose_tiles(fc_ctx* c) {
     case 243: { constexpr int LL = 243; BODY; } break;   \
     case 729: { constexpr int LL = 729; BODY; } break;   \
     case 2187: { constexpr int LL = 2187; BODY; } break; \
+    case 45: { constexpr int LL = 45; BODY; } break;     \
+    case 135: { constexpr int LL = 135; BODY; } break;   \
+    case 405: { constexpr int LL = 405; BODY; } break;   \
+    case 1215: { constexpr int LL = 1215; BODY; } break; \
     default: break;                      \
   }
 
@@ -553,7 +568,7 @@ bool env_flag(const char* name, int dflt) {
 int allow_reg_smem(int mx) {
   int rc = FC_OK;
   auto al = [&](auto k) { if (rc == FC_OK) rc = allow_smem(k, mx); };
-  for (int L : {9, 27, 81, 243, 729, 2187}) {
+  for (int L : {9, 27, 81, 243, 729, 2187, 45, 135, 405, 1215}) {
     FC_POW3_SWITCH(L, {
       al(k_row_fwd_r<LL>);
       al(k_row_fwd_pp<LL>);

@@ -110,14 +110,94 @@ struct R9Driver {
   }
 };
 
+__host__ __device__ constexpr bool is_pow3(int L) { return L == 1 || (L % 3 == 0 && is_pow3(L / 3)); }
+// Register-path lengths: 3^k (9 .. 2187) and 5 * 3^k (45 .. 1215, the cfg5 axis)
+__host__ __device__ constexpr bool is_reg_len(int L) {
+  return (L >= 9 && L <= 2187 && is_pow3(L)) || (L % 5 == 0 && L / 5 >= 9 && L / 5 <= 243 && is_pow3(L / 5));
+}
+// threads per pencil: every register-path length holds 9 elements per thread
+template <int L>
+struct RegTP {
+  static_assert(is_reg_len(L), "register FFT length");
+  static constexpr int value = L / 9;
+};
+// twiddle-table entries of length L (3^k: R9 table; 5 M: M's table + 4 M combine twiddles)
+template <int L>
+__host__ __device__ constexpr int reg_table() {
+  if constexpr (is_pow3(L)) return R9<L>::table;
+  else return R9<L / 5>::table + 4 * (L / 5);
+}
+
+template <int L, int CPT, bool INV>
+__device__ __forceinline__ void fft_reg(double2 (&v)[CPT][9], double2* sm, int pstride, int j,
+                                        const double2* __restrict__ tw);
+
+// L = 5 M (M = 3^k >= 9), decimation in time.  Thread j's elements j + s TP all
+// lie in the sub-sequence r = j mod 5 (TP = L/9 is a multiple of 5), at
+// positions j' + s TP/5 with j' = j / 5: the natural register layout of an
+// M-point transform.  Stage A: five M-point register FFTs side by side (group r
+// uses sm + r M as its exchange buffer).  Stage B, through shared memory in
+// place: X[k2 + M k1] = sum_r w5^{r k1} (w_L^{r k2} Y_r[k2]), k2 < M (radix-5
+// butterflies; constant input still gives exact zeros: the sub-transforms leave
+// only Y_r[0] = M x, and the k2 = 0 butterfly of five equal values is exact).
+template <int L, int CPT, bool INV>
+__device__ __forceinline__ void fft_reg_5m(double2 (&v)[CPT][9], double2* sm, int pstride, int j,
+                                           const double2* __restrict__ tw) {
+  constexpr int M = L / 5;
+  constexpr int TP = L / 9;
+  const int r = j % 5;
+  fft_reg<M, CPT, INV>(v, sm + r * M, pstride, j / 5, tw);
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < CPT; ++c)
+#pragma unroll
+    for (int s = 0; s < 9; ++s) sm[c * pstride + r * M + j / 5 + s * (TP / 5)] = v[c][s];
+  __syncthreads();
+  const double2* twc = tw + R9<M>::table;  // w_L^{r k2} at twc[(r - 1) M + k2]
+  for (int k2 = j; k2 < M; k2 += TP) {
+    double2 w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      w[q] = __ldg(twc + q * M + k2);
+      if (INV) w[q].y = -w[q].y;
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      double2* b = sm + c * pstride + k2;
+      double2 x0 = b[0], x1 = b[M], x2 = b[2 * M], x3 = b[3 * M], x4 = b[4 * M];
+      if (k2 != 0) {
+        x1 = cmul(x1, w[0]);
+        x2 = cmul(x2, w[1]);
+        x3 = cmul(x3, w[2]);
+        x4 = cmul(x4, w[3]);
+      }
+      bfly5<INV>(x0, x1, x2, x3, x4);
+      b[0] = x0;
+      b[M] = x1;
+      b[2 * M] = x2;
+      b[3 * M] = x3;
+      b[4 * M] = x4;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < CPT; ++c)
+#pragma unroll
+    for (int s = 0; s < 9; ++s) v[c][s] = sm[c * pstride + j + s * TP];
+}
+
 // Full transform of CPT pencils: on entry v[c][s] = x_c[j + s*TP], on exit X_c[j + s*TP].
 // All threads of the block must call it (it contains block barriers); its last
 // smem access is followed by no barrier, so callers reusing sm must sync first.
 template <int L, int CPT, bool INV>
 __device__ __forceinline__ void fft_reg(double2 (&v)[CPT][9], double2* sm, int pstride, int j,
                                         const double2* __restrict__ tw) {
-  R9Driver<L, CPT, INV, 0>::run(v, sm, pstride, j, tw);
-  if constexpr (R9<L>::TAIL) r3_tail<L, CPT, INV>(v, j, tw);
+  if constexpr (is_pow3(L)) {
+    R9Driver<L, CPT, INV, 0>::run(v, sm, pstride, j, tw);
+    if constexpr (R9<L>::TAIL) r3_tail<L, CPT, INV>(v, j, tw);
+  } else {
+    fft_reg_5m<L, CPT, INV>(v, sm, pstride, j, tw);
+  }
 }
 
 }  // namespace fc

@@ -44,7 +44,7 @@ template <int L>
 __global__ void __launch_bounds__(256, 2) k_row_fwd_pp(Geo g, RowGeo rg, Coef C, InArgs ia, const RhsState* st,
                                                        const double2* __restrict__ tw, int64_t ntile,
                                                        const __grid_constant__ CUtensorMap tmW) {
-  constexpr int TP = R9<L>::TP;
+  constexpr int TP = RegTP<L>::value;
   constexpr int hl = (L + 1) / 2;
   constexpr int stride = pipe_stride<L>();
   constexpr int zoff = (2 * stride + 15) & ~15;  // doubles: Z starts 128-byte aligned
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256, 2) k_row_inv_pp(Geo g, RowGeo rg, EpArgs 
                                                        const double2* __restrict__ tw, int64_t ntile, int stage_c, int nst,
                                                        int qbuf,
                                                        const __grid_constant__ CUtensorMap tmW) {
-  constexpr int TP = R9<L>::TP;
+  constexpr int TP = RegTP<L>::value;
   constexpr int hl = (L + 1) / 2;
   extern __shared__ __align__(128) unsigned char smraw[];
   double2* S = reinterpret_cast<double2*>(smraw);

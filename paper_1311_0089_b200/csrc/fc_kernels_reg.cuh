@@ -55,7 +55,7 @@ template <int L>
 __global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, InArgs ia, const RhsState* st,
                                                           const double2* __restrict__ tw, double2* __restrict__ W,
                                                           const __grid_constant__ CUtensorMap tmW) {
-  constexpr int TP = R9<L>::TP;
+  constexpr int TP = RegTP<L>::value;
   extern __shared__ __align__(128) unsigned char smraw[];  // TMA boxes need 128-byte alignment
   double2* sm = reinterpret_cast<double2*>(smraw);
   const int c = g.dim;
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
                                                           const double2* __restrict__ tw,
                                                           const double2* __restrict__ W, int prefetch,
                                                           const __grid_constant__ CUtensorMap tmW) {
-  constexpr int TP = R9<L>::TP;
+  constexpr int TP = RegTP<L>::value;
   constexpr int hl = (L + 1) / 2;
   extern __shared__ __align__(128) unsigned char smraw[];  // TMA boxes need 128-byte alignment
   double2* sm = reinterpret_cast<double2*>(smraw);
@@ -385,7 +385,7 @@ template <int L, bool INV>
 __device__ __forceinline__ void mid_tma(const Geo& g, const MidGeo& mg, const RhsState* st,
                                         const double2* __restrict__ tw, const double2* __restrict__ src,
                                         double2* __restrict__ dst, const CUtensorMap& tmM, double2* sm) {
-  constexpr int TP = R9<L>::TP;
+  constexpr int TP = RegTP<L>::value;
   const int c = g.dim;
   int64_t bid = blockIdx.x;
   const int ib = bid % mg.nib; bid /= mg.nib;
@@ -457,7 +457,7 @@ template <int L, bool INV>
 __global__ void __launch_bounds__(kMaxBlock) k_mid_r(Geo g, MidGeo mg, SlabMap sm_, const RhsState* st,
                                                       const double2* __restrict__ tw,
                                                       const double2* __restrict__ src, double2* __restrict__ dst) {
-  constexpr int TP = R9<L>::TP;
+  constexpr int TP = RegTP<L>::value;
   extern __shared__ double2 sm[];
   const int c = g.dim;
   int64_t bid = blockIdx.x;
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
                                                                               const RhsState* st,
                                                                               const double2* __restrict__ tw,
                                                                               double2* __restrict__ W) {
-  constexpr int TP = R9<L>::TP;
+  constexpr int TP = RegTP<L>::value;
   extern __shared__ __align__(128) unsigned char smraw[];
   double2* sm = reinterpret_cast<double2*>(smraw);
   const int qb = blockIdx.x % og.nqb;
@@ -660,7 +660,7 @@ template <int L>
 __global__ void __launch_bounds__(kMaxBlock, 1) k_row_fwd_aniso_r(Geo g, RowGeo rg, Coef C, InArgs ia,
                                                                   const RhsState* st, const double2* __restrict__ tw,
                                                                   double2* __restrict__ W, int npen) {
-  constexpr int TP = R9<L>::TP;
+  constexpr int TP = RegTP<L>::value;
   extern __shared__ double2 sm[];
   const int c = g.dim;
   const int nsym = c * (c + 1) / 2;
@@ -774,7 +774,7 @@ namespace fc {
 template <int L, int C>
 __global__ void __launch_bounds__(kMaxBlockOuter, 1) k_outer_p(Geo g, OuterGeo og, SlabMap sm_, const RhsState* st,
                                                                const double2* __restrict__ tw, double2* __restrict__ W) {
-  constexpr int TP = R9<L>::TP;
+  constexpr int TP = RegTP<L>::value;
   extern __shared__ double2 sm[];
   const int stage = og.QB * C * L;
   const int qq = threadIdx.x / TP;
@@ -899,7 +899,7 @@ namespace fc {
 template <int L, int C>
 __global__ void __launch_bounds__(512, 1) k_outer_c1(Geo g, OuterGeo og, SlabMap sm_, const RhsState* st,
                                                      const double2* __restrict__ tw, double2* __restrict__ W) {
-  constexpr int TP = R9<L>::TP;
+  constexpr int TP = RegTP<L>::value;
   extern __shared__ double2 sm[];
   const int qb = blockIdx.x % og.nqb;
   const int r = blockIdx.x / og.nqb;
