@@ -196,6 +196,7 @@ struct fc_ctx {
   int outer_persist = 0;    // persistent double-buffered outer sweep (FC_OUTER_PERSIST)
   int outer_c1 = 0;         // one-component-per-thread outer sweep: pencil groups per CTA (0 = off)
   int row_pipe = 0;         // persistent double-buffered first sweep (FC_ROW_PIPE)
+  int outer_seq = 0;        // outer sweep one component at a time (FC_OUTER_SEQ)
   CUtensorMap tmW{};        // TMA view of the row-sweep spectrum (RowGeo::tma)
   CUtensorMap tmM{};        // TMA view of the middle sweep's transposed side (MidGeo::tma)
   int row_pipe_blocks = 0;  // its resident CTAs per SM
@@ -525,6 +526,9 @@ int choose_tiles(fc_ctx* c) {
     c->outer_qb = qb;
     c->smem_outer_r = (size_t)16 * d * qb * c->n0g;
     og.tma = env_int("FC_OUTER_TMA", 1);
+    // d = 3 with long pencils: one component at a time (measured at 729^3: -19 %;
+    // slower for the small 243-length CTAs and for d = 2)
+    c->outer_seq = env_int("FC_OUTER_SEQ", d == 3 && TP > 32);
     c->outer_persist = env_int("FC_OUTER_PERSIST", 0) && 2 * c->smem_outer_r <= (size_t)c->smem_optin - 2048;
     {
       // one component per thread: d * QB * TP threads (<= 512)
@@ -579,6 +583,8 @@ int allow_reg_smem(int mx) {
       al(k_mid_tma<LL, true>);
       al(k_outer_r<LL, 2>);
       al(k_outer_r<LL, 3>);
+      al(k_outer_seq<LL, 2>);
+      al(k_outer_seq<LL, 3>);
       al(k_outer_p<LL, 2>);
       al(k_outer_p<LL, 3>);
       al(k_outer_c1<LL, 2>);
@@ -834,6 +840,13 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     TRY(launch(c, "outer", [&] {
       if (d == 2) FC_POW3_SWITCH(c->n0g, (k_outer_p<LL, 2><<<grid, nt, smem, s>>>(g, og, smap, st, tw, Wout)))
       else FC_POW3_SWITCH(c->n0g, (k_outer_p<LL, 3><<<grid, nt, smem, s>>>(g, og, smap, st, tw, Wout)))
+    }));
+  } else if (c->outer_qb && c->outer_seq && c->P == 1 && og.tma) {
+    const int nt = c->outer_qb * (c->n0g / 9);
+    const double2* tw = c->rtw(c->n0g);
+    TRY(launch(c, "outer", [&] {
+      if (d == 2) FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 2><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
+      else FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
     }));
   } else if (c->outer_qb) {
     const int nt = c->outer_qb * (c->n0g / 9);

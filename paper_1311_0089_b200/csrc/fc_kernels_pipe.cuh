@@ -314,4 +314,118 @@ __global__ void __launch_bounds__(256, 2) k_row_inv_pp(Geo g, RowGeo rg, EpArgs 
   finish_block(ea.fin, red);
 }
 
+// Outer sweep, components one after another (single slab, TMA pencils): each
+// thread transforms one component pencil at a time (9 complex in registers
+// instead of C x 9), parking the spectra in their shared-memory rows, applies
+// Gamma_hat from shared memory and transforms back.  Fewer registers, so more
+// resident warps than k_outer_r, for one extra shared-memory pass per
+// component.  Same arithmetic as k_outer_r.
+template <int L, int C>
+__global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, OuterGeo og, const RhsState* st,
+                                                                      const double2* __restrict__ tw,
+                                                                      double2* __restrict__ W) {
+  constexpr int TP = RegTP<L>::value;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double2* sm = reinterpret_cast<double2*>(smraw);
+  __shared__ uint64_t bar;
+  const int qb = blockIdx.x % og.nqb;
+  const int r = blockIdx.x / og.nqb;
+  if (!rhs_active(st, r)) return;
+  const int qq = threadIdx.x / TP;
+  const int j = threadIdx.x - qq * TP;
+  const int ql = qb * og.QB + qq;
+  const bool live = ql < og.Q;
+  const int nq = min(og.QB, og.Q - qb * og.QB);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, (unsigned)(C * nq * L * 16));
+#pragma unroll
+    for (int a = 0; a < C; ++a)
+      bulk_g2s(sm + (size_t)a * og.QB * L, W + ((int64_t)(r * C + a) * og.Q + (int64_t)qb * og.QB) * L,
+               (unsigned)(nq * L * 16), &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+#pragma unroll 1
+  for (int a = 0; a < C; ++a) {  // forward transforms, spectra back in place
+    double2* row = sm + ((size_t)a * og.QB + qq) * L;
+    double2 v[1][9];
+#pragma unroll
+    for (int s = 0; s < 9; ++s) v[0][s] = live ? row[j + s * TP] : make_double2(0.0, 0.0);
+    fft_reg<L, 1, false>(v, row, L, j, tw);
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < 9; ++s) row[j + s * TP] = v[0][s];
+  }
+  __syncthreads();
+  if (live) {  // Gamma_hat(k) v = xi (xi . v) / den, 0 at k = 0 (per thread: its own modes)
+    const int q = ql;
+    double xi1 = 0.0, xi2 = 0.0;
+    if (C == 2) {
+      xi1 = g.xi[1][q];
+    } else {
+      const int k2 = q / og.n1, k1 = q - k2 * og.n1;
+      xi1 = g.xi[1][k1];
+      xi2 = g.xi[2][k2];
+    }
+#pragma unroll
+    for (int s = 0; s < 9; ++s) {
+      const int i0 = j + s * TP;
+      double2 v[C];
+#pragma unroll
+      for (int a = 0; a < C; ++a) v[a] = sm[((size_t)a * og.QB + qq) * L + i0];
+      const double xi[3] = {g.xi[0][i0], xi1, xi2};
+      double2 out[C];
+      if (q == 0 && i0 == 0) {
+#pragma unroll
+        for (int a = 0; a < C; ++a) out[a] = make_double2(0.0, 0.0);
+      } else {
+        double2 dots = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int a = 0; a < C; ++a) {
+          dots.x += xi[a] * v[a].x;
+          dots.y += xi[a] * v[a].y;
+        }
+        double den = 0.0;
+        if (og.orth) {
+#pragma unroll
+          for (int a = 0; a < C; ++a) den += xi[a] * xi[a];
+        } else {
+#pragma unroll
+          for (int a = 0; a < C; ++a)
+#pragma unroll
+            for (int b = 0; b < C; ++b) den += xi[a] * og.M[a][b] * xi[b];
+        }
+        const double inv = 1.0 / den;
+        const double2 qv = make_double2(dots.x * inv, dots.y * inv);
+#pragma unroll
+        for (int a = 0; a < C; ++a) out[a] = make_double2(xi[a] * qv.x, xi[a] * qv.y);
+      }
+#pragma unroll
+      for (int a = 0; a < C; ++a) sm[((size_t)a * og.QB + qq) * L + i0] = out[a];
+    }
+  }
+#pragma unroll 1
+  for (int a = 0; a < C; ++a) {  // inverse transforms (each thread reads the modes it wrote)
+    double2* row = sm + ((size_t)a * og.QB + qq) * L;
+    double2 v[1][9];
+#pragma unroll
+    for (int s = 0; s < 9; ++s) v[0][s] = row[j + s * TP];
+    fft_reg<L, 1, true>(v, row, L, j, tw);
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < 9; ++s) row[j + s * TP] = v[0][s];
+  }
+  fence_proxy_async();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int a = 0; a < C; ++a)
+      bulk_s2g(W + ((int64_t)(r * C + a) * og.Q + (int64_t)qb * og.QB) * L, sm + (size_t)a * og.QB * L,
+               (unsigned)(nq * L * 16));
+    bulk_commit();
+    bulk_wait_read0();
+  }
+}
+
 }  // namespace fc

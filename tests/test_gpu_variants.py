@@ -119,7 +119,7 @@ def test_mid_sweep_variants_3d():
                     os.environ[k] = v
 
     it0, x0 = run({})
-    for env in ({"FC_MID_TMA": "0"}, {"FC_OUTER_THREADS": "256"}, {"FC_OUTER_TMA": "0"}):
+    for env in ({"FC_MID_TMA": "0"}, {"FC_OUTER_THREADS": "256"}, {"FC_OUTER_TMA": "0"}, {"FC_OUTER_SEQ": "1"}):
         it, x = run(env)
         assert it == it0, env
         assert np.array_equal(x, x0), (env, rel_l2(x, x0))
