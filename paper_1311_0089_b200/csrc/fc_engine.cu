@@ -68,6 +68,8 @@ struct DevPlan {
 
 // register-path lengths (fc_fft_reg.cuh): 3^k for 9..2187 and 5 * 3^k for 45..1215
 bool is_pow3_reg(int L) { return fc::is_reg_len(L); }
+// lengths the measured-and-off kernel variants are compiled for (FC_EXP_SWITCH)
+bool exp_len(int L) { return L == 243 || L == 729 || L == 2187; }
 
 // Twiddle table of fc_fft_reg.cuh for L = 3^k: for radix-9 pass S >= 1 (Ns = 9^S)
 // tw[off9(S) + (r-1) Ns + k] = w_L^{k r L/(9 Ns)}, r = 1..8, k < Ns; tail block
@@ -467,7 +469,7 @@ int choose_tiles(fc_ctx* c) {
     // doubles), last sweep p / e (2 npen L doubles)
     c->smem_row_r = (size_t)24 * (((size_t)2 * npen * rg.nl + 3) & ~(size_t)1);
     c->inv_prefetch = env_int("FC_INV_PREFETCH", 0);
-    c->row_pipe = env_int("FC_ROW_PIPE", 0) && rg.nl >= 81;
+    c->row_pipe = env_int("FC_ROW_PIPE", 0) && exp_len(rg.nl);
     // TMA boxes of the transposed spectrum: nbox boxes of boxK modes x 2 npen rows
     rg.nbox = (rg.hl + 255) / 256;
     rg.boxK = ((rg.hl + rg.nbox - 1) / rg.nbox + 3) & ~3;  // boxes start 128-byte aligned in smem
@@ -490,7 +492,7 @@ int choose_tiles(fc_ctx* c) {
       const size_t cap = (size_t)env_int("FC_ANISO_SMEM_KB", 160) * 1024;
       int na = (int)std::min<size_t>(cap / per_pen, (size_t)(kMaxBlock / (d * (rg.nl / 9))));
       na = std::min(na, (rg.np + 1) / 2);
-      if (env_int("FC_ANISO_ROWS", 1) && na >= 1) {
+      if (env_int("FC_ANISO_ROWS", 1) && na >= 1 && exp_len(rg.nl)) {
         c->aniso_npen = na;
         c->smem_aniso_r = std::max(per_pen * na, (size_t)16 * d * na * rg.nl);
       }
@@ -528,11 +530,12 @@ int choose_tiles(fc_ctx* c) {
     og.tma = env_int("FC_OUTER_TMA", 1);
     // d = 3 with long pencils: one component at a time (measured at 729^3: -19 %;
     // slower for the small 243-length CTAs and for d = 2)
-    c->outer_seq = env_int("FC_OUTER_SEQ", d == 3 && TP > 32);
-    c->outer_persist = env_int("FC_OUTER_PERSIST", 0) && 2 * c->smem_outer_r <= (size_t)c->smem_optin - 2048;
+    c->outer_seq = env_int("FC_OUTER_SEQ", d == 3 && TP > 32) && (d == 3 || exp_len(c->n0g));
+    c->outer_persist = env_int("FC_OUTER_PERSIST", 0) && exp_len(c->n0g) &&
+                       2 * c->smem_outer_r <= (size_t)c->smem_optin - 2048;
     {
       // one component per thread: d * QB * TP threads (<= 512)
-      const int want = env_int(d == 3 ? "FC_OUTER_C1_3D" : "FC_OUTER_C1_2D", 0);
+      const int want = env_int(d == 3 ? "FC_OUTER_C1_3D" : "FC_OUTER_C1_2D", 0) && exp_len(c->n0g);
       if (want) {
         int qb1 = std::max(1, std::min(og.Q, 512 / (d * TP)));
         while (qb1 > 1 && (size_t)16 * d * qb1 * c->n0g > (size_t)c->smem_optin - 2048) --qb1;
@@ -559,6 +562,18 @@ int choose_tiles(fc_ctx* c) {
     default: break;                      \
   }
 
+// Measured-and-off kernel variants (FC_ROW_PIPE, FC_OUTER_PERSIST, FC_OUTER_C1_*,
+// FC_ANISO_SPLIT=0, FC_OUTER_SEQ for d = 2) are compiled for the BASELINE lengths
+// only (build time); the host enables them only for these lengths.
+#define FC_EXP_SWITCH(L, BODY)                            \
+  switch (L) {                                            \
+    case 243: { constexpr int LL = 243; BODY; } break;   \
+    case 729: { constexpr int LL = 729; BODY; } break;   \
+    case 2187: { constexpr int LL = 2187; BODY; } break; \
+    default: break;                                       \
+  }
+
+
 int env_int_g(const char* name, int dflt) {
   const char* v = getenv(name);
   return v ? atoi(v) : dflt;
@@ -573,22 +588,24 @@ int allow_reg_smem(int mx) {
   int rc = FC_OK;
   auto al = [&](auto k) { if (rc == FC_OK) rc = allow_smem(k, mx); };
   for (int L : {9, 27, 81, 243, 729, 2187, 45, 135, 405, 1215}) {
-    FC_POW3_SWITCH(L, {
-      al(k_row_fwd_r<LL>);
+    FC_EXP_SWITCH(L, {
       al(k_row_fwd_pp<LL>);
       al(k_row_fwd_aniso_r<LL>);
+      al(k_outer_p<LL, 2>);
+      al(k_outer_p<LL, 3>);
+      al(k_outer_c1<LL, 2>);
+      al(k_outer_c1<LL, 3>);
+      al(k_outer_seq<LL, 2>);
+    });
+    FC_POW3_SWITCH(L, {
+      al(k_row_fwd_r<LL>);
       al(k_row_inv_r<LL>);
       al(k_mid_r<LL, false>);
       al(k_mid_r<LL, true>);
       al(k_mid_tma<LL, true>);
       al(k_outer_r<LL, 2>);
       al(k_outer_r<LL, 3>);
-      al(k_outer_seq<LL, 2>);
       al(k_outer_seq<LL, 3>);
-      al(k_outer_p<LL, 2>);
-      al(k_outer_p<LL, 3>);
-      al(k_outer_c1<LL, 2>);
-      al(k_outer_c1<LL, 3>);
     });
   }
   return rc;
@@ -721,7 +738,7 @@ int launch_row_fwd_pp(fc_ctx* c, int R, const InArgs& ia, const RhsState* st, do
   const size_t smem = c->smem_row_pp;
   cudaStream_t s = c->stream;
   return launch(c, "row_fwd", [&] {
-    FC_POW3_SWITCH(rp.nl, (k_row_fwd_pp<LL><<<grid, nt, smem, s>>>(g, rp, C, ia, st, tw, ntile, c->tmW)));
+    FC_EXP_SWITCH(rp.nl, (k_row_fwd_pp<LL><<<grid, nt, smem, s>>>(g, rp, C, ia, st, tw, ntile, c->tmW)));
   });
 }
 
@@ -796,7 +813,7 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     const int64_t nb = (int64_t)R * ra.no * ra.ntiles;
     const int np_ = c->aniso_npen;
     TRY(launch(c, "row_fwd", [&] {
-      FC_POW3_SWITCH(rg.nl, (k_row_fwd_aniso_r<LL><<<(unsigned)nb, nt, c->smem_aniso_r, s>>>(g, ra, C, ia, st, tw, Wrow, np_)));
+      FC_EXP_SWITCH(rg.nl, (k_row_fwd_aniso_r<LL><<<(unsigned)nb, nt, c->smem_aniso_r, s>>>(g, ra, C, ia, st, tw, Wrow, np_)));
     }));
   } else if (c->row_npen && c->row_pipe && row_pipe_ok(c, ia)) {
     TRY(launch_row_fwd_pp(c, R, ia, st, Wrow));
@@ -829,8 +846,8 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     const double2* tw = c->rtw(c->n0g);
     const size_t smem = (size_t)16 * d * o1.QB * c->n0g;
     TRY(launch(c, "outer", [&] {
-      if (d == 2) FC_POW3_SWITCH(c->n0g, (k_outer_c1<LL, 2><<<(unsigned)(R * o1.nqb), nt, smem, s>>>(g, o1, smap, st, tw, Wout)))
-      else FC_POW3_SWITCH(c->n0g, (k_outer_c1<LL, 3><<<(unsigned)(R * o1.nqb), nt, smem, s>>>(g, o1, smap, st, tw, Wout)))
+      if (d == 2) FC_EXP_SWITCH(c->n0g, (k_outer_c1<LL, 2><<<(unsigned)(R * o1.nqb), nt, smem, s>>>(g, o1, smap, st, tw, Wout)))
+      else FC_EXP_SWITCH(c->n0g, (k_outer_c1<LL, 3><<<(unsigned)(R * o1.nqb), nt, smem, s>>>(g, o1, smap, st, tw, Wout)))
     }));
   } else if (c->outer_qb && c->outer_persist) {
     const int nt = c->outer_qb * (c->n0g / 9);
@@ -838,14 +855,14 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     const size_t smem = 2 * (size_t)16 * d * c->outer_qb * c->n0g;
     const unsigned grid = (unsigned)std::min<int64_t>((int64_t)R * og.nqb, c->num_sms);
     TRY(launch(c, "outer", [&] {
-      if (d == 2) FC_POW3_SWITCH(c->n0g, (k_outer_p<LL, 2><<<grid, nt, smem, s>>>(g, og, smap, st, tw, Wout)))
-      else FC_POW3_SWITCH(c->n0g, (k_outer_p<LL, 3><<<grid, nt, smem, s>>>(g, og, smap, st, tw, Wout)))
+      if (d == 2) FC_EXP_SWITCH(c->n0g, (k_outer_p<LL, 2><<<grid, nt, smem, s>>>(g, og, smap, st, tw, Wout)))
+      else FC_EXP_SWITCH(c->n0g, (k_outer_p<LL, 3><<<grid, nt, smem, s>>>(g, og, smap, st, tw, Wout)))
     }));
   } else if (c->outer_qb && c->outer_seq && c->P == 1 && og.tma) {
     const int nt = c->outer_qb * (c->n0g / 9);
     const double2* tw = c->rtw(c->n0g);
     TRY(launch(c, "outer", [&] {
-      if (d == 2) FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 2><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
+      if (d == 2) FC_EXP_SWITCH(c->n0g, (k_outer_seq<LL, 2><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
       else FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
     }));
   } else if (c->outer_qb) {
@@ -1056,7 +1073,7 @@ int create_slab(fc_ctx** out, int32_t dim, const int64_t* shape, const double* h
   }
   if (c->row_pipe) {
     int nb = 0;
-    FC_POW3_SWITCH(c->rg.nl, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_row_fwd_pp<LL>, c->rg.nl / 9, c->smem_row_pp)));
+    FC_EXP_SWITCH(c->rg.nl, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_row_fwd_pp<LL>, c->rg.nl / 9, c->smem_row_pp)));
     c->row_pipe_blocks = nb;
   }
   if (cudaMalloc(&c->any_active, sizeof(int)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "flag alloc"));
