@@ -536,26 +536,15 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
     __syncthreads();
   }
   const int q = sm_.qs[sm_.me] + (live ? ql : 0);  // global (k2, k1) pencil index
-  // element offsets of this pencil's axis-0 entries in the received segments
-  // element offsets of this pencil's axis-0 entries: one contiguous pencil for
-  // a single slab (uniform fast path), received segments otherwise
-  int64_t eoff[9], cstride[9];
-  if (sm_.P == 1) {
-#pragma unroll
-    for (int s = 0; s < 9; ++s) {
-      eoff[s] = (int64_t)ql * L + j + s * TP;
-      cstride[s] = (int64_t)og.Q * L;
-    }
-  } else {
-#pragma unroll
-    for (int s = 0; s < 9; ++s) {
-      const int i0 = j + s * TP;
-      const int p = slab_of(sm_.s0, sm_.P, i0);
-      const int n0p = sm_.s0[p + 1] - sm_.s0[p];
-      eoff[s] = sm_.roff[p] + (int64_t)ql * n0p + (i0 - sm_.s0[p]);
-      cstride[s] = (int64_t)og.Q * n0p;
-    }
-  }
+  // element offset of entry i0 of this pencil's component rc: one contiguous
+  // pencil for a single slab (uniform fast path), received segments otherwise.
+  // Recomputed at the stores instead of held across the transforms (registers).
+  auto eoff = [&](int i0, int rc) -> int64_t {
+    if (sm_.P == 1) return ((int64_t)rc * og.Q + ql) * L + i0;
+    const int p = slab_of(sm_.s0, sm_.P, i0);
+    const int n0p = sm_.s0[p + 1] - sm_.s0[p];
+    return sm_.roff[p] + (int64_t)ql * n0p + (i0 - sm_.s0[p]) + (int64_t)rc * og.Q * n0p;
+  };
   double2 v[C][9];
   if (bulk) {
     mbar_wait(&bar, 0);
@@ -569,7 +558,7 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
     for (int a = 0; a < C; ++a) {
 #pragma unroll
       for (int s = 0; s < 9; ++s)
-        v[a][s] = live ? W[eoff[s] + (int64_t)(r * C + a) * cstride[s]] : make_double2(0.0, 0.0);
+        v[a][s] = live ? W[eoff(j + s * TP, r * C + a)] : make_double2(0.0, 0.0);
     }
   }
   double2* smp = sm + (size_t)qq * C * L;
@@ -641,7 +630,7 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
 #pragma unroll
     for (int s = 0; s < 9; ++s) {
       if (sm_.fused) *outer_dst(sm_, W, og.Q, r * C + a, ql, j + s * TP) = v[a][s];
-      else W[eoff[s] + (int64_t)(r * C + a) * cstride[s]] = v[a][s];
+      else W[eoff(j + s * TP, r * C + a)] = v[a][s];
     }
   }
 }
