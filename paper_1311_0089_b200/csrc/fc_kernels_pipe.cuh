@@ -346,6 +346,58 @@ __global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, Oute
   }
   __syncthreads();
   mbar_wait(&bar, 0);
+  if constexpr (C == 3) {  // four transforms (g3_* in fc_kernels_reg.cuh); same arithmetic as k_outer_r<L, 3>
+    const int k2 = ql / og.n1, k1 = ql - k2 * og.n1;
+    const double xi1 = g.xi[1][live ? k1 : 0];
+    const double xi2 = g.xi[2][live ? k2 : 0];
+    double2* row0 = sm + ((size_t)0 * og.QB + qq) * L;
+    double2* row1 = sm + ((size_t)1 * og.QB + qq) * L;
+    double2* row2 = sm + ((size_t)2 * og.QB + qq) * L;
+#pragma unroll 1
+    for (int a = 0; a < 2; ++a) {  // F0 v0 -> row0, F0 (xi1 v1 + xi2 v2) -> row1
+      double2* row = a == 0 ? row0 : row1;
+      double2 v[1][9];
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+        const int i = j + s * TP;
+        v[0][s] = !live ? make_double2(0.0, 0.0) : a == 0 ? row0[i] : g3_fold(xi1, xi2, row1[i], row2[i]);
+      }
+      fft_reg<L, 1, false>(v, row, L, j, tw);
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < 9; ++s) row[j + s * TP] = v[0][s];
+    }
+    __syncthreads();
+    if (live) {
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+        const int i0 = j + s * TP;
+        double2 t0 = row0[i0], t1 = row1[i0];
+        g3_mode(og, g.xi[0][i0], xi1, xi2, ql == 0 && i0 == 0, t0, t1);
+        row0[i0] = t0;
+        row1[i0] = t1;
+      }
+    }
+#pragma unroll 1
+    for (int a = 0; a < 2; ++a) {  // row0 <- F0^-1(xi0 q); rows 1, 2 <- xi1 / xi2 F0^-1(q)
+      double2* row = a == 0 ? row0 : row1;
+      double2 v[1][9];
+#pragma unroll
+      for (int s = 0; s < 9; ++s) v[0][s] = row[j + s * TP];
+      fft_reg<L, 1, true>(v, row, L, j, tw);
+      __syncthreads();
+      if (a == 0) {
+#pragma unroll
+        for (int s = 0; s < 9; ++s) row0[j + s * TP] = v[0][s];
+      } else {
+#pragma unroll
+        for (int s = 0; s < 9; ++s) {
+          row1[j + s * TP] = g3_scale(xi1, v[0][s]);
+          row2[j + s * TP] = g3_scale(xi2, v[0][s]);
+        }
+      }
+    }
+  } else {
 #pragma unroll 1
   for (int a = 0; a < C; ++a) {  // forward transforms, spectra back in place
     double2* row = sm + ((size_t)a * og.QB + qq) * L;
@@ -416,6 +468,7 @@ __global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, Oute
 #pragma unroll
     for (int s = 0; s < 9; ++s) row[j + s * TP] = v[0][s];
   }
+  }  // C == 2
   fence_proxy_async();
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -502,6 +502,43 @@ __global__ void __launch_bounds__(kMaxBlock) k_mid_r(Geo g, MidGeo mg, SlabMap s
   }
 }
 
+// d = 3 outer sweep with four axis-0 transforms instead of six.  Along an
+// axis-0 pencil xi1 and xi2 are constants, so
+//   xi . F0(v) = xi0 F0(v0) + F0(xi1 v1 + xi2 v2)
+//   F0^-1(xi_a q) = xi_a F0^-1(q)   (a = 1, 2),   q = (xi . v^) / den,
+// i.e. one forward transform of v0, one of the folded u = xi1 v1 + xi2 v2, one
+// inverse of xi0 q and one of q, whose result is scaled by xi1 / xi2.  Same
+// operator up to rounding; the helpers below fix the arithmetic (explicit
+// roundings) so every d = 3 outer kernel that uses them agrees bitwise.
+__device__ __forceinline__ double2 g3_fold(double xi1, double xi2, double2 v1, double2 v2) {
+  return make_double2(__fma_rn(xi2, v2.x, __dmul_rn(xi1, v1.x)), __fma_rn(xi2, v2.y, __dmul_rn(xi1, v1.y)));
+}
+// (F0 v0, F0 u) at one mode -> (xi0 q, q); both 0 at k = 0
+__device__ __forceinline__ void g3_mode(const OuterGeo& og, double xi0, double xi1, double xi2, bool kzero,
+                                        double2& t0, double2& t1) {
+  if (kzero) {
+    t0 = make_double2(0.0, 0.0);
+    t1 = make_double2(0.0, 0.0);
+    return;
+  }
+  double den;
+  if (og.orth) {
+    den = __fma_rn(xi2, xi2, __fma_rn(xi1, xi1, __dmul_rn(xi0, xi0)));
+  } else {
+    const double xi[3] = {xi0, xi1, xi2};
+    den = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) den = __fma_rn(__dmul_rn(xi[a], og.M[a][b]), xi[b], den);
+  }
+  const double inv = 1.0 / den;
+  const double2 qv = make_double2(__dmul_rn(__fma_rn(xi0, t0.x, t1.x), inv), __dmul_rn(__fma_rn(xi0, t0.y, t1.y), inv));
+  t0 = make_double2(__dmul_rn(xi0, qv.x), __dmul_rn(xi0, qv.y));
+  t1 = qv;
+}
+__device__ __forceinline__ double2 g3_scale(double xi, double2 v) { return make_double2(__dmul_rn(xi, v.x), __dmul_rn(xi, v.y)); }
+
 // Outer sweep: each thread owns the C component pencils of one q so Gamma_hat
 // is applied in registers between the forward and inverse transforms.
 template <int L, int C>
@@ -545,6 +582,64 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
     const int n0p = sm_.s0[p + 1] - sm_.s0[p];
     return sm_.roff[p] + (int64_t)ql * n0p + (i0 - sm_.s0[p]) + (int64_t)rc * og.Q * n0p;
   };
+  if constexpr (C == 3) {
+    const int k2 = q / og.n1, k1 = q - k2 * og.n1;
+    const double xi1 = g.xi[1][live ? k1 : 0];
+    const double xi2 = g.xi[2][live ? k2 : 0];
+    auto ld = [&](int a, int i0) -> double2 {
+      return bulk ? sm[((size_t)a * og.QB + qq) * L + i0] : W[eoff(i0, r * 3 + a)];
+    };
+    double2 v[2][9];
+    if (bulk) mbar_wait(&bar, 0);
+#pragma unroll
+    for (int s = 0; s < 9; ++s) {
+      const int i0 = j + s * TP;
+      v[0][s] = live ? ld(0, i0) : make_double2(0.0, 0.0);
+      v[1][s] = live ? g3_fold(xi1, xi2, ld(1, i0), ld(2, i0)) : make_double2(0.0, 0.0);
+    }
+    double2* smp = sm + (size_t)qq * C * L;
+    fft_reg<L, 2, false>(v, smp, L, j, tw);
+    const bool qzero = live && q == 0;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) {
+      const int i0 = j + s * TP;
+      g3_mode(og, g.xi[0][i0], xi1, xi2, qzero && i0 == 0, v[0][s], v[1][s]);
+    }
+    fft_reg<L, 2, true>(v, smp, L, j, tw);
+    if (bulk) {
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+        const int i0 = j + s * TP;
+        sm[((size_t)0 * og.QB + qq) * L + i0] = v[0][s];
+        sm[((size_t)1 * og.QB + qq) * L + i0] = g3_scale(xi1, v[1][s]);
+        sm[((size_t)2 * og.QB + qq) * L + i0] = g3_scale(xi2, v[1][s]);
+      }
+      fence_proxy_async();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int a = 0; a < C; ++a)
+          bulk_s2g(W + ((int64_t)(r * C + a) * og.Q + (int64_t)qb * og.QB) * L, sm + (size_t)a * og.QB * L,
+                   (unsigned)(nq * L * 16));
+        bulk_commit();
+        bulk_wait_read0();
+      }
+      return;
+    }
+    if (!live) return;
+#pragma unroll
+    for (int s = 0; s < 9; ++s) {
+      const int i0 = j + s * TP;
+      const double2 o[3] = {v[0][s], g3_scale(xi1, v[1][s]), g3_scale(xi2, v[1][s])};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (sm_.fused) *outer_dst(sm_, W, og.Q, r * C + a, ql, i0) = o[a];
+        else W[eoff(i0, r * C + a)] = o[a];
+      }
+    }
+    return;
+  } else {
   double2 v[C][9];
   if (bulk) {
     mbar_wait(&bar, 0);
@@ -633,6 +728,7 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
       else W[eoff(j + s * TP, r * C + a)] = v[a][s];
     }
   }
+  }  // C == 2
 }
 
 }  // namespace fc
