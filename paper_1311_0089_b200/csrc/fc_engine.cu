@@ -1433,6 +1433,12 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
     nit = 1;
   }
   const bool record = iterates != nullptr;
+  // x += alpha p is deferred into the next iteration's first sweep, which reads
+  // p_old anyway (saves the x read of p in k_cg_update: 1 of its 6 words per
+  // element); the last update of each RHS is flushed after the loop.  Bitwise
+  // identical to the immediate update.  record_iterates needs x every iteration.
+  static const bool defer_env = env_flag("FC_DEFER_X", 1);
+  const bool defer = defer_env && !record;
   for (int it = 0; any && it < max_iter; ++it) {
     double* pcur = c->p[it & 1];
     double* pold = c->p[(it + 1) & 1];
@@ -1442,6 +1448,7 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
     ia.u = c->r;
     ia.p_old = pold;
     ia.p_new = pcur;
+    ia.xacc = defer ? c->x : nullptr;
     EpArgs ea{};
     ea.mode = EP_AP;
     ea.out = c->Ap;
@@ -1452,7 +1459,8 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
     dim3 grid(nvec, R);
     FinArgs fb = fin_args(c, FIN_BETA, R, nvec, tol, max_iter);
     TRY(launch(c, "cg_update", [&] {
-      k_cg_update<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->st, c->x, c->r, pcur, c->Ap, c->part, nvec, fb);
+      k_cg_update<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->st, defer ? nullptr : c->x, c->r, pcur, c->Ap,
+                                            c->part, nvec, fb);
     }));
     // the flag is monotone (an inactive RHS never reactivates), so reading a
     // later iteration's value is always a valid stop decision
@@ -1474,6 +1482,21 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
   }
   TRY(sync(c));
   CK(cudaMemcpy(hs.data(), c->st, sizeof(RhsState) * R, cudaMemcpyDeviceToHost));
+  if (defer) {
+    // a RHS whose last k_cg_update stopped it (converged or max_iter) still owes
+    // alpha_k p_k; one stopped by breakdown (or at r0) owes nothing.  RHS r was
+    // active in loop iterations 0 .. iterations-1, so p_k is p[(iterations-1) & 1]
+    for (int r = 0; r < R; ++r) {
+      const RhsState& q = hs[r];
+      const bool owes = q.iterations >= 1 && q.status != ST_BREAKDOWN && (q.converged || q.status == ST_MAXITER);
+      if (!owes) continue;
+      const double* pl = c->p[(q.iterations - 1) & 1];
+      TRY(launch(c, "x_flush", [&] {
+        k_x_flush<<<(unsigned)std::min<int64_t>(4 * 148, ((int64_t)d * c->N + kThreads - 1) / kThreads), kThreads, 0,
+                    s>>>((int64_t)d * c->N, c->st, r, c->x, pl);
+      }));
+    }
+  }
   const int hc = c->hcap;
   for (int r = 0; r < R; ++r) {
     rep[r].iterations = hs[r].iterations;

@@ -114,6 +114,7 @@ struct InArgs {
   const double* u;            // IN_FIELD / IN_RAW source, IN_FP e, IN_PNEW r
   const double* p_old;        // IN_PNEW
   double* p_new;              // IN_PNEW
+  double* xacc;               // IN_PNEW: deferred x += alpha p_old (null: k_cg_update updates x)
   double E[8][kMaxDim];       // per-RHS loads (IN_CONST / IN_FP uses A0 below)
   double A0[kMaxDim][kMaxDim];
 };
@@ -178,11 +179,12 @@ __device__ __forceinline__ bool rhs_active(const RhsState* st, int r) {
 // loads of a thread can be issued back to back.
 struct InEval {
   int mode, d, a;
-  double s, beta;
+  double s, beta, alpha;
   bool first;
   int64_t N, base;
   const double* u;
   const double* p_old;
+  double* xacc;  // deferred x update of the previous iteration (IN_PNEW, not first)
   const double* A;
   int kind;
   double E0, E1, E2, Ea;  // load of this RHS (scalars: no local-memory arrays)
@@ -226,7 +228,9 @@ struct InEval {
       if constexpr (KIND == 0) {
         const int64_t e = base + a * N + v;
         const double x = __ldg(u + e);
-        const double q = first ? x : __dadd_rn(x, __dmul_rn(beta, __ldg(p_old + e)));
+        const double po = first ? 0.0 : __ldg(p_old + e);
+        const double q = first ? x : __dadd_rn(x, __dmul_rn(beta, po));
+        if (xacc) xacc[e] = __dadd_rn(xacc[e], __dmul_rn(alpha, po));
         pn = q;
         acc = __dmul_rn(__ldg(A + v), q);
       } else {
@@ -235,8 +239,12 @@ struct InEval {
           if (b >= d) break;
           const int64_t e = base + b * N + v;
           const double x = __ldg(u + e);
-          const double q = first ? x : __dadd_rn(x, __dmul_rn(beta, __ldg(p_old + e)));
-          if (b == a) pn = q;
+          const double po = first ? 0.0 : __ldg(p_old + e);
+          const double q = first ? x : __dadd_rn(x, __dmul_rn(beta, po));
+          if (b == a) {
+            pn = q;
+            if (xacc) xacc[e] = __dadd_rn(xacc[e], __dmul_rn(alpha, po));
+          }
           acc = __dadd_rn(acc, __dmul_rn(__ldg(A + (int64_t)pidx(d, a, b) * N + v), q));
         }
       }
@@ -281,7 +289,9 @@ struct InEval {
         if (kind == 0) {
           const int64_t e = base + a * N + v;
           const double x = __ldg(u + e);
-          const double q = first ? x : __dadd_rn(x, __dmul_rn(beta, __ldg(p_old + e)));
+          const double po = first ? 0.0 : __ldg(p_old + e);
+          const double q = first ? x : __dadd_rn(x, __dmul_rn(beta, po));
+          if (xacc) xacc[e] = __dadd_rn(xacc[e], __dmul_rn(alpha, po));
           pn = q;
           acc = __dmul_rn(__ldg(A + v), q);
         } else {
@@ -290,8 +300,12 @@ struct InEval {
             if (b >= d) break;
             const int64_t e = base + b * N + v;
             const double x = __ldg(u + e);
-            const double q = first ? x : __dadd_rn(x, __dmul_rn(beta, __ldg(p_old + e)));
-            if (b == a) pn = q;
+            const double po = first ? 0.0 : __ldg(p_old + e);
+            const double q = first ? x : __dadd_rn(x, __dmul_rn(beta, po));
+            if (b == a) {
+              pn = q;
+              if (xacc) xacc[e] = __dadd_rn(xacc[e], __dmul_rn(alpha, po));
+            }
             acc = __dadd_rn(acc, __dmul_rn(coefv(b, v), q));
           }
         }
@@ -347,6 +361,8 @@ __device__ __forceinline__ InEval make_eval(const InArgs& ia, const Geo& g, cons
   ev.kind = C.kind;
   ev.first = ia.mode == IN_PNEW ? st[r].first != 0 : true;
   ev.beta = ia.mode == IN_PNEW ? st[r].beta : 0.0;
+  ev.xacc = (ia.mode == IN_PNEW && !ev.first) ? ia.xacc : nullptr;
+  ev.alpha = ev.xacc != nullptr ? st[r].alpha : 0.0;
   // loads / reference rows only where the mode uses them (the static-index
   // selections cost ~100 instructions per thread)
   ev.E0 = ev.E1 = ev.E2 = ev.Ea = 0.0;
@@ -1007,7 +1023,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_update(int64_t len, RhsState* s
   // tile starts at an even offset, so a tile starting at an odd element (odd
   // per-RHS length, r odd) peels one element; an odd tail is done scalar
   auto upd1 = [&](int64_t e) {
-    x[e] = __dadd_rn(x[e], __dmul_rn(alpha, p[e]));
+    if (x) x[e] = __dadd_rn(x[e], __dmul_rn(alpha, p[e]));
     const double rn = __dsub_rn(rr[e], __dmul_rn(alpha, Ap[e]));
     rr[e] = rn;
     return __dmul_rn(rn, rn);
@@ -1022,20 +1038,43 @@ __global__ void __launch_bounds__(kThreads) k_cg_update(int64_t len, RhsState* s
     const double2* p2 = reinterpret_cast<const double2*>(p);
     const double2* a2 = reinterpret_cast<const double2*>(Ap);
     const int64_t h0 = v0 >> 1, h1 = v1 >> 1;
+    if (x) {
 #pragma unroll 4
-    for (int64_t i = h0 + threadIdx.x; i < h1; i += blockDim.x) {
-      const double2 xv = x2[i], rv = r2[i], pv = __ldg(p2 + i), av = __ldg(a2 + i);
-      x2[i] = make_double2(__dadd_rn(xv.x, __dmul_rn(alpha, pv.x)), __dadd_rn(xv.y, __dmul_rn(alpha, pv.y)));
-      const double2 rn = make_double2(__dsub_rn(rv.x, __dmul_rn(alpha, av.x)), __dsub_rn(rv.y, __dmul_rn(alpha, av.y)));
-      r2[i] = rn;
-      acc += __dmul_rn(rn.x, rn.x);
-      acc += __dmul_rn(rn.y, rn.y);
+      for (int64_t i = h0 + threadIdx.x; i < h1; i += blockDim.x) {
+        const double2 xv = x2[i], rv = r2[i], pv = __ldg(p2 + i), av = __ldg(a2 + i);
+        x2[i] = make_double2(__dadd_rn(xv.x, __dmul_rn(alpha, pv.x)), __dadd_rn(xv.y, __dmul_rn(alpha, pv.y)));
+        const double2 rn =
+            make_double2(__dsub_rn(rv.x, __dmul_rn(alpha, av.x)), __dsub_rn(rv.y, __dmul_rn(alpha, av.y)));
+        r2[i] = rn;
+        acc += __dmul_rn(rn.x, rn.x);
+        acc += __dmul_rn(rn.y, rn.y);
+      }
+    } else {  // x deferred to the next first sweep (InArgs::xacc): r and Ap only
+#pragma unroll 4
+      for (int64_t i = h0 + threadIdx.x; i < h1; i += blockDim.x) {
+        const double2 rv = r2[i], av = __ldg(a2 + i);
+        const double2 rn =
+            make_double2(__dsub_rn(rv.x, __dmul_rn(alpha, av.x)), __dsub_rn(rv.y, __dmul_rn(alpha, av.y)));
+        r2[i] = rn;
+        acc += __dmul_rn(rn.x, rn.x);
+        acc += __dmul_rn(rn.y, rn.y);
+      }
     }
   }
   if (threadIdx.x == blockDim.x - 1 && v1 < g1 && v1 >= v0) acc += upd1(v1);
   double s = block_sum(acc, red);
   if (threadIdx.x == 0) part[(int64_t)r * nslot + blockIdx.x] = s;
   finish_block(fin, red);
+}
+
+// x += alpha p for one RHS: the deferred x update of its last CG iteration
+// (the first sweep applies it for every earlier iteration, see InArgs::xacc)
+__global__ void __launch_bounds__(kThreads) k_x_flush(int64_t len, const RhsState* st, int r, double* __restrict__ x,
+                                                      const double* __restrict__ p) {
+  const double alpha = st[r].alpha;
+  const int64_t base = (int64_t)r * len;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+    x[base + i] = __dadd_rn(x[base + i], __dmul_rn(alpha, p[base + i]));
 }
 
 // out = a - b ; partial <out, out>      (r = rhs - op(x), solver.py:186)
@@ -1238,7 +1277,11 @@ __global__ void __launch_bounds__(256) k_pointwise_aniso(Geo g, Coef C, InArgs i
         } else {
           double xb = __ldg(e0.u + base + b * N + v);
           if (e0.mode == IN_PNEW) {
-            if (!e0.first) xb = __dadd_rn(xb, __dmul_rn(e0.beta, __ldg(e0.p_old + base + b * N + v)));
+            if (!e0.first) {
+              const double po = __ldg(e0.p_old + base + b * N + v);
+              xb = __dadd_rn(xb, __dmul_rn(e0.beta, po));
+              if (e0.xacc) e0.xacc[base + b * N + v] = __dadd_rn(e0.xacc[base + b * N + v], __dmul_rn(e0.alpha, po));
+            }
             ia.p_new[base + b * N + v] = xb;
           }
           x[b] = xb;

@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_pp(Geo g, RowGeo rg, Coef C,
   double2* Z = reinterpret_cast<double2*>(S + zoff);
   __shared__ uint64_t bar;
   __shared__ double s_beta[FC_MAX_RHS_DEV];
+  __shared__ double s_alpha[FC_MAX_RHS_DEV];
   __shared__ int s_flags[FC_MAX_RHS_DEV];  // bit 0 active, bit 1 first
   const int c = g.dim;
   const int j = threadIdx.x;  // one pencil per CTA: thread j = FFT lane
@@ -63,6 +64,7 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_pp(Geo g, RowGeo rg, Coef C,
     const bool first = ia.mode == IN_PNEW ? st[r].first != 0 : true;
     s_flags[r] = (act ? 1 : 0) | (first ? 2 : 0);
     s_beta[r] = ia.mode == IN_PNEW ? st[r].beta : 0.0;
+    s_alpha[r] = ia.mode == IN_PNEW ? st[r].alpha : 0.0;
   }
   if (threadIdx.x == 0) mbar_init(&bar, 1);
   __syncthreads();
@@ -117,6 +119,8 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_pp(Geo g, RowGeo rg, Coef C,
     const double* st_u = S + bulk_shift(o.u);
     const double* st_p = S + stride + (o.p ? bulk_shift(o.p) : 0);
     double* pw = pnew ? ia.p_new + (o.u - ia.u) : nullptr;
+    double* xw = (pnew && !first && ia.xacc) ? ia.xacc + (o.u - ia.u) : nullptr;
+    const double alpha = s_alpha[r];
     const double A0aa = ia.mode == IN_FP ? pick3(ia.A0, a, a) : 0.0;
     double2 v[1][9];
 #pragma unroll
@@ -131,6 +135,7 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_pp(Geo g, RowGeo rg, Coef C,
           if (pnew) {
             x = first ? x : __dadd_rn(x, __dmul_rn(beta, st_p[e]));
             pw[e] = x;
+            if (xw) xw[e] = __dadd_rn(xw[e], __dmul_rn(alpha, st_p[e]));
           }
           double val;
           if (ia.mode == IN_RAW) val = x;

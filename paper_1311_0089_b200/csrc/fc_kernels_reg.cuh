@@ -107,6 +107,16 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, 
     st_u += su;
     st_p += sp;
     st_a += sa;
+    // deferred x += alpha p_old of the previous iteration (solver.py:213): the x
+    // loads are issued before the wait so they overlap the bulk copies
+    double* xw = ev.xacc ? ev.xacc + ub : nullptr;
+    double xv[2][9];
+    if (xw) {
+#pragma unroll
+      for (int s = 0; s < 9; ++s)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) xv[h][s] = (2 * p + h < nrows) ? xw[(2 * p + h) * L + j + s * TP] : 0.0;
+    }
     __syncthreads();  // barrier initialised before anyone polls it
     mbar_wait(&bar, 0);
     double* pw = ia.p_new + ub;
@@ -122,6 +132,7 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, 
           const int e = row * L + i;
           double x = st_u[e];
           if (ev.mode == IN_PNEW) {
+            if (xw) xw[e] = __dadd_rn(xv[h][s], __dmul_rn(ev.alpha, st_p[e]));
             x = ev.first ? x : __dadd_rn(x, __dmul_rn(ev.beta, st_p[e]));
             pw[e] = x;
           }
@@ -802,7 +813,13 @@ __global__ void __launch_bounds__(kMaxBlock, 1) k_row_fwd_aniso_r(Geo g, RowGeo 
           x = SU[b * blk + e];
           if (mode == IN_PNEW && !ev.first) x = __dadd_rn(x, __dmul_rn(ev.beta, SP[b * blk + e]));
         }
-        if (mode == IN_PNEW && b == a) q[h] = x;
+        if (mode == IN_PNEW && b == a) {
+          q[h] = x;
+          if (ev.xacc) {
+            double* xw = ev.xacc + rbase + (int64_t)a * g.N + vbase + e;
+            *xw = __dadd_rn(*xw, __dmul_rn(ev.alpha, SP[b * blk + e]));
+          }
+        }
         if (mode == IN_RAW) {
           if (b == a) acc = x;
           continue;
