@@ -190,16 +190,25 @@ class Workload:
         S = 2 * self.d - 1
         return 8 * self.N * (self.nA + 2 * S * c * R + 9 * c * R)
 
+    # single-context solves defer x += alpha p into the next first sweep
+    # (FC_DEFER_X, fc_engine.cu); the sharded paths keep it in cg_update
+    defer_x = os.environ.get("FC_DEFER_X", "1") != "0"
+
     def kernel_bytes(self, name):
-        """Algorithmic bytes of one launch (SURVEY 8(d) byte model, CG loop)."""
+        """Algorithmic bytes of one launch (SURVEY 8(d) byte model, CG loop).
+
+        The per-iteration total (iter_bytes) is the fixed SURVEY model; with the
+        deferred x update 2cR words move from cg_update to row_fwd and cg_update
+        drops its p read, so the per-kernel split follows what each kernel moves."""
         w, c, R, nA = 8, self.d, self.R, self.nA
+        dx = 2 * c * R if self.defer_x else 0
         per = {
-            "row_fwd": w * (nA + 4 * c * R),   # read r, p ; write p' ; write spectrum  (+ A once)
+            "row_fwd": w * (nA + 4 * c * R + dx),  # read r, p ; write p' ; write spectrum (+ A ; + x r/w deferred)
             "mid_fwd": w * 2 * c * R,
             "outer": w * 2 * c * R,
             "mid_inv": w * 2 * c * R,
             "row_inv": w * 3 * c * R,          # read spectrum, write Ap, read p
-            "cg_update": w * 6 * c * R,        # read x, r, p, Ap ; write x, r
+            "cg_update": w * (3 if self.defer_x else 6) * c * R,  # read r, Ap ; write r (+ read x, p ; write x)
         }.get(name)
         return None if per is None else per * self.N
 
@@ -285,6 +294,8 @@ def run_gpu(args):
     # 3-D configs shard along axis 0 across the ranks (NCCL exchanges inside the
     # library, strong scaling); cfg2 runs independent replicas (weak scaling)
     sharded = world > 1 and d == 3 and not args.replicas
+    if sharded:
+        wl.defer_x = False
     if sharded:
         from paper_1311_0089_b200 import parallel
 

@@ -1437,7 +1437,7 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
   // p_old anyway (saves the x read of p in k_cg_update: 1 of its 6 words per
   // element); the last update of each RHS is flushed after the loop.  Bitwise
   // identical to the immediate update.  record_iterates needs x every iteration.
-  static const bool defer_env = env_flag("FC_DEFER_X", 1);
+  const bool defer_env = env_flag("FC_DEFER_X", 1);  // read per solve (tests toggle it)
   const bool defer = defer_env && !record;
   for (int it = 0; any && it < max_iter; ++it) {
     double* pcur = c->p[it & 1];

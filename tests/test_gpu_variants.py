@@ -84,6 +84,8 @@ def test_default_path_matches_oracle(medium, default_solve):
     {"FC_INV_QBUF": "0"},
     {"FC_OUTER_PERSIST": "1"},
     {"FC_OUTER_C1_2D": "1"},
+    {"FC_DEFER_X": "0"},
+    {"FC_DEFER_X": "0", "FC_ROW_PIPE": "1"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_variant_is_bitwise_identical(medium, default_solve, env):
     its0, x0 = default_solve
@@ -156,3 +158,61 @@ def test_anisotropic_first_sweep_variants():
     it1, x1 = run({"FC_ANISO_SPLIT": "0"})
     assert it0 == it1
     assert np.array_equal(x0, x1), rel_l2(x1, x0)
+
+
+def _env_run(env, fn):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("case", ["iso2d_3k", "iso2d_generic", "aniso3d", "aniso3d_fused", "line1d"])
+@pytest.mark.parametrize("max_iter", [4, 1000])
+def test_deferred_x_update_is_bitwise_identical(case, max_iter):
+    """The CG x update deferred into the next first sweep (FC_DEFER_X=1, the
+    default) and flushed after the loop gives the same solution bits as the
+    immediate update in k_cg_update, for RHSs stopping at different iterations,
+    at max_iter, and on every first-sweep kernel (register / generic / split and
+    fused anisotropic / 1-D line)."""
+    from conftest import random_spd_packed
+    from paper_1311_0089_b200 import CoefficientField
+
+    rng = np.random.default_rng(7)
+    env = {}
+    if case == "iso2d_3k":
+        shape, loads = (81, 243), np.array([[1.0, 0.0], [0.0, 1.0], [0.6, 0.8]])
+        coef_fn = lambda spec: CoefficientField.isotropic(spec, np.where(rng.random(shape) < 0.4, 30.0, 1.0))
+    elif case == "iso2d_generic":
+        shape, loads = (25, 35), np.array([[1.0, 0.0], [0.0, 1.0]])
+        coef_fn = lambda spec: CoefficientField.isotropic(spec, np.where(rng.random(shape) < 0.4, 30.0, 1.0))
+    elif case in ("aniso3d", "aniso3d_fused"):
+        shape, loads = (27, 27, 81), np.array([[1.0, 0.0, 0.0], [0.0, 0.0, 1.0]])
+        coef_fn = lambda spec: CoefficientField(spec, random_spd_packed(shape, rng))
+        if case == "aniso3d_fused":
+            env = {"FC_ANISO_SPLIT": "0"}
+    else:
+        # continuous values: with two phases 1-D CG stops after 2 iterations
+        shape, loads = (243,), np.array([[1.0]])
+        coef_fn = lambda spec: CoefficientField.isotropic(spec, 1.0 + 30.0 * rng.random(shape))
+    spec = GridSpec((1.0,) * len(shape), shape)
+    coef = coef_fn(spec)
+
+    def run():
+        ctx = _native.Context(spec)
+        ctx.set_coefficients(coef)
+        reps, x, _ = ctx.solve_cg(loads, 1e-8, max_iter)
+        return [(r["iterations"], r["converged"]) for r in reps], x
+
+    r1, x1 = _env_run({**env, "FC_DEFER_X": "1"}, run)
+    r0, x0 = _env_run({**env, "FC_DEFER_X": "0"}, run)
+    assert r1 == r0
+    assert np.array_equal(x1, x0), rel_l2(x1, x0)
+    if max_iter == 4:
+        assert all(it == 4 and not conv for it, conv in r1)
