@@ -1486,14 +1486,18 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
     // a RHS whose last k_cg_update stopped it (converged or max_iter) still owes
     // alpha_k p_k; one stopped by breakdown (or at r0) owes nothing.  RHS r was
     // active in loop iterations 0 .. iterations-1, so p_k is p[(iterations-1) & 1]
+    unsigned owe = 0u, use1 = 0u;
     for (int r = 0; r < R; ++r) {
       const RhsState& q = hs[r];
-      const bool owes = q.iterations >= 1 && q.status != ST_BREAKDOWN && (q.converged || q.status == ST_MAXITER);
-      if (!owes) continue;
-      const double* pl = c->p[(q.iterations - 1) & 1];
+      if (q.iterations >= 1 && q.status != ST_BREAKDOWN && (q.converged || q.status == ST_MAXITER)) {
+        owe |= 1u << r;
+        if ((q.iterations - 1) & 1) use1 |= 1u << r;
+      }
+    }
+    if (owe != 0u) {
+      const dim3 grid((unsigned)std::min<int64_t>(4 * 148, ((int64_t)d * c->N + kThreads - 1) / kThreads), R);
       TRY(launch(c, "x_flush", [&] {
-        k_x_flush<<<(unsigned)std::min<int64_t>(4 * 148, ((int64_t)d * c->N + kThreads - 1) / kThreads), kThreads, 0,
-                    s>>>((int64_t)d * c->N, c->st, r, c->x, pl);
+        k_x_flush<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->st, c->x, c->p[0], c->p[1], owe, use1);
       }));
     }
   }

@@ -1050,14 +1050,27 @@ __global__ void __launch_bounds__(kThreads) k_cg_update(int64_t len, RhsState* s
         acc += __dmul_rn(rn.y, rn.y);
       }
     } else {  // x deferred to the next first sweep (InArgs::xacc): r and Ap only
-#pragma unroll 4
-      for (int64_t i = h0 + threadIdx.x; i < h1; i += blockDim.x) {
-        const double2 rv = r2[i], av = __ldg(a2 + i);
-        const double2 rn =
-            make_double2(__dsub_rn(rv.x, __dmul_rn(alpha, av.x)), __dsub_rn(rv.y, __dmul_rn(alpha, av.y)));
-        r2[i] = rn;
-        acc += __dmul_rn(rn.x, rn.x);
-        acc += __dmul_rn(rn.y, rn.y);
+      // all loads of the tile issued before the first use (same summation order)
+      constexpr int U = kVecTile / 2 / kThreads;
+      double2 rv[U], av[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = h0 + threadIdx.x + (int64_t)u * kThreads;
+        if (i < h1) {
+          rv[u] = r2[i];
+          av[u] = __ldg(a2 + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = h0 + threadIdx.x + (int64_t)u * kThreads;
+        if (i < h1) {
+          const double2 rn = make_double2(__dsub_rn(rv[u].x, __dmul_rn(alpha, av[u].x)),
+                                          __dsub_rn(rv[u].y, __dmul_rn(alpha, av[u].y)));
+          r2[i] = rn;
+          acc += __dmul_rn(rn.x, rn.x);
+          acc += __dmul_rn(rn.y, rn.y);
+        }
       }
     }
   }
@@ -1069,8 +1082,14 @@ __global__ void __launch_bounds__(kThreads) k_cg_update(int64_t len, RhsState* s
 
 // x += alpha p for one RHS: the deferred x update of its last CG iteration
 // (the first sweep applies it for every earlier iteration, see InArgs::xacc)
-__global__ void __launch_bounds__(kThreads) k_x_flush(int64_t len, const RhsState* st, int r, double* __restrict__ x,
-                                                      const double* __restrict__ p) {
+// RHS r = blockIdx.y is flushed when bit r of owe is set, from p1 when bit r
+// of use1 is set, else from p0.
+__global__ void __launch_bounds__(kThreads) k_x_flush(int64_t len, const RhsState* st, double* __restrict__ x,
+                                                      const double* __restrict__ p0, const double* __restrict__ p1,
+                                                      unsigned owe, unsigned use1) {
+  const int r = blockIdx.y;
+  if (!((owe >> r) & 1u)) return;
+  const double* p = ((use1 >> r) & 1u) ? p1 : p0;
   const double alpha = st[r].alpha;
   const int64_t base = (int64_t)r * len;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
