@@ -1009,14 +1009,18 @@ __global__ void __launch_bounds__(kThreads) k_cg_update(int64_t len, RhsState* s
                                                         const double* __restrict__ Ap, double* part, int nslot,
                                                         FinArgs fin) {
   __shared__ double red[kThreads / 32];
-  const int r = blockIdx.y;
+  // tiles run in reverse order: the first ones read the Ap the last sweep
+  // wrote last (still in L2), the last ones write the r the next first sweep
+  // reads first.  Slot = tile index, so the reduction order is unchanged.
+  const int r = gridDim.y - 1 - blockIdx.y;
+  const int tile = gridDim.x - 1 - blockIdx.x;
   if (!st[r].active) {
     finish_block(fin, red);
     return;
   }
   const double alpha = st[r].alpha;
   const int64_t base = (int64_t)r * len;
-  const int64_t t0 = (int64_t)blockIdx.x * kVecTile;
+  const int64_t t0 = (int64_t)tile * kVecTile;
   const int64_t t1 = min(len, t0 + kVecTile);
   double acc = 0.0;
   // 16-byte accesses for any length: the buffers are 16-byte aligned and every
@@ -1076,7 +1080,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_update(int64_t len, RhsState* s
   }
   if (threadIdx.x == blockDim.x - 1 && v1 < g1 && v1 >= v0) acc += upd1(v1);
   double s = block_sum(acc, red);
-  if (threadIdx.x == 0) part[(int64_t)r * nslot + blockIdx.x] = s;
+  if (threadIdx.x == 0) part[(int64_t)r * nslot + tile] = s;
   finish_block(fin, red);
 }
 
