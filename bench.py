@@ -202,8 +202,14 @@ class Workload:
         drops its p read, so the per-kernel split follows what each kernel moves."""
         w, c, R, nA = 8, self.d, self.R, self.nA
         dx = 2 * c * R if self.defer_x else 0
+        first = w * (nA + 4 * c * R + dx)  # read r, p ; write p' ; write spectrum (+ A ; + x r/w deferred)
+        # packed coefficients run the first sweep split (FC_ANISO_SPLIT, default
+        # on): a pointwise kernel writes y = A p' (one more field write, which the
+        # row FFT reads back) -- charged at the model's bytes plus that round trip
+        split = nA > 1 and os.environ.get("FC_ANISO_SPLIT", "1") != "0"
         per = {
-            "row_fwd": w * (nA + 4 * c * R + dx),  # read r, p ; write p' ; write spectrum (+ A ; + x r/w deferred)
+            "pointwise": first if split else None,
+            "row_fwd": w * 2 * c * R if split else first,
             "mid_fwd": w * 2 * c * R,
             "outer": w * 2 * c * R,
             "mid_inv": w * 2 * c * R,
@@ -406,7 +412,7 @@ def run_gpu(args):
                     "share_of_step": tot / ms_prof, "bytes_sent_per_gpu": sent,
                     "GBps_per_gpu": sent / (tot / cnt / 1000) / 1e9,
                     "transport": "NCCL send/recv over NVLink (one process per GPU)"}
-    op_names = [k for k in ("row_fwd", "mid_fwd", "outer", "mid_inv", "row_inv") if k in prof]
+    op_names = [k for k in ("pointwise", "row_fwd", "mid_fwd", "outer", "mid_inv", "row_inv") if k in prof]
     op_ms = sum(per_kernel[k]["avg_ms"] for k in op_names)
     op_bytes = sum(wl.kernel_bytes(k) for k in op_names)
     operator = {"kernels": op_names, "ms": op_ms, "GBps": op_bytes / (op_ms / 1000) / 1e9}
