@@ -132,7 +132,6 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, 
           const int e = row * L + i;
           double x = st_u[e];
           if (ev.mode == IN_PNEW) {
-            if (xw) xw[e] = __dadd_rn(xv[h][s], __dmul_rn(ev.alpha, st_p[e]));
             x = ev.first ? x : __dadd_rn(x, __dmul_rn(ev.beta, st_p[e]));
             pw[e] = x;
           }
@@ -145,6 +144,15 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, 
         }
       }
       v[0][s] = make_double2(y[0], y[1]);
+    }
+    if (xw) {  // after the pointwise step: the x loads have had the longest time to land
+#pragma unroll
+      for (int s = 0; s < 9; ++s)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = (2 * p + h) * L + j + s * TP;
+          if (2 * p + h < nrows) xw[e] = __dadd_rn(xv[h][s], __dmul_rn(ev.alpha, st_p[e]));
+        }
     }
   } else {
     with_in_mode(ev.mode, ev.kind, [&](auto M, auto K) {
