@@ -190,8 +190,8 @@ class Workload:
         S = 2 * self.d - 1
         return 8 * self.N * (self.nA + 2 * S * c * R + 9 * c * R)
 
-    # single-context solves defer x += alpha p into the next first sweep
-    # (FC_DEFER_X, fc_engine.cu); the sharded paths keep it in cg_update
+    # CG solves defer x += alpha p into the next first sweep (FC_DEFER_X,
+    # fc_engine.cu / fc_shard.inc); record_iterates keeps it in cg_update
     defer_x = os.environ.get("FC_DEFER_X", "1") != "0"
 
     def kernel_bytes(self, name):
@@ -300,8 +300,6 @@ def run_gpu(args):
     # 3-D configs shard along axis 0 across the ranks (NCCL exchanges inside the
     # library, strong scaling); cfg2 runs independent replicas (weak scaling)
     sharded = world > 1 and d == 3 and not args.replicas
-    if sharded:
-        wl.defer_x = False
     if sharded:
         from paper_1311_0089_b200 import parallel
 

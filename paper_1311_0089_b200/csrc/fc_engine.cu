@@ -1483,17 +1483,8 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
   TRY(sync(c));
   CK(cudaMemcpy(hs.data(), c->st, sizeof(RhsState) * R, cudaMemcpyDeviceToHost));
   if (defer) {
-    // a RHS whose last k_cg_update stopped it (converged or max_iter) still owes
-    // alpha_k p_k; one stopped by breakdown (or at r0) owes nothing.  RHS r was
-    // active in loop iterations 0 .. iterations-1, so p_k is p[(iterations-1) & 1]
-    unsigned owe = 0u, use1 = 0u;
-    for (int r = 0; r < R; ++r) {
-      const RhsState& q = hs[r];
-      if (q.iterations >= 1 && q.status != ST_BREAKDOWN && (q.converged || q.status == ST_MAXITER)) {
-        owe |= 1u << r;
-        if ((q.iterations - 1) & 1) use1 |= 1u << r;
-      }
-    }
+    unsigned owe, use1;
+    x_flush_masks(hs.data(), R, owe, use1);
     if (owe != 0u) {
       const dim3 grid((unsigned)std::min<int64_t>(4 * 148, ((int64_t)d * c->N + kThreads - 1) / kThreads), R);
       TRY(launch(c, "x_flush", [&] {

@@ -1100,6 +1100,21 @@ __global__ void __launch_bounds__(kThreads) k_x_flush(int64_t len, const RhsStat
     x[base + i] = __dadd_rn(x[base + i], __dmul_rn(alpha, p[base + i]));
 }
 
+// Host side of the deferred x update: a RHS whose last k_cg_update stopped it
+// (converged or max_iter) still owes alpha_k p_k; one stopped by a breakdown
+// (or at r0) owes nothing.  RHS r was active in loop iterations
+// 0 .. iterations-1, so p_k is p[(iterations - 1) & 1] (use1 bit set: p[1]).
+inline void x_flush_masks(const RhsState* hs, int R, unsigned& owe, unsigned& use1) {
+  owe = use1 = 0u;
+  for (int r = 0; r < R; ++r) {
+    const RhsState& q = hs[r];
+    if (q.iterations >= 1 && q.status != ST_BREAKDOWN && (q.converged || q.status == ST_MAXITER)) {
+      owe |= 1u << r;
+      if ((q.iterations - 1) & 1) use1 |= 1u << r;
+    }
+  }
+}
+
 // out = a - b ; partial <out, out>      (r = rhs - op(x), solver.py:186)
 __global__ void __launch_bounds__(kThreads) k_sub_dot(int64_t len, const double* a, const double* b, double* out,
                                                       double* part, int nslot, FinArgs fin) {

@@ -181,3 +181,19 @@ def test_cfg5_device_generator_matches_host():
     r2, x2, _ = many.solve_cg(E, 1e-8, 1000)
     assert r2[0]["iterations"] == r0[0]["iterations"]
     assert rel_l2(x2, x0) <= 1e-12
+
+
+@pytest.mark.parametrize("max_iter", [5, 500])
+def test_sharded_deferred_x_update_is_bitwise_identical(max_iter, monkeypatch):
+    """Sharded CG with the x update deferred into the first sweep (default)
+    equals the immediate update (FC_DEFER_X=0) bit for bit, including the
+    flush of RHSs stopped by max_iter."""
+    a = gen.cfg3_sphere(27)
+    E = np.array([[1.0, 0.0, 0.0], [0.2, -0.5, 1.0]])
+    _, many = _pair(a.spec, iso=a.isotropic_values, P=3)
+    monkeypatch.setenv("FC_DEFER_X", "1")
+    r1, x1, _ = many.solve_cg(E, 1e-8, max_iter)
+    monkeypatch.setenv("FC_DEFER_X", "0")
+    r0, x0, _ = many.solve_cg(E, 1e-8, max_iter)
+    assert [q["iterations"] for q in r1] == [q["iterations"] for q in r0]
+    assert np.array_equal(x1, x0), rel_l2(x1, x0)
