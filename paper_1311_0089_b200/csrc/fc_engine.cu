@@ -501,7 +501,8 @@ int choose_tiles(fc_ctx* c) {
   if (d == 3 && is_pow3_reg(c->n[1])) {
     MidGeo& mg = c->mg;
     const int TP = c->n[1] / 9;
-    int bp = std::max(1, std::min(16, std::min(env_int("FC_MID_THREADS", 512), kMaxBlock) / TP));
+    // 256 threads for 243-point pencils (cfg3: mid_inv -8 %), 512 for longer ones (cfg4: 256 is slower)
+    int bp = std::max(1, std::min(16, std::min(env_int("FC_MID_THREADS", TP <= 27 ? 256 : 512), kMaxBlock) / TP));
     bp = std::min(bp, c->n[0]);
     mg.B = bp;
     mg.nib = (mg.n0 + bp - 1) / bp;
@@ -530,7 +531,7 @@ int choose_tiles(fc_ctx* c) {
     og.tma = env_int("FC_OUTER_TMA", 1);
     // d = 3 with long pencils: one component at a time (measured at 729^3: -19 %;
     // slower for the small 243-length CTAs and for d = 2)
-    c->outer_seq = env_int("FC_OUTER_SEQ", d == 3 && TP > 32) && (d == 3 || exp_len(c->n0g));
+    c->outer_seq = env_int("FC_OUTER_SEQ", d == 3 && TP >= 27) && (d == 3 || exp_len(c->n0g));
     c->outer_persist = env_int("FC_OUTER_PERSIST", 0) && exp_len(c->n0g) &&
                        2 * c->smem_outer_r <= (size_t)c->smem_optin - 2048;
     {

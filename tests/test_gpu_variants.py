@@ -216,3 +216,23 @@ def test_deferred_x_update_is_bitwise_identical(case, max_iter):
     assert np.array_equal(x1, x0), rel_l2(x1, x0)
     if max_iter == 4:
         assert all(it == 4 and not conv for it, conv in r1)
+
+
+def test_outer_sequential_default_at_243():
+    """243^3 (cfg3 size) runs the one-component-at-a-time outer sweep by
+    default; it must give the same bits as the register version."""
+    from paper_1311_0089_b200 import generators as gen
+
+    a = gen.cfg3_sphere(243)
+    E = np.array([[1.0, 0.0, 0.0]])
+
+    def run():
+        ctx = _native.Context(a.spec)
+        ctx.set_coefficients(a)
+        reps, x, _ = ctx.solve_cg(E, 1e-8, 1000)
+        return reps[0]["iterations"], x
+
+    i1, x1 = _env_run({}, run)
+    i0, x0 = _env_run({"FC_OUTER_SEQ": "0"}, run)
+    assert i1 == i0 == 52
+    assert np.array_equal(x1, x0), rel_l2(x1, x0)
