@@ -346,3 +346,33 @@ def test_device_voronoi_generator_matches_host():
     outs, x, _ = ctx.solve_cg(np.array([[1.0, 0.0, 0.0]]), 1e-8, 2000)
     assert outs[0]["iterations"] == int(g["cg_iterations"])
     assert rel_l2(x[0], g["cg_solution"]) <= max(SOL_TOL, 10 * float(g["cg_floor"]))
+
+
+@pytest.mark.slow
+def test_cfg4_full_size_anchor():
+    """cfg4 at 729^3 (BASELINE configs[3]) against the first CG iterations of the
+    CPU oracle at full size (tests/golden/make_cfg4_anchor.py):
+    same generator (device labels), max_iter = 3, residual history r_0..r_3 within
+    1e-12 relative, the 4096 sampled solution values within 1e-9 relative L2,
+    energy within 1e-10 relative."""
+    from paper_1311_0089_b200 import _native
+
+    g = golden("cfg4_729_anchor")
+    n = int(g["n"])
+    seeds, packed = gen.cfg4_grains(512, gen.SEEDS["cfg4"], n)
+    ctx = _native.Context(GridSpec((1.0,) * 3, (n,) * 3))
+    ctx.generate_voronoi(seeds, packed)
+    E = np.array([[1.0, 0.0, 0.0]])
+    outs, x, _ = ctx.solve_cg(E, 1e-8, int(g["max_iter"]))
+    assert outs[0]["iterations"] == int(g["iterations"])
+    h = outs[0]["history"]
+    ref_h = g["history"]
+    hist_dev = float(np.max(np.abs(h - ref_h) / ref_h[0]))
+    got = x[0].reshape(-1)[g["sample_idx"]]
+    sample_err = rel_l2(got, g["sample"])
+    en = ctx.energy(E)[0, 0]
+    en_err = abs(en - float(g["energy"])) / abs(float(g["energy"]))
+    log_parity({"case": "cfg4_729_anchor", "hist_dev": hist_dev, "sample_err": sample_err, "energy_err": en_err})
+    assert hist_dev <= 1e-12, hist_dev
+    assert sample_err <= SOL_TOL, sample_err
+    assert en_err <= AH_TOL, en_err
