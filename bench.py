@@ -1,24 +1,34 @@
 """Benchmark of the GaNi CG hot path (BASELINE.json metric) on B200.
 
-Workload (BASELINE configs[1], "cfg2"): 2187 x 2187 two-phase random medium
-(contrast 100, seed 2187), three load cases E=(1,0),(0,1),(1,1)/sqrt2 batched in
-ONE device CG solve to relative residual 1e-8.  A step is one complete batched
-solve (about 83 iterations per load case); the metric counts grid points x CG
-iterations per second summed over the load cases.  Synthetic inputs, fp64.
+Headline workload (N = 1): BASELINE configs[3], "cfg4" -- the largest
+single-GPU configuration: a 729^3 polycrystal of 512 seeded Voronoi grains
+with lognormal SPD tensors (packed, 6 words per voxel), E = (1, 0, 0), CG to
+relative residual 1e-8 (132 iterations).  A step is one complete solve; the
+metric counts grid points x CG iterations per second.  Synthetic inputs, fp64.
+The other BASELINE configurations that fit one GPU are measured in the same
+run under ``other_configs``: cfg2 (2187^2, three batched load cases), cfg3
+(243^3 sphere, CG) and cfg3's fixed point (A0 = 25.5 I, tol 1e-6).
 
   value : coefficients resident in HBM before the timed region; solution stays
           on the device.
-  e2e   : the public API with HOST buffers: coefficient upload (pinned), the
-          batched solve, solution download (pinned), every step.
-  roofline: dominant kernel, algorithmic bytes (SURVEY 8(d) model) per launch /
-          its average CUDA-event duration over the timed region vs the measured
-          HBM copy bandwidth in MEASURED_PEAKS.json.
+  e2e   : through the C-ABI binding with HOST buffers: the coefficient field
+          uploaded from pinned memory, the solve, the solution downloaded to
+          pinned memory, every step.
+  roofline: dominant kernel by CUDA-event time; its ALGORITHMIC bytes (SURVEY
+          8(d) model) summed over the launches that did work -- the right-hand
+          side sweeps (profiled as "<kernel>_rhs"), the first iteration (no
+          p_old, no deferred x) and the iterations with fewer active load
+          cases are charged what they move -- over its total time, against the
+          measured HBM copy bandwidth (MEASURED_PEAKS.json).
   cpu_baseline: the CPU oracle port (numpy pocketfft, the reference's own
-          algorithm and calls) on a time-bounded sample, one process per load case.
+          algorithm and calls, single-threaded per process) on the box's host
+          cores, one process per core, measured BEFORE any CUDA work.
 
 ``--impl reference`` times that CPU implementation alone (the reference arm).
-``--gpus N`` under torchrun: independent replicas of the workload, one per GPU
-(weak scaling; the slab-decomposed multi-GPU operator is not in this build).
+``--gpus N`` (N > 1) without torchrun re-launches itself under
+``torch.distributed.run``; cfg3 / cfg4 / cfg5 are then slab-decomposed over the N
+ranks (one GPU each, NCCL exchanges inside the library, strong scaling), cfg2
+runs independent replicas (weak scaling).
 """
 
 from __future__ import annotations
@@ -26,12 +36,12 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import threading
 import time
-from concurrent.futures import ProcessPoolExecutor
 from pathlib import Path
 
 import numpy as np
@@ -43,6 +53,7 @@ METRIC = "CG operator applications/sec (grid pts×iters/s) and achieved HBM GB/s
 UNIT = "grid-pt*iter/s"
 TOL = 1e-8
 MAX_ITER = 2000
+W = 8  # bytes per fp64 word
 
 
 def peaks():
@@ -54,6 +65,16 @@ def peaks():
 
 
 # --------------------------------------------------------------------------- dist
+def relaunch_under_torchrun(n):
+    """`bench.py --gpus N` outside torchrun: re-exec as N ranks on this node."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -135,10 +156,11 @@ class ClockSampler:
 class Workload:
     """One BASELINE configuration: device setup, loads, byte model, CPU sample."""
 
-    def __init__(self, name, n):
+    def __init__(self, name, n=0, world=1):
         from paper_1311_0089_b200 import generators as gen
 
         self.name = name
+        self.method = "cg"
         if name == "cfg2":
             self.n = n or 2187
             self.shape = (self.n, self.n)
@@ -146,297 +168,491 @@ class Workload:
             self.nA = 1
             self.desc = (f"cfg2: {self.n}x{self.n} two-phase random medium (contrast 100, seed 2187), "
                          f"3 load cases batched in one CG solve to 1e-8 (BASELINE configs[1])")
-        elif name == "cfg3":
+        elif name in ("cfg3", "cfg3fp"):
             self.n = n or 243
             self.shape = (self.n,) * 3
             self.loads = np.array([[1.0, 0.0, 0.0]])
             self.nA = 1
-            self.desc = f"cfg3: {self.n}^3 centred sphere (radius 0.35 cell, contrast 50), E=(1,0,0), CG to 1e-8"
+            if name == "cfg3":
+                self.desc = (f"cfg3: {self.n}^3 centred sphere (radius 0.35 cell, contrast 50), E=(1,0,0), "
+                             f"CG to 1e-8 (BASELINE configs[2])")
+            else:
+                self.method = "fixed_point"
+                self.desc = (f"cfg3 fixed point: {self.n}^3 centred sphere (contrast 50), E=(1,0,0), "
+                             f"A0 = 25.5 I, update norm to 1e-6 (BASELINE configs[2])")
         elif name == "cfg4":
             self.n = n or 729
             self.shape = (self.n,) * 3
             self.loads = np.array([[1.0, 0.0, 0.0]])
             self.nA = 6
             self.desc = (f"cfg4: {self.n}^3 polycrystal, 512 seeded Voronoi grains (seed 729) with lognormal "
-                         f"SPD tensors, generated on the device; E=(1,0,0), CG to 1e-8")
+                         f"SPD tensors (packed, 6 words/voxel), generated on the device; E=(1,0,0), CG to 1e-8 "
+                         f"(BASELINE configs[3])")
+        elif name == "cfg5":
+            # full size needs >= 2 GPUs of HBM; one GPU runs the 405^3 down-scale
+            self.n = n or (1215 if world >= 2 else 405)
+            self.shape = (self.n,) * 3
+            self.loads = np.array([gen.CFG5_LOAD])
+            self.nA = 1
+            self.desc = (f"cfg5: {self.n}^3 two-phase medium, seeded overlapping spheres of radius "
+                         f"{20.0 * self.n / 1215:g} voxels to 30% volume fraction (contrast 1000), generated on "
+                         f"the device; E=(1,1,1)/sqrt3, CG to 1e-8 (BASELINE configs[4]"
+                         f"{'' if self.n == 1215 else ', down-scaled from 1215^3'})")
         else:
             raise ValueError(name)
         self.d = len(self.shape)
         self.R = self.loads.shape[0]
         self.N = int(np.prod(self.shape))
 
+    # ---- device setup ------------------------------------------------------
     def host_field(self):
         from paper_1311_0089_b200 import generators as gen
 
         if self.name == "cfg2":
             return gen.cfg2_random_two_phase(self.n)
-        if self.name == "cfg3":
+        if self.name in ("cfg3", "cfg3fp"):
             return gen.cfg3_sphere(self.n)
         return None
 
-    def setup(self, ctx, host_field=None):
-        """Put the coefficient field in HBM (upload, or generate on the device for cfg4)."""
+    def setup(self, ctx, host_field=None, count_fn=None, want_labels=False):
+        """Coefficient field into HBM (upload, or the device generator for cfg4 / cfg5)."""
+        from paper_1311_0089_b200 import generators as gen
+
+        if host_field is not None:
+            ctx.set_coefficients(host_field)
+            return None
         if self.name == "cfg4":
-            from paper_1311_0089_b200 import generators as gen
-
             seeds, packed = gen.cfg4_grains(512, gen.SEEDS["cfg4"], self.n)
-            ctx.generate_voronoi(seeds, packed)
-            return 3 * 512 * 8 + 6 * 512 * 8
-        ctx.set_coefficients(host_field)
-        return host_field.isotropic_values.nbytes
+            return ctx.generate_voronoi(seeds, packed, want_labels=want_labels), packed
+        if self.name == "cfg5":
+            gen.cfg5_device(ctx, self.n, count_fn=count_fn)
+            return None
+        ctx.set_coefficients(self.host_field())
+        return None
 
+    # ---- byte model (SURVEY 8(d)) ----------------------------------------------
     def iter_bytes(self):
-        c, R = self.d, self.R
-        S = 2 * self.d - 1
-        return 8 * self.N * (self.nA + 2 * S * c * R + 9 * c * R)
+        """Fixed SURVEY model per CG iteration (B_iter) or fixed-point iteration (B_fp)."""
+        c, R, S = self.d, self.R, 2 * self.d - 1
+        extra = c * R if self.method == "fixed_point" else 9 * c * R
+        return W * self.N * (self.nA + 2 * S * c * R + extra)
 
-    # CG solves defer x += alpha p into the next first sweep (FC_DEFER_X,
-    # fc_engine.cu / fc_shard.inc); record_iterates keeps it in cg_update
-    defer_x = os.environ.get("FC_DEFER_X", "1") != "0"
+    def launch_words(self, kernel, phase, split):
+        """(coefficient words read once per launch, words per active RHS) per voxel.
 
-    def kernel_bytes(self, name):
-        """Algorithmic bytes of one launch (SURVEY 8(d) byte model, CG loop).
+        phase: "rhs" (IN_CONST first sweep / EP_RHS last sweep), "first" (first CG
+        iteration: p' = r, no deferred x), "steady", "fp" (fixed-point iteration).
+        With ``split`` the packed-coefficient first sweep is a pointwise kernel
+        (writes y = A p') followed by the row FFT on y."""
+        c, nA = self.d, self.nA
+        first_sweep = {"rhs": (nA, c),           # read A ; write spectrum (or y)
+                       "first": (nA, 3 * c),     # + read r ; write p'
+                       "steady": (nA, 6 * c),    # + read p_old ; x read / write (deferred update)
+                       "fp": (nA, 2 * c)}        # read A, e ; write spectrum
+        if kernel == "pointwise":
+            return first_sweep[phase]
+        if kernel == "row_fwd":
+            return (0, 2 * c) if split else first_sweep[phase]
+        if kernel in ("mid_fwd", "outer", "mid_inv"):
+            return (0, 2 * c)
+        if kernel == "row_inv":
+            return (0, 2 * c) if phase == "rhs" else (0, 3 * c)  # spectrum in, r / Ap (+ p or e) out
+        if kernel == "cg_update":
+            return (0, 3 * c)                    # read r, Ap ; write r (x deferred)
+        if kernel == "x_flush":
+            return (0, 3 * c)                    # read x, p ; write x
+        return None
 
-        The per-iteration total (iter_bytes) is the fixed SURVEY model; with the
-        deferred x update 2cR words move from cg_update to row_fwd and cg_update
-        drops its p read, so the per-kernel split follows what each kernel moves."""
-        w, c, R, nA = 8, self.d, self.R, self.nA
-        dx = 2 * c * R if self.defer_x else 0
-        first = w * (nA + 4 * c * R + dx)  # read r, p ; write p' ; write spectrum (+ A ; + x r/w deferred)
-        # packed coefficients run the first sweep split (FC_ANISO_SPLIT, default
-        # on): a pointwise kernel writes y = A p' (one more field write, which the
-        # row FFT reads back) -- charged at the model's bytes plus that round trip
-        split = nA > 1 and os.environ.get("FC_ANISO_SPLIT", "1") != "0"
-        per = {
-            "pointwise": first if split else None,
-            "row_fwd": w * 2 * c * R if split else first,
-            "mid_fwd": w * 2 * c * R,
-            "outer": w * 2 * c * R,
-            "mid_inv": w * 2 * c * R,
-            "row_inv": w * 3 * c * R,          # read spectrum, write Ap, read p
-            "cg_update": w * (3 if self.defer_x else 6) * c * R,  # read r, Ap ; write r (+ read x, p ; write x)
-        }.get(name)
-        return None if per is None else per * self.N
+    def kernel_bytes(self, prof, iters, steps, local=1.0):
+        """Algorithmic bytes per kernel name over the profiled steps (None: not modelled)."""
+        split = "pointwise" in prof
+        out = {}
+        for name in prof:
+            base, _, tag = name.partition("_rhs")
+            rhs = name.endswith("_rhs")
+            kern = name[:-4] if rhs else name
+            if self.launch_words(kern, "steady", split) is None:
+                out[name] = None
+                continue
+            if rhs:
+                a, b = self.launch_words(kern, "rhs", split)
+                words = a + b * self.R
+            elif self.method == "fixed_point":
+                a, b = self.launch_words(kern, "fp", split)
+                words = sum(a + b * sum(1 for it in iters if it >= i) for i in range(1, max(iters) + 1))
+            elif kern == "x_flush":
+                words = self.launch_words(kern, "steady", split)[1] * sum(1 for it in iters if it > 0)
+            else:
+                words = 0
+                for i in range(1, max(iters) + 1):
+                    act = sum(1 for it in iters if it >= i)
+                    a, b = self.launch_words(kern, "first" if i == 1 else "steady", split)
+                    # cg_update of the iteration that stops a RHS still runs for it
+                    words += a + b * act
+            out[name] = W * self.N * local * words * steps
+        return out
 
 
-def _oracle_worker(args):
-    name, n, E, seconds = args
+def config_dict(wl, parallelism):
+    return {"workload": wl.desc, "grid": list(wl.shape), "load_cases": wl.R, "tol": TOL,
+            "method": wl.method, "parallelism": parallelism,
+            "l2": "inputs larger than L2 (per-iteration working set > 126 MB)"}
+
+
+def parallelism_label(world, wl, replicas):
+    if world == 1:
+        return "single"
+    return "replicas" if (wl.d == 2 or replicas) else f"slab{world}"
+
+
+# --------------------------------------------------------------------------- CPU (oracle port)
+_CPU = {}
+
+
+def _cpu_field(name, n):
+    """The workload's coefficient field for the CPU oracle, as full (d, d, *N) tensors.
+
+    cfg4 at 729^3 needs ~170 GB in the reference's layout and ~250 s per iteration
+    on one core, so its CPU sample runs the same generator at 243^3 (labels by a
+    periodic k-d tree: identical to generators.voronoi_labels up to exact
+    distance ties).  cfg5 likewise runs at <= 243^3."""
     from oracle import fftcell_oracle as orc
     from paper_1311_0089_b200 import generators as gen
 
     if name == "cfg2":
-        a = gen.cfg2_random_two_phase(n)
-        full = orc.isotropic_full(a.components[0], 2)
-    elif name == "cfg3":
-        a = gen.cfg3_sphere(n)
-        full = orc.isotropic_full(a.components[0], 3)
-    else:
-        a = gen.cfg4_polycrystal(n)
-        full = orc.unpack(a.components, 3)
-    rep = orc.solve_cg(full, tuple(E), a.spec.shape, a.spec.half_periods, TOL, MAX_ITER, max_seconds=seconds)
-    return rep["iterations"], rep["loop_seconds"], a.spec.total
+        return orc.isotropic_full(gen.cfg2_random_two_phase(n).components[0], 2), n
+    if name in ("cfg3", "cfg3fp"):
+        return orc.isotropic_full(gen.cfg3_sphere(n).components[0], 3), n
+    if name == "cfg4":
+        from scipy.spatial import cKDTree
+
+        n = min(n, 243)
+        seeds, packed = gen.cfg4_grains(512, gen.SEEDS["cfg4"], n)
+        pts = np.indices((n, n, n)).reshape(3, -1).T.astype(float)
+        _, lab = cKDTree(seeds, boxsize=float(n)).query(pts, workers=-1)
+        return orc.unpack(np.moveaxis(packed[lab.reshape(n, n, n)], -1, 0), 3), n
+    n = min(n, 243)
+    return orc.isotropic_full(gen.cfg5_two_phase(n).components[0], 3), n
 
 
-def cpu_sample(wl, seconds):
-    """Time-bounded oracle CG, one process per load case (the reference is single-threaded).
+def _cpu_worker(conn, E, n, d):
+    from oracle import fftcell_oracle as orc
 
-    cfg4 at 729^3 does not fit the reference's ~440 B/voxel; its sample runs the same
-    generator at 81^3 (throughput per grid point is reported)."""
-    n = wl.n if wl.name != "cfg4" else min(wl.n, 81)
-    with ProcessPoolExecutor(len(wl.loads)) as ex:
-        res = list(ex.map(_oracle_worker, [(wl.name, n, E, seconds) for E in wl.loads]))
-    work = sum(N * it for it, _, N in res)
-    t = max(s for _, s, _ in res)
-    its = [it for it, _, _ in res]
-    return work, t, its, n
+    st = orc.CGStepper(_CPU["full"], tuple(E), (n,) * d, (1.0,) * d, TOL)
+    t0 = time.perf_counter()
+    st.setup()
+    conn.send(time.perf_counter() - t0)
+    while True:
+        k = conn.recv()
+        if k is None:
+            break
+        t0 = time.perf_counter()
+        done = 0
+        for _ in range(k):
+            if not st.step():
+                st.setup()  # converged: restart (the sample measures iterations)
+            done += 1
+        conn.send((done, time.perf_counter() - t0))
+
+
+class CpuPool:
+    """One single-threaded oracle CG per host core (load cases round-robin).  Must
+    be created before any CUDA work (the workers are forked)."""
+
+    def __init__(self, wl, procs=None):
+        import multiprocessing as mp
+
+        for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[var] = "1"
+        self.procs = procs or min(os.cpu_count() or 1, 16)
+        full, self.n = _cpu_field(wl.name, wl.n)
+        _CPU["full"] = full
+        self.N = self.n ** wl.d
+        self.wl = wl
+        ctx = mp.get_context("fork")
+        self.conns, self.ps = [], []
+        for w in range(self.procs):
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_cpu_worker, args=(b, wl.loads[w % wl.R], self.n, wl.d), daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.ps.append(p)
+        _CPU.clear()
+        self.setup_s = max(c.recv() for c in self.conns)
+
+    def step(self, k=1):
+        """k CG iterations on every worker; returns (grid-pt iterations, seconds)."""
+        for c in self.conns:
+            c.send(k)
+        res = [c.recv() for c in self.conns]
+        return self.N * sum(r[0] for r in res), max(r[1] for r in res)
+
+    def close(self):
+        for c in self.conns:
+            c.send(None)
+        for p in self.ps:
+            p.join(timeout=30)
+
+    def sample_desc(self, what):
+        return (f"{what}; {self.procs} processes (one per host core, single-threaded numpy pocketfft "
+                f"restatement of solver.py:142-230), {self.wl.name} generator at {self.n}^{self.wl.d}"
+                f"{' (down-scaled: the full size does not fit the reference layout in host RAM)' if self.n != self.wl.n else ''}")
 
 
 # --------------------------------------------------------------------------- arms
 def run_reference(args):
     world, rank, _ = dist_setup()
+    wl = Workload(args.config, args.n, world)
     if rank != 0:
         return
-    wl = Workload(args.config, args.n)
-    total_work, total_t = 0.0, 0.0
-    sample = None
+    pool = CpuPool(wl)
+    work, secs = 0.0, 0.0
     for step in range(args.warmup + args.steps):
-        work, t, its, n = cpu_sample(wl, args.cpu_seconds)
+        w, s = pool.step(1)
         if step >= args.warmup:
-            total_work += work
-            total_t += t
-            sample = (its, n)
-    v = total_work / total_t
+            work += w
+            secs += s
+    pool.close()
+    v = work / secs
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total_t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(wl),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": len(wl.loads), "kind": "port",
-                         "sample": f"per step: the first CG iterations of each of the {len(wl.loads)} load case(s) "
-                                   f"of {wl.name} at {sample[1]}^{wl.d}, {args.cpu_seconds:g} s each, one process "
-                                   f"per load case (numpy pocketfft restatement of solver.py:142-230); "
-                                   f"iterations {sample[0]}"},
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
+        "higher_is_better": True, "scaling": "weak" if parallelism_label(world, wl, args.replicas) != f"slab{world}"
+        else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(wl, parallelism_label(world, wl, args.replicas)),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": pool.procs, "kind": "port",
+                         "sample": pool.sample_desc("per step: one CG iteration on every process (setup and "
+                                                    "right-hand side untimed)")},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def config_dict(wl, parallelism="replicas"):
-    return {"workload": wl.desc, "grid": list(wl.shape), "load_cases": wl.R, "tol": TOL,
-            "parallelism": parallelism,
-            "l2": "inputs larger than L2 (per-iteration working set > 126 MB)"}
+def cpu_baseline(wl, seconds):
+    """Bounded CPU sample for our line: setup, then iterations for ~`seconds`."""
+    pool = CpuPool(wl)
+    work, secs = 0.0, 0.0
+    while secs < seconds:
+        w, s = pool.step(1)
+        work += w
+        secs += s
+    pool.close()
+    return {"value": work / secs, "unit": UNIT, "cores": pool.procs, "kind": "port",
+            "sample": pool.sample_desc(f"{int(work / pool.N / pool.procs)} CG iteration(s) per process after an "
+                                       f"untimed setup of {pool.setup_s:.1f} s")}
+
+
+def roofline_block(wl, prof, iters, steps, ms_prof, peak, peak_kind, local=1.0):
+    kb = wl.kernel_bytes(prof, iters, steps, local)
+    per_kernel = {}
+    for k, (n, ms) in prof.items():
+        per_kernel[k] = {"launches": n, "total_ms": ms, "avg_ms": ms / max(n, 1),
+                         "GBps": kb[k] / (ms / 1000) / 1e9 if kb.get(k) else None,
+                         "bytes": kb.get(k)}
+    modelled = {k: v for k, v in prof.items() if kb.get(k)}
+    top = max(modelled, key=lambda k: modelled[k][1])
+    achieved = kb[top] / (prof[top][1] / 1000) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "ncu_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get(f"{wl.name}/{top}")
+    roof = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
+            "bytes_per_launch": kb[top] / max(prof[top][0], 1), "avg_launch_ms": prof[top][1] / max(prof[top][0], 1),
+            "share_of_step": prof[top][1] / ms_prof,
+            "timing": "CUDA events around every launch on the library stream over a second region of the same "
+                      "steps; bytes = SURVEY 8(d) model per launch that did work (right-hand side, first and "
+                      "steady iterations, active load cases), summed, over the summed launch time"}
+    op_names = [k for k in ("pointwise", "row_fwd", "mid_fwd", "outer", "mid_inv", "row_inv") if k in prof]
+    op_ms = sum(prof[k][1] for k in op_names)
+    op_bytes = sum(kb[k] for k in op_names)
+    operator = {"kernels": op_names, "ms_per_iteration": op_ms / steps / max(iters),
+                "GBps": op_bytes / (op_ms / 1000) / 1e9}
+    operator["frac"] = operator["GBps"] / peak
+    return roof, per_kernel, operator
+
+
+def measure(wl, ctx, args, world, steps, fp_ref=None):
+    """Warm-up, timed value region, profiled region.  Returns a dict of results."""
+    loads = wl.loads
+
+    if wl.method == "fixed_point":
+        scale = np.sqrt(np.sum(loads * loads, axis=1))
+
+        def solve():
+            reps, _ = ctx.solve_fixed_point(loads, 1e-6, MAX_ITER, fp_ref, scale, want_x=False)
+            return reps
+    else:
+        def solve():
+            reps, _, _ = ctx.solve_cg(loads, TOL, MAX_ITER, want_x=False)
+            return reps
+
+    for _ in range(args.warmup):
+        reps = solve()
+    iters = [r["iterations"] for r in reps]
+    launches0 = ctx.launch_count()
+    barrier(world)
+    ctx.timer_mark(0)
+    for _ in range(steps):
+        reps = solve()
+    ctx.timer_mark(1)
+    ms = ctx.timer_elapsed(0, 1)
+    launches = ctx.launch_count() - launches0
+    assert [r["iterations"] for r in reps] == iters
+    psteps = min(steps, args.profile_steps)
+    ctx.profile_reset()
+    ctx.set_profiling(True)
+    barrier(world)
+    ctx.timer_mark(4)
+    for _ in range(psteps):
+        solve()
+    ctx.timer_mark(5)
+    ms_prof = ctx.timer_elapsed(4, 5)
+    ctx.set_profiling(False)
+    prof = ctx.profile()
+    return {"iters": iters, "ms": max_over_ranks(world, ms), "launches": launches, "prof": prof,
+            "psteps": psteps, "ms_prof": ms_prof}
+
+
+def summarize(wl, res, steps, world, sharded, peak, peak_kind):
+    iters = res["iters"]
+    copies = 1 if sharded else world
+    work_per_step = wl.N * sum(iters)
+    value = copies * work_per_step * steps / (res["ms"] / 1000.0)
+    local = (wl.shape[0] // world) / wl.shape[0] if sharded else 1.0
+    roof, per_kernel, operator = roofline_block(wl, res["prof"], iters, res["psteps"], res["ms_prof"], peak,
+                                                peak_kind, local)
+    step_ms = res["ms"] / steps
+    ib = wl.iter_bytes() * local
+    iteration = {"bytes": ib, "ms": step_ms / max(iters), "GBps": ib / (step_ms / max(iters) / 1000) / 1e9}
+    iteration["frac"] = iteration["GBps"] / peak
+    return value, roof, per_kernel, operator, iteration
 
 
 def run_gpu(args):
     world, rank, local = dist_setup()
+    wl = Workload(args.config, args.n, world)
+    label = parallelism_label(world, wl, args.replicas)
+    sharded = label.startswith("slab")
+    cpu = None
+    if world == 1 and not args.no_cpu:  # before any CUDA work (forked workers)
+        cpu = cpu_baseline(wl, args.cpu_seconds)
+
     from paper_1311_0089_b200 import _native
-    from paper_1311_0089_b200.material import CoefficientField
     from paper_1311_0089_b200.grid import GridSpec
 
-    wl = Workload(args.config, args.n)
-    loads, R, N, d = wl.loads, wl.R, wl.N, wl.d
-    host = wl.host_field()
-    spec = GridSpec((1.0,) * d, wl.shape)
-    # 3-D configs shard along axis 0 across the ranks (NCCL exchanges inside the
-    # library, strong scaling); cfg2 runs independent replicas (weak scaling)
-    sharded = world > 1 and d == 3 and not args.replicas
+    peak, peak_kind = peaks()
+    spec = GridSpec((1.0,) * wl.d, wl.shape)
     if sharded:
         from paper_1311_0089_b200 import parallel
 
         ctx = parallel.distributed_context(spec, device=local)
     else:
         ctx = _native.Context(spec, local)
-    wl.setup(ctx, host)
+    count_fn = None
+    if sharded and wl.name == "cfg5":
+        import torch
+        import torch.distributed as dist
 
-    def solve_resident():
-        reps, _, _ = ctx.solve_cg(loads, TOL, MAX_ITER, want_x=False)
-        return reps
+        def count_fn(v):
+            t = torch.tensor([v], dtype=torch.int64)
+            dist.all_reduce(t)
+            return int(t.item())
+    host = wl.host_field()
+    gen_out = wl.setup(ctx, host, count_fn=count_fn, want_labels=(wl.name == "cfg4" and not sharded))
 
-    for _ in range(args.warmup):
-        reps = solve_resident()
-    iters = [r["iterations"] for r in reps]
-    work_per_step = N * sum(iters)
-
-    # ---- timed: resident inputs (value) --------------------------------------
-    # K steps bracketed by stream events, no per-kernel events inside (those
-    # cost ~3 % of the step); the per-kernel breakdown comes from a second
-    # region of the same K steps with an event pair around every launch.
-    launches0 = ctx.launch_count()
-    barrier(world)
     with ClockSampler(local) as clk:
-        ctx.timer_mark(0)
-        for _ in range(args.steps):
-            reps = solve_resident()
-        ctx.timer_mark(1)
-        ms = ctx.timer_elapsed(0, 1)
-    launches = ctx.launch_count() - launches0
-    assert [r["iterations"] for r in reps] == iters
-    ctx.profile_reset()
-    ctx.set_profiling(True)
-    barrier(world)
-    ctx.timer_mark(4)
-    for _ in range(args.steps):
-        reps = solve_resident()
-    ctx.timer_mark(5)
-    ms_prof = ctx.timer_elapsed(4, 5)
-    ctx.set_profiling(False)
-    prof = ctx.profile()
-    ms_max = max_over_ranks(world, ms)
-    copies = 1 if sharded else world
-    value = copies * work_per_step * args.steps / (ms_max / 1000.0)
+        res = measure(wl, ctx, args, world, args.steps)
+    value, roof, per_kernel, operator, iteration = summarize(wl, res, args.steps, world, sharded, peak, peak_kind)
 
-    # ---- e2e: host buffers through the public API -----------------------------
+    # ---- e2e: host buffers through the C-ABI binding ----------------------------
     import torch
+    from types import SimpleNamespace
 
+    R, d = wl.R, wl.d
     x_out = torch.empty((R, d) + wl.shape, dtype=torch.float64, pin_memory=True).numpy()
-    a_pinned = None
+    field = None
     if host is not None:
-        pin_a = torch.empty(host.components.shape, dtype=torch.float64, pin_memory=True).numpy()
-        pin_a[...] = host.components
-        a_pinned = CoefficientField(host.spec, pin_a)
-    h2d = wl.setup(ctx, a_pinned) + loads.nbytes
-    ctx.solve_cg(loads, TOL, MAX_ITER, out=x_out)
-    d2h = x_out.nbytes
-    e2e_steps = max(1, args.steps if wl.name != "cfg4" else 1)
-    barrier(world)
-    ctx.timer_mark(2)
-    for _ in range(e2e_steps):
-        wl.setup(ctx, a_pinned)
-        ctx.solve_cg(loads, TOL, MAX_ITER, out=x_out)
-    ctx.timer_mark(3)
-    ms_e2e = max_over_ranks(world, ctx.timer_elapsed(2, 3))
-    e2e = copies * work_per_step * e2e_steps / (ms_e2e / 1000.0)
+        pin = torch.empty(host.components.shape, dtype=torch.float64, pin_memory=True).numpy()
+        pin[...] = host.components
+        field = SimpleNamespace(isotropic_values=pin[0] if host.isotropic_values is not None else None,
+                                components=pin)
+    elif wl.name == "cfg4" and gen_out is not None:
+        labels, grains = gen_out
+        pin = torch.empty((6,) + wl.shape, dtype=torch.float64, pin_memory=True).numpy()
+        for m in range(6):
+            np.take(grains[:, m], labels, out=pin[m])
+        del labels
+        field = SimpleNamespace(isotropic_values=None, components=pin)
+    e2e = None
+    if field is not None:
+        e2e_steps = min(args.steps, args.e2e_steps)
+        h2d = field.components.nbytes if field.isotropic_values is None else field.isotropic_values.nbytes
+        h2d += wl.loads.nbytes
+        ctx.set_coefficients(field)
+        ctx.solve_cg(wl.loads, TOL, MAX_ITER, out=x_out)
+        barrier(world)
+        ctx.timer_mark(2)
+        for _ in range(e2e_steps):
+            ctx.set_coefficients(field)
+            ctx.solve_cg(wl.loads, TOL, MAX_ITER, out=x_out)
+        ctx.timer_mark(3)
+        ms_e2e = max_over_ranks(world, ctx.timer_elapsed(2, 3))
+        copies = 1 if sharded else world
+        e2e = {"value": copies * wl.N * sum(res["iters"]) * e2e_steps / (ms_e2e / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(x_out.nbytes), "steps": e2e_steps,
+               "path": "Context.set_coefficients (pinned host field) + Context.solve_cg(out=pinned host array)"}
+        del field, pin
+    del x_out
 
-    if rank != 0:
-        return
-    peak, peak_kind = peaks()
-    # sharded: rank 0's kernels process its slab only (planes [0, n0/P))
-    local = (wl.shape[0] // world) / wl.shape[0] if sharded else 1.0
-    kbytes = wl.kernel_bytes
-    wl.kernel_bytes = lambda k: None if kbytes(k) is None else kbytes(k) * local
-    kern = {k: v for k, v in prof.items() if wl.kernel_bytes(k) is not None}
-    top = max(kern, key=lambda k: kern[k][1])
-    avg_ms = kern[top][1] / kern[top][0]
-    bytes_launch = wl.kernel_bytes(top)
-    achieved = bytes_launch / (avg_ms / 1000.0) / 1e9
-    traffic = None
-    tp = ROOT / "profiles" / "ncu_traffic.json"
-    if tp.exists():
-        traffic = json.loads(tp.read_text()).get(f"{wl.name}/{top}")
-    step_ms = ms / args.steps
-    n_iter = max(iters)
-    roofline = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
-                "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_ms,
-                "share_of_step": kern[top][1] / ms_prof,
-                "timing": "CUDA events around every launch on the library stream, over a second region of the "
-                          "same K steps (the value region carries no per-kernel events)",
-                "profiled_ms_per_step": ms_prof / args.steps}
-    per_kernel = {}
-    for k, v in prof.items():
-        avg = v[1] / max(v[0], 1)
-        kb = wl.kernel_bytes(k)
-        per_kernel[k] = {"launches": v[0], "avg_ms": avg, "GBps": kb / (avg / 1000) / 1e9 if kb else None}
-    ib = wl.iter_bytes() * local  # per GPU
-    iteration = {"bytes": ib, "ms": step_ms / n_iter, "GBps": ib / (step_ms / n_iter / 1000) / 1e9}
-    iteration["frac"] = iteration["GBps"] / peak
     exchange = None
+    prof = res["prof"]
     if "exchange" in prof:  # spectrum transposes between ranks (SURVEY 8(e)), broken out
         from paper_1311_0089_b200 import parallel
 
         cnt, tot = prof["exchange"]
         sent = 16 * sum(int(v) for p, v in enumerate(parallel.exchange_counts(wl.shape, R, world)[rank]) if p != rank)
         exchange = {"per_exchange_ms": tot / cnt, "exchanges_per_iteration": 2,
-                    "share_of_step": tot / ms_prof, "bytes_sent_per_gpu": sent,
+                    "share_of_step": tot / res["ms_prof"], "bytes_sent_per_gpu": sent,
                     "GBps_per_gpu": sent / (tot / cnt / 1000) / 1e9,
                     "transport": "NCCL send/recv over NVLink (one process per GPU)"}
-    op_names = [k for k in ("pointwise", "row_fwd", "mid_fwd", "outer", "mid_inv", "row_inv") if k in prof]
-    op_ms = sum(per_kernel[k]["avg_ms"] for k in op_names)
-    op_bytes = sum(wl.kernel_bytes(k) for k in op_names)
-    operator = {"kernels": op_names, "ms": op_ms, "GBps": op_bytes / (op_ms / 1000) / 1e9}
-    operator["frac"] = operator["GBps"] / peak
+    del ctx
 
-    cpu = None
-    if world == 1 and not args.no_cpu:
-        work, t, its, n = cpu_sample(wl, args.cpu_seconds)
-        cpu = {"value": work / t, "unit": UNIT, "cores": R, "kind": "port",
-               "sample": f"first CG iterations of each of the {R} load case(s) of {wl.name} at {n}^{d}, "
-                         f"{args.cpu_seconds:g} s each, one process per load case; iterations {its}"}
+    # ---- the other single-GPU BASELINE configurations (same run, value only) ------
+    others = {}
+    if world == 1 and not args.no_others and args.config == "cfg4":
+        from paper_1311_0089_b200.material import CoefficientField  # noqa: F401
+
+        for name in ("cfg2", "cfg3", "cfg3fp"):
+            ow = Workload(name)
+            octx = _native.Context(GridSpec((1.0,) * ow.d, ow.shape), local)
+            ow.setup(octx, ow.host_field())
+            ores = measure(ow, octx, args, world, args.steps, fp_ref=25.5 * np.eye(3))
+            ov, oroof, okern, oop, oit = summarize(ow, ores, args.steps, 1, False, peak, peak_kind)
+            others[name] = {"config": config_dict(ow, "single"), "value": ov, "unit": UNIT,
+                            "ms_per_step": ores["ms"] / args.steps, "iterations": ores["iters"],
+                            "roofline": oroof, "iteration_roofline": oit, "operator_roofline": oop,
+                            "kernels": okern}
+            del octx
+
+    if rank != 0:
+        return
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": res["ms"] / args.steps, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(wl, f"slab{world}" if sharded else ("replicas" if world > 1 else "single")),
-        "iterations": iters,
-        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-        "gpu_launches": launches,
-        "roofline": roofline,
+        "config": config_dict(wl, label),
+        "iterations": res["iters"],
+        "e2e": e2e,
+        "gpu_launches": res["launches"],
+        "roofline": roof,
         "iteration_roofline": iteration,
         "operator_roofline": operator,
         "kernels": per_kernel,
         "exchange": exchange,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
+        "other_configs": others or None,
     }
     print(json.dumps(line), flush=True)
 
@@ -447,13 +663,18 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4"],
-                    help="BASELINE configuration (default cfg2 = configs[1], the metric's workload)")
+    ap.add_argument("--config", default="cfg4", choices=["cfg2", "cfg3", "cfg3fp", "cfg4", "cfg5"],
+                    help="BASELINE configuration (default cfg4 = configs[3], the largest single-GPU one)")
     ap.add_argument("--n", type=int, default=0, help="override the grid size (0 = BASELINE size)")
-    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-others", action="store_true", help="skip the other single-GPU configurations")
+    ap.add_argument("--profile-steps", type=int, default=3, help="steps of the per-kernel profiled region")
+    ap.add_argument("--e2e-steps", type=int, default=5, help="steps of the e2e region (<= --steps)")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas even for 3-D configs")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
     if args.impl == "reference":
         run_reference(args)
     else:
