@@ -65,6 +65,24 @@ int32_t fc_version(void);
 const char* fc_last_error(void);
 int32_t fc_device_count(int32_t* count);
 
+/* Plan options (no reference equivalent: kernel selection of this library).
+ * Process-wide defaults copied into every context at creation, where the
+ * kernels and tile geometry are chosen; existing contexts are unaffected.
+ * Defaults are the measured-fastest choices; the alternatives perform the same
+ * arithmetic and exist for bitwise variant tests and A/B measurements.  Keys:
+ *   force_generic (0)  generic shared-memory FFT on every axis
+ *   row_threads (256), mid_threads (0 = auto), outer_threads (0 = auto)  CTA sizes
+ *   row_tma / mid_tma / outer_tma (1)  TMA data movement in the sweeps
+ *   outer_seq (-1 = auto)  d = 3 outer sweep one component at a time
+ *   inv_pipe (-1 = auto)  persistent double-buffered last sweep
+ *   aniso_fused (1)  packed coefficients: fused first sweep (0: pointwise kernel + row FFT)
+ *   defer_x (1)  CG x update deferred into the next first sweep
+ *   fused_exchange (1)  in-process slabs store straight into the peers' buffers
+ *   sync_debug (0)  synchronize after every launch
+ * Unknown keys return FC_EINVAL. */
+int32_t fc_set_plan_option(const char* key, int32_t value);
+int32_t fc_reset_plan_options(void);
+
 /* GridSpec + device binding (grid.py:30-83): odd positive shape, Y > 0. */
 int32_t fc_create(fc_ctx** out, int32_t dim, const int64_t* shape, const double* half_periods,
                   int32_t device);
@@ -75,7 +93,7 @@ void fc_destroy(fc_ctx* ctx);
  * emulate ranks).  Every entry point below accepts it transparently: host
  * arrays keep the full-grid layout, the library scatters / gathers slabs and
  * runs two axis-0 exchanges (peer copies over NVLink) per operator
- * application.  d = 3 with power-of-three axes (9 .. 2187). */
+ * application.  d = 3, any odd axis lengths (register FFT for 3^k and 5 3^k, shared-memory FFT otherwise). */
 int32_t fc_create_sharded(fc_ctx** out, int32_t dim, const int64_t* shape, const double* half_periods,
                           int32_t nslabs, const int32_t* devices);
 

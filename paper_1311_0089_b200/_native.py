@@ -40,6 +40,8 @@ SIGNATURES = [
     ("fc_version", ctypes.c_int32, []),
     ("fc_last_error", ctypes.c_char_p, []),
     ("fc_device_count", ctypes.c_int32, [ctypes.POINTER(ctypes.c_int32)]),
+    ("fc_set_plan_option", ctypes.c_int32, [ctypes.c_char_p, ctypes.c_int32]),
+    ("fc_reset_plan_options", ctypes.c_int32, []),
     ("fc_create", ctypes.c_int32,
      [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, _i64p, _dp, ctypes.c_int32]),
     ("fc_create_sharded", ctypes.c_int32,
@@ -119,6 +121,23 @@ def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().fc_nccl_unique_id(buf))
     return buf.raw
+
+
+class plan_options:
+    """Context manager: plan options (fc_set_plan_option) for the contexts created
+    inside the block, e.g. ``with plan_options(aniso_fused=0): Context(spec)``.
+    Options are frozen into a context at creation; the defaults are restored on exit."""
+
+    def __init__(self, **opts):
+        self.opts = opts
+
+    def __enter__(self):
+        for k, v in self.opts.items():
+            _check(lib().fc_set_plan_option(k.encode(), int(v)))
+        return self
+
+    def __exit__(self, *exc):
+        _check(lib().fc_reset_plan_options())
 
 
 def device_count():

@@ -25,6 +25,7 @@
 #include "fc_kernels.cuh"
 #include "fc_kernels_reg.cuh"
 #include "fc_kernels_pipe.cuh"
+#include "fc_kernels_pk.cuh"
 
 // Field allocations carry this many spare bytes: 16-byte-aligned bulk copies
 // (fc_tma.cuh) of a row block may read up to 8 bytes past its last element.
@@ -68,8 +69,6 @@ struct DevPlan {
 
 // register-path lengths (fc_fft_reg.cuh): 3^k for 9..2187 and 5 * 3^k for 45..1215
 bool is_pow3_reg(int L) { return fc::is_reg_len(L); }
-// lengths the measured-and-off kernel variants are compiled for (FC_EXP_SWITCH)
-bool exp_len(int L) { return L == 243 || L == 729 || L == 2187; }
 
 // Twiddle table of fc_fft_reg.cuh for L = 3^k: for radix-9 pass S >= 1 (Ns = 9^S)
 // tw[off9(S) + (r-1) Ns + k] = w_L^{k r L/(9 Ns)}, r = 1..8, k < Ns; tail block
@@ -126,6 +125,27 @@ struct Prof {
   double ms = 0.0;
 };
 
+// Plan options: kernel selection and tile geometry, frozen when a context is
+// created (copied from the process-wide table set through fc_set_plan_option).
+// The defaults are the measured-fastest choices; the alternatives exist for the
+// bitwise variant tests (tests/test_gpu_variants.py) and A/B measurements.
+struct PlanOpts {
+  int force_generic = 0;   // generic shared-memory Stockham FFT on every axis
+  int row_threads = 256;   // first / last sweep CTA size (pencils of the row block)
+  int mid_threads = 0;     // middle sweep CTA size (0: 256 for pencils <= 243, else 512)
+  int outer_threads = 0;   // outer sweep CTA size (0: 2 pencils for short 3-D pencils, else 256)
+  int row_tma = 1;         // TMA tensor boxes for the transposed half spectrum
+  int mid_tma = 1;         // TMA inverse middle sweep
+  int outer_tma = 1;       // bulk pencil copies in the outer sweep
+  int outer_seq = -1;      // d = 3 outer sweep one component at a time (-1: for pencils >= 243)
+  int inv_pipe = -1;       // persistent double-buffered last sweep (-1: for one-pencil row blocks)
+  int aniso_fused = 1;     // packed coefficients: fused first sweep (0: pointwise kernel + row FFT)
+  int defer_x = 1;         // CG x update deferred into the next first sweep
+  int fused_exchange = 1;  // in-process slabs: sweeps store straight into the peers' buffers
+  int sync_debug = 0;      // synchronize after every launch (error attribution)
+};
+PlanOpts g_plan_opts;
+
 }  // namespace
 
 struct fc_ctx {
@@ -137,7 +157,8 @@ struct fc_ctx {
   cudaStream_t stream = nullptr;
   int smem_optin = 0;
   int num_sms = 0;
-  bool force_generic = false;  // FC_FORCE_GENERIC=1: generic smem FFT for every axis
+  PlanOpts opt;                // plan options (fixed at creation)
+  bool force_generic = false;  // opt.force_generic: generic smem FFT for every axis
 
   std::map<int, DevPlan> plans;  // by length
   double* xi = nullptr;          // concatenated per-axis frequency tables
@@ -178,6 +199,7 @@ struct fc_ctx {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   std::vector<cudaEvent_t> ev_pool;
   int64_t launches = 0;
+  const char* prof_tag = "";  // appended to profile names ("_rhs": right-hand-side / warm-start operators)
 
   Geo geo() const {
     Geo g{};
@@ -192,22 +214,16 @@ struct fc_ctx {
   const FftPlan& plan(int L) const { return plans.at(L).plan; }
   const double2* rtw(int L) const { return plans.at(L).rtw; }
   // register-path tiling per sweep (0 = generic path)
-  int row_npen = 0, mid_bp = 0, outer_qb = 0, inv_prefetch = 1;
-  int aniso_npen = 0;       // all-components first sweep for packed coefficients (0 = off)
-  int aniso_split = 1;      // packed coefficients: pointwise kernel + staged row FFT
-  int outer_persist = 0;    // persistent double-buffered outer sweep (FC_OUTER_PERSIST)
-  int outer_c1 = 0;         // one-component-per-thread outer sweep: pencil groups per CTA (0 = off)
-  int row_pipe = 0;         // persistent double-buffered first sweep (FC_ROW_PIPE)
-  int outer_seq = 0;        // outer sweep one component at a time (FC_OUTER_SEQ)
+  int row_npen = 0, mid_bp = 0, outer_qb = 0;
+  int pk_npen = 0;          // fused packed-coefficient first sweep: pencils per component (0: split)
+  size_t smem_pk = 0;
+  int outer_seq = 0;        // d = 3 outer sweep one component at a time
   CUtensorMap tmW{};        // TMA view of the row-sweep spectrum (RowGeo::tma)
+  CUtensorMap tmP{};        // the same for the fused packed first sweep's row blocks (2 pk_npen rows)
   CUtensorMap tmM{};        // TMA view of the middle sweep's transposed side (MidGeo::tma)
-  int row_pipe_blocks = 0;  // its resident CTAs per SM
-  size_t smem_row_pp = 0;
-  int inv_pipe_blocks = 0;  // persistent double-buffered last sweep (FC_INV_PIPE): CTAs per SM
+  int inv_pipe_blocks = 0;  // persistent double-buffered last sweep: CTAs per SM (0: off)
   int inv_pipe_stage = 0;   // its stage size (complex)
-  int inv_pipe_nst = 2;     // its number of stages (FC_INV_STAGES, 2..4)
-  int inv_pipe_qbuf = 1;    // bulk-load the epilogue input per block (FC_INV_QBUF)
-  size_t smem_aniso_r = 0;
+  static constexpr int inv_pipe_nst = 2;   // its stages
   size_t smem_row_r = 0, smem_row_inv_r = 0, smem_mid_r = 0, smem_outer_r = 0;
 
   // slab decomposition along axis 0.  A plain context is the P = 1
@@ -324,19 +340,19 @@ int launch(fc_ctx* c, const char* name, F&& f) {
   c->launches++;
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_err(FC_ECUDA, "launch of %s failed: %s", name, cudaGetErrorString(err));
-  static const bool sync_debug = getenv("FC_SYNC_DEBUG") != nullptr;
-  if (sync_debug) {
+  if (c->opt.sync_debug) {
     err = cudaStreamSynchronize(c->stream);
     if (err != cudaSuccess) return set_err(FC_ECUDA, "kernel %s failed: %s", name, cudaGetErrorString(err));
   }
   if (c->prof_on) {
     cudaEventRecord(e1, c->stream);
-    auto it = c->prof_idx.find(name);
+    const std::string key = std::string(name) + c->prof_tag;
+    auto it = c->prof_idx.find(key);
     int idx;
     if (it == c->prof_idx.end()) {
       idx = (int)c->prof.size();
-      c->prof_idx[name] = idx;
-      c->prof.push_back(Prof{name, 0, 0.0});
+      c->prof_idx[key] = idx;
+      c->prof.push_back(Prof{key, 0, 0.0});
     } else {
       idx = it->second;
     }
@@ -344,6 +360,15 @@ int launch(fc_ctx* c, const char* name, F&& f) {
   }
   return FC_OK;
 }
+
+// Profile names of the launches enqueued while alive get `tag` appended (bench.py
+// charges the right-hand-side / warm-start operators their own byte counts).
+struct ProfTag {
+  fc_ctx* c;
+  const char* saved;
+  ProfTag(fc_ctx* c_, const char* tag) : c(c_), saved(c_->prof_tag) { c->prof_tag = tag; }
+  ~ProfTag() { c->prof_tag = saved; }
+};
 
 // Accumulate finished profiling intervals (call after a stream sync).
 void drain_profile(fc_ctx* c) {
@@ -453,56 +478,41 @@ int choose_tiles(fc_ctx* c) {
     c->smem_outer = (size_t)32 * d * best * og.n0;
   }
   // register-resident path for power-of-three axes (fc_kernels_reg.cuh)
-  auto env_int = [](const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v ? atoi(v) : dflt;
-  };
+  const PlanOpts& op = c->opt;
   if (c->force_generic) return FC_OK;
   if (is_pow3_reg(rg.nl)) {
     const int TP = rg.nl / 9;
-    int npen = std::max(1, std::min(16, std::min(env_int("FC_ROW_THREADS", 256), 256) / TP));
+    int npen = std::max(1, std::min(16, std::min(op.row_threads, 256) / TP));
     npen = std::min(npen, (rg.np + 1) / 2);
     rg.B = 2 * npen;
     rg.ntiles = (rg.np + rg.B - 1) / rg.B;
     c->row_npen = npen;
     // exchange buffer (16 npen (L+1)) + staging: first sweep u, p_old, A (3 x 2 npen L
-    // doubles), last sweep p / e (2 npen L doubles)
+    // doubles)
     c->smem_row_r = (size_t)24 * (((size_t)2 * npen * rg.nl + 3) & ~(size_t)1);
-    c->inv_prefetch = env_int("FC_INV_PREFETCH", 0);
-    c->row_pipe = env_int("FC_ROW_PIPE", 0) && exp_len(rg.nl);
     // TMA boxes of the transposed spectrum: nbox boxes of boxK modes x 2 npen rows
     rg.nbox = (rg.hl + 255) / 256;
     rg.boxK = ((rg.hl + rg.nbox - 1) / rg.nbox + 3) & ~3;  // boxes start 128-byte aligned in smem
-    // persistent first sweep: stage U, P (2 x stride doubles, 128-byte rounded) +
-    // spectrum buffer (L complex for the FFT, nbox boxK 2 complex for the split)
-    c->smem_row_pp = (size_t)8 * ((2 * ((2 * rg.nl + 3) & ~1) + 15) & ~15) +
-                     (size_t)16 * std::max(rg.nl, rg.nbox * rg.boxK * 2);
     const size_t ybytes = (size_t)16 * rg.nbox * rg.boxK * 2 * npen;
     c->smem_row_r = std::max(c->smem_row_r, (size_t)16 * (((size_t)npen * rg.nl + 7) & ~(size_t)7) + ybytes);
-    c->smem_row_inv_r = std::max((size_t)16 * npen * (rg.nl + 1), ybytes) +
-                        (c->inv_prefetch ? (size_t)16 * npen * rg.nl + 16 : 0);
-    c->aniso_split = env_int("FC_ANISO_SPLIT", 1);
-    rg.exp_natural = env_int("FC_EXP_NATURAL_STORE", 0);
-    // packed coefficients: one CTA per row block for all components (its own
-    // row-block size: the c inputs, c old directions and nsym tensor entries of
-    // 2 npen rows are staged in shared memory)
-    {
-      const size_t arrays = (size_t)(2 * d + d * (d + 1) / 2);
-      const size_t per_pen = arrays * 2 * rg.nl * 8;
-      const size_t cap = (size_t)env_int("FC_ANISO_SMEM_KB", 160) * 1024;
-      int na = (int)std::min<size_t>(cap / per_pen, (size_t)(kMaxBlock / (d * (rg.nl / 9))));
-      na = std::min(na, (rg.np + 1) / 2);
-      if (env_int("FC_ANISO_ROWS", 1) && na >= 1 && exp_len(rg.nl)) {
-        c->aniso_npen = na;
-        c->smem_aniso_r = std::max(per_pen * na, (size_t)16 * d * na * rg.nl);
+    c->smem_row_inv_r = std::max((size_t)16 * npen * (rg.nl + 1), ybytes);
+    // packed coefficients: fused first sweep (fc_kernels_pk.cuh), d components of
+    // npk pencils per CTA (<= 256 threads), if two CTAs fit an SM
+    if (op.aniso_fused && d >= 2) {
+      const int npk = std::max(1, std::min((rg.np + 1) / 2, 256 / (d * TP)));
+      const size_t sm = pk_smem(rg.nl, d, npk, rg.nbox, rg.boxK);
+      if (d * TP <= 256 && 2 * (sm + 1024) <= (size_t)c->smem_optin + 1024 && sm <= 110 * 1024) {
+        c->pk_npen = npk;
+        c->smem_pk = sm;
       }
     }
-    }
+  }
   if (d == 3 && is_pow3_reg(c->n[1])) {
     MidGeo& mg = c->mg;
     const int TP = c->n[1] / 9;
     // 256 threads for 243-point pencils (cfg3: mid_inv -8 %), 512 for longer ones (cfg4: 256 is slower)
-    int bp = std::max(1, std::min(16, std::min(env_int("FC_MID_THREADS", TP <= 27 ? 256 : 512), kMaxBlock) / TP));
+    const int mt = op.mid_threads > 0 ? op.mid_threads : (TP <= 27 ? 256 : 512);
+    int bp = std::max(1, std::min(16, std::min(mt, kMaxBlock) / TP));
     bp = std::min(bp, c->n[0]);
     mg.B = bp;
     mg.nib = (mg.n0 + bp - 1) / bp;
@@ -521,28 +531,17 @@ int choose_tiles(fc_ctx* c) {
     const int TP = c->n0g / 9;
     // d = 3 holds 3 x 9 complex per thread: short pencils (TP <= 32) run best
     // as small CTAs (measured at 243^3: 2 pencils, 54 threads, -22 %)
-    const int outer_dflt = (d == 3 && TP <= 32) ? 2 * TP : 256;
-    int qb = std::max(1, std::min(32, std::min(env_int("FC_OUTER_THREADS", outer_dflt), kMaxBlockOuter) / TP));
+    const int ot = op.outer_threads > 0 ? op.outer_threads : ((d == 3 && TP <= 32) ? 2 * TP : 256);
+    int qb = std::max(1, std::min(32, std::min(ot, kMaxBlockOuter) / TP));
     qb = std::min(qb, og.Q);
     og.QB = qb;
     og.nqb = (og.Q + qb - 1) / qb;
     c->outer_qb = qb;
     c->smem_outer_r = (size_t)16 * d * qb * c->n0g;
-    og.tma = env_int("FC_OUTER_TMA", 1);
+    og.tma = op.outer_tma;
     // d = 3 with long pencils: one component at a time (measured at 729^3: -19 %;
     // slower for the small 243-length CTAs and for d = 2)
-    c->outer_seq = env_int("FC_OUTER_SEQ", d == 3 && TP >= 27) && (d == 3 || exp_len(c->n0g));
-    c->outer_persist = env_int("FC_OUTER_PERSIST", 0) && exp_len(c->n0g) &&
-                       2 * c->smem_outer_r <= (size_t)c->smem_optin - 2048;
-    {
-      // one component per thread: d * QB * TP threads (<= 512)
-      const int want = env_int(d == 3 ? "FC_OUTER_C1_3D" : "FC_OUTER_C1_2D", 0) && exp_len(c->n0g);
-      if (want) {
-        int qb1 = std::max(1, std::min(og.Q, 512 / (d * TP)));
-        while (qb1 > 1 && (size_t)16 * d * qb1 * c->n0g > (size_t)c->smem_optin - 2048) --qb1;
-        if (d * TP <= 512 && (size_t)16 * d * qb1 * c->n0g <= (size_t)c->smem_optin - 2048) c->outer_c1 = qb1;
-      }
-    }
+    c->outer_seq = d == 3 && (op.outer_seq >= 0 ? op.outer_seq : TP >= 27);
   }
   return FC_OK;
 }
@@ -563,42 +562,13 @@ int choose_tiles(fc_ctx* c) {
     default: break;                      \
   }
 
-// Measured-and-off kernel variants (FC_ROW_PIPE, FC_OUTER_PERSIST, FC_OUTER_C1_*,
-// FC_ANISO_SPLIT=0, FC_OUTER_SEQ for d = 2) are compiled for the BASELINE lengths
-// only (build time); the host enables them only for these lengths.
-#define FC_EXP_SWITCH(L, BODY)                            \
-  switch (L) {                                            \
-    case 243: { constexpr int LL = 243; BODY; } break;   \
-    case 729: { constexpr int LL = 729; BODY; } break;   \
-    case 2187: { constexpr int LL = 2187; BODY; } break; \
-    default: break;                                       \
-  }
-
-
-int env_int_g(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
-
-bool env_flag(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return (v ? atoi(v) : dflt) != 0;
-}
-
 int allow_reg_smem(int mx) {
   int rc = FC_OK;
   auto al = [&](auto k) { if (rc == FC_OK) rc = allow_smem(k, mx); };
   for (int L : {9, 27, 81, 243, 729, 2187, 45, 135, 405, 1215}) {
-    FC_EXP_SWITCH(L, {
-      al(k_row_fwd_pp<LL>);
-      al(k_row_fwd_aniso_r<LL>);
-      al(k_outer_p<LL, 2>);
-      al(k_outer_p<LL, 3>);
-      al(k_outer_c1<LL, 2>);
-      al(k_outer_c1<LL, 3>);
-      al(k_outer_seq<LL, 2>);
-    });
     FC_POW3_SWITCH(L, {
+      al(k_row_fwd_pk<LL, 2>);
+      al(k_row_fwd_pk<LL, 3>);
       al(k_row_fwd_r<LL>);
       al(k_row_inv_r<LL>);
       al(k_mid_r<LL, false>);
@@ -619,8 +589,10 @@ int allow_reg_smem(int mx) {
 int make_row_tmap(fc_ctx* c) {
   RowGeo& rg = c->rg;
   rg.tma = 0;
-  const char* env = getenv("FC_ROW_TMA");
-  if (c->dim < 2 || !c->row_npen || rg.nbox == 0 || (env && atoi(env) == 0)) return FC_OK;
+  if (c->dim < 2 || !c->row_npen || rg.nbox == 0 || !c->opt.row_tma) {
+    c->pk_npen = 0;  // the fused packed first sweep stores through its tensor map
+    return FC_OK;
+  }
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (encode == nullptr) {
     cudaDriverEntryPointQueryResult q;
@@ -639,11 +611,17 @@ int make_row_tmap(fc_ctx* c) {
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rc != CUDA_SUCCESS) return set_err(FC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)rc);
   rg.tma = 1;
+  if (c->pk_npen) {  // same view, boxes of the fused packed first sweep's 2 pk_npen rows
+    cuuint32_t boxp[3] = {(cuuint32_t)(4 * c->pk_npen), (cuuint32_t)rg.boxK, 1};
+    const CUresult rp = encode(&c->tmP, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxp, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rp != CUDA_SUCCESS) return set_err(FC_ECUDA, "cuTensorMapEncodeTiled (packed first sweep) failed (%d)", (int)rp);
+  }
   // middle sweep (d = 3, one slab): W2[rc][k2][k1][i0] as doubles {2 n0, n1, R c h2}
   MidGeo& mg = c->mg;
   mg.tma = 0;
-  const char* envm = getenv("FC_MID_TMA");
-  if (c->dim == 3 && c->mid_bp && c->P == 1 && mg.nbox > 0 && !(envm && atoi(envm) == 0)) {
+  if (c->dim == 3 && c->mid_bp && c->P == 1 && mg.nbox > 0 && c->opt.mid_tma) {
     cuuint64_t md[3] = {(cuuint64_t)2 * mg.n0, (cuuint64_t)mg.n1, (cuuint64_t)c->Rcap * c->dim * mg.h2};
     cuuint64_t ms[2] = {(cuuint64_t)16 * mg.n0, (cuuint64_t)16 * mg.n0 * mg.n1};
     cuuint32_t mb[3] = {(cuuint32_t)(2 * mg.B), (cuuint32_t)mg.rows, 1};
@@ -712,37 +690,6 @@ int ensure_workspace(fc_ctx* c, int R, int hcap) {
 int64_t nslot_row(const fc_ctx* c) { return c->dim == 1 ? 1 : (int64_t)c->rg.no * c->rg.ntiles * c->dim; }
 int64_t nslot_vec(const fc_ctx* c) { return ((int64_t)c->dim * c->N + kVecTile - 1) / kVecTile; }
 
-// Persistent double-buffered first sweep (fc_kernels_pipe.cuh): only for
-// inputs that every tile stages (isotropic coefficients or raw fields; a
-// fixed-point reference without off-diagonal entries), as in k_row_fwd_r.
-bool row_pipe_ok(const fc_ctx* c, const InArgs& ia) {
-  if (c->row_pipe_blocks <= 0 || !c->rg.tma || c->row_npen != 1) return false;
-  if (ia.mode == IN_RAW) return true;
-  if (c->coef_kind != 0 || ia.mode == IN_CONST) return false;
-  if (ia.mode == IN_FP)
-    for (int a = 0; a < c->dim; ++a)
-      for (int b = 0; b < c->dim; ++b)
-        if (a != b && ia.A0[a][b] != 0.0) return false;
-  return true;
-}
-
-int launch_row_fwd_pp(fc_ctx* c, int R, const InArgs& ia, const RhsState* st, double2* Wrow) {
-  const Geo g = c->geo();
-  const Coef C = c->coef();
-  RowGeo rp = c->rg;
-  rp.B = 2;
-  rp.ntiles = (rp.np + 1) / 2;
-  const int64_t ntile = (int64_t)R * rp.no * rp.ntiles * c->dim;
-  const unsigned grid = (unsigned)std::min<int64_t>(ntile, (int64_t)c->num_sms * c->row_pipe_blocks);
-  const int nt = rp.nl / 9;
-  const double2* tw = c->rtw(rp.nl);
-  const size_t smem = c->smem_row_pp;
-  cudaStream_t s = c->stream;
-  return launch(c, "row_fwd", [&] {
-    FC_EXP_SWITCH(rp.nl, (k_row_fwd_pp<LL><<<grid, nt, smem, s>>>(g, rp, C, ia, st, tw, ntile, c->tmW)));
-  });
-}
-
 // One operator application over R fields, in three phases so a sharded run can
 // exchange spectra between them: 0 = first sweep (+ forward middle sweep),
 // 1 = outer sweep (Gamma_hat), 2 = inverse middle sweep + last sweep.
@@ -786,99 +733,71 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     });
   };
   if (phases & PH_FWD) {
-  if (C.kind == 1 && c->aniso_split && c->row_npen && ia.mode != IN_RAW) {
-    // split variant: pointwise y = M(x) u (+ p') at streaming bandwidth, then the
-    // staged row FFT on y.  y lives in the Ap buffer (free until the last sweep).
-    double* y = c->Ap;
-    const int blocks = c->num_sms * 8;
-    TRY(launch(c, "pointwise", [&] { k_pointwise_aniso<<<blocks, 256, 0, s>>>(g, C, ia, st, R, y); }));
-    InArgs raw{};
-    raw.mode = IN_RAW;
-    raw.s = 1.0;
-    raw.u = y;
-    const int nt = c->row_npen * (rg.nl / 9);
-    const double2* tw = c->rtw(rg.nl);
-    if (c->row_pipe && row_pipe_ok(c, raw)) {
-      TRY(launch_row_fwd_pp(c, R, raw, st, Wrow));
-    } else {
+    const double2* twr = c->row_npen ? c->rtw(rg.nl) : nullptr;
+    if (C.kind == 1 && c->pk_npen && ia.mode != IN_RAW) {
+      // packed coefficients, fused: y = M(x) u in shared memory, row FFT of all d
+      // components in the same CTA (fc_kernels_pk.cuh)
+      const int npk = c->pk_npen;
+      const int64_t nb = (int64_t)R * rg.no * ((rg.np + 2 * npk - 1) / (2 * npk));
+      const int nt = d * npk * (rg.nl / 9);
       TRY(launch(c, "row_fwd", [&] {
-        FC_POW3_SWITCH(rg.nl, (k_row_fwd_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, C, raw, st, tw, Wrow, c->tmW)));
+        if (d == 2) FC_POW3_SWITCH(rg.nl, (k_row_fwd_pk<LL, 2><<<(unsigned)nb, nt, c->smem_pk, s>>>(g, rg, C, ia, st, twr, npk, c->tmP)))
+        else FC_POW3_SWITCH(rg.nl, (k_row_fwd_pk<LL, 3><<<(unsigned)nb, nt, c->smem_pk, s>>>(g, rg, C, ia, st, twr, npk, c->tmP)))
+      }));
+    } else if (C.kind == 1 && c->row_npen && ia.mode != IN_RAW) {
+      // packed coefficients, split: pointwise y = M(x) u (+ p') at streaming
+      // bandwidth, then the staged row FFT on y.  y lives in the Ap buffer (free
+      // until the last sweep).
+      double* y = c->Ap;
+      const int blocks = c->num_sms * 8;
+      TRY(launch(c, "pointwise", [&] { k_pointwise_aniso<<<blocks, 256, 0, s>>>(g, C, ia, st, R, y); }));
+      InArgs raw{};
+      raw.mode = IN_RAW;
+      raw.s = 1.0;
+      raw.u = y;
+      const int nt = c->row_npen * (rg.nl / 9);
+      TRY(launch(c, "row_fwd", [&] {
+        FC_POW3_SWITCH(rg.nl, (k_row_fwd_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, C, raw, st, twr, Wrow, c->tmW)));
+      }));
+    } else if (c->row_npen) {
+      const int nt = c->row_npen * (rg.nl / 9);
+      TRY(launch(c, "row_fwd", [&] {
+        FC_POW3_SWITCH(rg.nl, (k_row_fwd_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, C, ia, st, twr, Wrow, c->tmW)));
+      }));
+    } else {
+      const FftPlan pl_last = c->plan(rg.nl);
+      TRY(launch(c, "row_fwd", [&] {
+        k_row_fwd<<<(unsigned)nrow_blocks, kThreads, c->smem_row, s>>>(g, rg, C, ia, st, pl_last, Wrow);
       }));
     }
-  } else if (c->aniso_npen && C.kind == 1) {
-    const int nt = d * c->aniso_npen * (rg.nl / 9);
-    const double2* tw = c->rtw(rg.nl);
-    RowGeo ra = rg;
-    ra.B = 2 * c->aniso_npen;
-    ra.ntiles = (rg.np + ra.B - 1) / ra.B;
-    const int64_t nb = (int64_t)R * ra.no * ra.ntiles;
-    const int np_ = c->aniso_npen;
-    TRY(launch(c, "row_fwd", [&] {
-      FC_EXP_SWITCH(rg.nl, (k_row_fwd_aniso_r<LL><<<(unsigned)nb, nt, c->smem_aniso_r, s>>>(g, ra, C, ia, st, tw, Wrow, np_)));
-    }));
-  } else if (c->row_npen && c->row_pipe && row_pipe_ok(c, ia)) {
-    TRY(launch_row_fwd_pp(c, R, ia, st, Wrow));
-  } else if (c->row_npen) {
-    const int nt = c->row_npen * (rg.nl / 9);
-    const double2* tw = c->rtw(rg.nl);
-    TRY(launch(c, "row_fwd", [&] {
-      FC_POW3_SWITCH(rg.nl, (k_row_fwd_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_r, s>>>(g, rg, C, ia, st, tw, Wrow, c->tmW)));
-    }));
-  } else {
-    const FftPlan pl_last = c->plan(rg.nl);
-    TRY(launch(c, "row_fwd", [&] {
-      k_row_fwd<<<(unsigned)nrow_blocks, kThreads, c->smem_row, s>>>(g, rg, C, ia, st, pl_last, Wrow);
-    }));
-  }
-  if (d == 3) TRY(mid(false));
+    if (d == 3) TRY(mid(false));
   }
   if (phases & PH_OUTER) {
-  OuterGeo og = c->og;
-  og.orth = orth;
-  for (int a = 0; a < 3; ++a)
-    for (int b = 0; b < 3; ++b) og.M[a][b] = M[a][b];
-  double2* Wout = c->P > 1 ? c->W2r : c->W2;
-  og.R = R;
-  if (c->outer_c1) {
-    OuterGeo o1 = og;
-    o1.QB = c->outer_c1;
-    o1.nqb = (og.Q + o1.QB - 1) / o1.QB;
-    const int nt = d * o1.QB * (c->n0g / 9);
-    const double2* tw = c->rtw(c->n0g);
-    const size_t smem = (size_t)16 * d * o1.QB * c->n0g;
-    TRY(launch(c, "outer", [&] {
-      if (d == 2) FC_EXP_SWITCH(c->n0g, (k_outer_c1<LL, 2><<<(unsigned)(R * o1.nqb), nt, smem, s>>>(g, o1, smap, st, tw, Wout)))
-      else FC_EXP_SWITCH(c->n0g, (k_outer_c1<LL, 3><<<(unsigned)(R * o1.nqb), nt, smem, s>>>(g, o1, smap, st, tw, Wout)))
-    }));
-  } else if (c->outer_qb && c->outer_persist) {
-    const int nt = c->outer_qb * (c->n0g / 9);
-    const double2* tw = c->rtw(c->n0g);
-    const size_t smem = 2 * (size_t)16 * d * c->outer_qb * c->n0g;
-    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)R * og.nqb, c->num_sms);
-    TRY(launch(c, "outer", [&] {
-      if (d == 2) FC_EXP_SWITCH(c->n0g, (k_outer_p<LL, 2><<<grid, nt, smem, s>>>(g, og, smap, st, tw, Wout)))
-      else FC_EXP_SWITCH(c->n0g, (k_outer_p<LL, 3><<<grid, nt, smem, s>>>(g, og, smap, st, tw, Wout)))
-    }));
-  } else if (c->outer_qb && c->outer_seq && c->P == 1 && og.tma) {
-    const int nt = c->outer_qb * (c->n0g / 9);
-    const double2* tw = c->rtw(c->n0g);
-    TRY(launch(c, "outer", [&] {
-      if (d == 2) FC_EXP_SWITCH(c->n0g, (k_outer_seq<LL, 2><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
-      else FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
-    }));
-  } else if (c->outer_qb) {
-    const int nt = c->outer_qb * (c->n0g / 9);
-    const double2* tw = c->rtw(c->n0g);
-    TRY(launch(c, "outer", [&] {
-      if (d == 2) FC_POW3_SWITCH(c->n0g, (k_outer_r<LL, 2><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, smap, st, tw, Wout)))
-      else FC_POW3_SWITCH(c->n0g, (k_outer_r<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, smap, st, tw, Wout)))
-    }));
-  } else {
-    const FftPlan pl0 = c->plan(c->n0g);  // outer axis: global length (a slab holds n[0] < n0g planes)
-    TRY(launch(c, "outer", [&] {
-      k_outer<<<(unsigned)(R * og.nqb), kThreads, c->smem_outer, s>>>(g, og, smap, st, pl0, Wout);
-    }));
-  }
+    OuterGeo og = c->og;
+    og.orth = orth;
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) og.M[a][b] = M[a][b];
+    double2* Wout = c->P > 1 ? c->W2r : c->W2;
+    og.R = R;
+    if (c->outer_qb && c->outer_seq && c->P == 1 && og.tma) {
+      const int nt = c->outer_qb * (c->n0g / 9);
+      const double2* tw = c->rtw(c->n0g);
+      TRY(launch(c, "outer", [&] {
+        FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
+      }));
+    } else if (c->outer_qb) {
+      const int nt = c->outer_qb * (c->n0g / 9);
+      const double2* tw = c->rtw(c->n0g);
+      TRY(launch(c, "outer", [&] {
+        if (d == 2) FC_POW3_SWITCH(c->n0g, (k_outer_r<LL, 2><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, smap, st, tw, Wout)))
+        else FC_POW3_SWITCH(c->n0g, (k_outer_r<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, smap, st, tw, Wout)))
+      }));
+    } else {
+      const FftPlan pl0 = c->plan(c->n0g);  // outer axis: global length (a slab holds n[0] < n0g planes)
+      TRY(launch(c, "outer", [&] {
+        k_outer<<<(unsigned)(R * og.nqb), kThreads, c->smem_outer, s>>>(g, og, smap, st, pl0, Wout);
+      }));
+    }
   }
   if (!(phases & PH_INV)) return FC_OK;
   if (d == 3) TRY(mid(true));
@@ -889,17 +808,16 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     const unsigned grid = (unsigned)std::min<int64_t>(ntile, (int64_t)c->num_sms * c->inv_pipe_blocks);
     const int stage_c = c->inv_pipe_stage;
     const int nst = c->inv_pipe_nst;
-    const int qbuf = c->inv_pipe_qbuf;
-    const size_t smem = (size_t)nst * 16 * stage_c + (qbuf ? (size_t)8 * (2 * c->row_npen * rg.nl + 2) : 0);
+    const size_t smem = (size_t)nst * 16 * stage_c + (size_t)8 * (2 * c->row_npen * rg.nl + 2);
     return launch(c, "row_inv", [&] {
-      FC_POW3_SWITCH(rg.nl, (k_row_inv_pp<LL><<<grid, nt, smem, s>>>(g, rg, ea, st, tw, ntile, stage_c, nst, qbuf, c->tmW)));
+      FC_POW3_SWITCH(rg.nl, (k_row_inv_pp<LL><<<grid, nt, smem, s>>>(g, rg, ea, st, tw, ntile, stage_c, nst, 1, c->tmW)));
     });
   }
   if (c->row_npen) {
     const int nt = c->row_npen * (rg.nl / 9);
     const double2* tw = c->rtw(rg.nl);
     return launch(c, "row_inv", [&] {
-      FC_POW3_SWITCH(rg.nl, (k_row_inv_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_inv_r, s>>>(g, rg, ea, st, tw, Wrow, c->inv_prefetch, c->tmW)));
+      FC_POW3_SWITCH(rg.nl, (k_row_inv_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_inv_r, s>>>(g, rg, ea, st, tw, Wrow, c->tmW)));
     });
   }
   const FftPlan pl_last = c->plan(rg.nl);
@@ -987,6 +905,28 @@ int32_t fc_device_count(int32_t* count) {
   return FC_OK;
 }
 
+int32_t fc_set_plan_option(const char* key, int32_t value) {
+  if (key == nullptr) return set_err(FC_EINVAL, "null option name");
+  PlanOpts& o = g_plan_opts;
+  const struct { const char* name; int* field; } table[] = {
+      {"force_generic", &o.force_generic}, {"row_threads", &o.row_threads}, {"mid_threads", &o.mid_threads},
+      {"outer_threads", &o.outer_threads}, {"row_tma", &o.row_tma}, {"mid_tma", &o.mid_tma},
+      {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"inv_pipe", &o.inv_pipe},
+      {"aniso_fused", &o.aniso_fused}, {"defer_x", &o.defer_x}, {"fused_exchange", &o.fused_exchange},
+      {"sync_debug", &o.sync_debug}};
+  for (const auto& t : table)
+    if (std::strcmp(t.name, key) == 0) {
+      *t.field = value;
+      return FC_OK;
+    }
+  return set_err(FC_EINVAL, "unknown plan option '%s'", key);
+}
+
+int32_t fc_reset_plan_options(void) {
+  g_plan_opts = PlanOpts{};
+  return FC_OK;
+}
+
 }  // extern "C"
 
 namespace {
@@ -1025,7 +965,8 @@ int create_slab(fc_ctx** out, int32_t dim, const int64_t* shape, const double* h
   cudaGetDeviceProperties(&prop, device);
   if (prop.major < 10) return fail(set_err(FC_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor));
   c->smem_optin = (int)prop.sharedMemPerBlockOptin;
-  c->force_generic = getenv("FC_FORCE_GENERIC") != nullptr && atoi(getenv("FC_FORCE_GENERIC")) != 0;
+  c->opt = g_plan_opts;
+  c->force_generic = c->opt.force_generic != 0;
   c->num_sms = prop.multiProcessorCount;
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(set_err(FC_ECUDA, "stream creation failed"));
@@ -1055,27 +996,16 @@ int create_slab(fc_ctx** out, int32_t dim, const int64_t* shape, const double* h
     return fail(rc);
   // measured: faster for one pencil per block (L = 2187, cfg2), slower for the
   // short rows of cfg3 / cfg4 (L = 243 / 729: many pencils per block)
-  if (c->row_npen && env_flag("FC_INV_PIPE", c->row_npen == 1)) {
+  if (c->row_npen && (c->opt.inv_pipe >= 0 ? c->opt.inv_pipe != 0 : c->row_npen == 1)) {
     const RowGeo& rg = c->rg;
     const int B = 2 * c->row_npen;
     c->inv_pipe_stage = (std::max(rg.nbox * rg.boxK * B, c->row_npen * (rg.nl + 1)) + 7) & ~7;
-    c->inv_pipe_nst = std::max(2, std::min(4, env_int_g("FC_INV_STAGES", 2)));
-    c->inv_pipe_qbuf = env_int_g("FC_INV_QBUF", 1) != 0;
-    const size_t qbytes = c->inv_pipe_qbuf ? (size_t)8 * (2 * c->row_npen * rg.nl + 2) : 0;
-    size_t smem = (size_t)c->inv_pipe_nst * 16 * c->inv_pipe_stage + qbytes;
-    while (c->inv_pipe_nst > 2 && 2 * (smem + 2048) > (size_t)c->smem_optin) {  // keep 2 CTAs per SM
-      --c->inv_pipe_nst;
-      smem = (size_t)c->inv_pipe_nst * 16 * c->inv_pipe_stage + qbytes;
-    }
+    const size_t qbytes = (size_t)8 * (2 * c->row_npen * rg.nl + 2);
+    const size_t smem = (size_t)c->inv_pipe_nst * 16 * c->inv_pipe_stage + qbytes;
     int nb = 0;
     FC_POW3_SWITCH(rg.nl, (allow_smem(k_row_inv_pp<LL>, mx),
                            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_row_inv_pp<LL>, c->row_npen * (rg.nl / 9), smem)));
     c->inv_pipe_blocks = nb;
-  }
-  if (c->row_pipe) {
-    int nb = 0;
-    FC_EXP_SWITCH(c->rg.nl, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_row_fwd_pp<LL>, c->rg.nl / 9, c->smem_row_pp)));
-    c->row_pipe_blocks = nb;
   }
   if (cudaMalloc(&c->any_active, sizeof(int)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "flag alloc"));
   if (cudaMalloc(&c->counter, sizeof(unsigned)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "counter alloc"));
@@ -1164,12 +1094,11 @@ int32_t fc_create_sharded(fc_ctx** out, int32_t dim, const int64_t* shape, const
         cudaGetLastError();
       }
   // fused exchange: the sweeps store into the other slabs' buffers directly
-  // (FC_FUSED_EXCHANGE=0 keeps the copy-engine exchange)
-  const char* fx = getenv("FC_FUSED_EXCHANGE");
-  const bool fuse = nslabs > 1 && !(fx && atoi(fx) == 0);
+  // (plan option fused_exchange = 0 keeps the copy-engine exchange)
+  const bool fuse = nslabs > 1 && c->sub[0]->opt.fused_exchange;
   for (fc_ctx* sl : c->sub) {
     sl->sibs = &c->sub;
-    sl->fused = fuse && !sl->outer_c1 && !sl->outer_persist;
+    sl->fused = fuse;
   }
   *out = c;
   return FC_OK;
@@ -1381,6 +1310,8 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
   CK(cudaMemsetAsync(c->x, 0, sizeof(double) * fieldR, s));
   const int nrow = (int)nslot_row(c);
   const int nvec = (int)nslot_vec(c);
+  {  // right-hand side and warm start (profiled as "<kernel>_rhs")
+  ProfTag rhs_tag(c, "_rhs");
   if (init != nullptr) {
     // x = G init (solver.py:185)
     TRY(upload_fields(c, c->p[0], init, R));
@@ -1423,6 +1354,7 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
       k_sub_dot<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->p[1], c->p[0], c->r, c->part, nvec, f);
     }));
   }
+  }
   std::vector<RhsState> hs(R);
   CK(cudaMemcpyAsync(hs.data(), c->st, sizeof(RhsState) * R, cudaMemcpyDeviceToHost, s));
   TRY(sync(c));
@@ -1438,8 +1370,7 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
   // p_old anyway (saves the x read of p in k_cg_update: 1 of its 6 words per
   // element); the last update of each RHS is flushed after the loop.  Bitwise
   // identical to the immediate update.  record_iterates needs x every iteration.
-  const bool defer_env = env_flag("FC_DEFER_X", 1);  // read per solve (tests toggle it)
-  const bool defer = defer_env && !record;
+  const bool defer = c->opt.defer_x && !record;
   for (int it = 0; any && it < max_iter; ++it) {
     double* pcur = c->p[it & 1];
     double* pold = c->p[(it + 1) & 1];

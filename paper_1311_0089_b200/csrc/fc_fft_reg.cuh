@@ -110,45 +110,6 @@ struct R9Driver {
   }
 };
 
-// Twiddle prefetch (one pencil per thread): the inter-pass twiddles of pass
-// S + 1 are loaded before the exchange after pass S, so their latency hides
-// behind the exchange barriers instead of stalling the first cmul of the pass.
-#ifndef FC_TW_PREFETCH
-#define FC_TW_PREFETCH 0  // measured neutral on cfg2 / cfg3 (off)
-#endif
-template <int L, bool INV, int S>
-__device__ __forceinline__ void tw9_load(double2 (&w)[8], int j, const double2* __restrict__ tw) {
-  constexpr int Ns = ipow9(S);
-  const int k = j % Ns;
-#pragma unroll
-  for (int r = 1; r < 9; ++r) {
-    w[r - 1] = __ldg(tw + R9<L>::off9(S) + (r - 1) * Ns + k);
-    if (INV) w[r - 1].y = -w[r - 1].y;
-  }
-}
-template <int L, int CPT, bool INV, int S>
-struct R9DriverPF {
-  __device__ __forceinline__ static void run(double2 (&v)[CPT][9], double2* sm, int pstride, int j,
-                                             const double2* __restrict__ tw, const double2 (&w)[8]) {
-    if constexpr (S > 0) {
-#pragma unroll
-      for (int c = 0; c < CPT; ++c)
-#pragma unroll
-        for (int r = 1; r < 9; ++r) v[c][r] = cmul(v[c][r], w[r - 1]);
-    }
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) bfly9<INV>(v[c]);
-    if constexpr (S + 1 < R9<L>::NP9) {
-      double2 wn[8];
-      tw9_load<L, INV, S + 1>(wn, j, tw);
-      r9_exchange<L, CPT, S>(v, sm, pstride, j);
-      R9DriverPF<L, CPT, INV, S + 1>::run(v, sm, pstride, j, tw, wn);
-    } else if constexpr (R9<L>::TAIL) {
-      r9_exchange<L, CPT, S>(v, sm, pstride, j);
-    }
-  }
-};
-
 __host__ __device__ constexpr bool is_pow3(int L) { return L == 1 || (L % 3 == 0 && is_pow3(L / 3)); }
 // Register-path lengths: 3^k (9 .. 2187) and 5 * 3^k (45 .. 1215, the cfg5 axis)
 __host__ __device__ constexpr bool is_reg_len(int L) {
@@ -232,12 +193,7 @@ template <int L, int CPT, bool INV>
 __device__ __forceinline__ void fft_reg(double2 (&v)[CPT][9], double2* sm, int pstride, int j,
                                         const double2* __restrict__ tw) {
   if constexpr (is_pow3(L)) {
-    if constexpr (FC_TW_PREFETCH && CPT == 1) {
-      const double2 w0[8] = {};
-      R9DriverPF<L, CPT, INV, 0>::run(v, sm, pstride, j, tw, w0);
-    } else {
-      R9Driver<L, CPT, INV, 0>::run(v, sm, pstride, j, tw);
-    }
+    R9Driver<L, CPT, INV, 0>::run(v, sm, pstride, j, tw);
     if constexpr (R9<L>::TAIL) r3_tail<L, CPT, INV>(v, j, tw);
   } else {
     fft_reg_5m<L, CPT, INV>(v, sm, pstride, j, tw);

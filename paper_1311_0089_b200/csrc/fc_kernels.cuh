@@ -691,7 +691,6 @@ __global__ void k_fin_global(FinArgs f, SlabSums ss) {
 // outer index o < no (d = 3: o = i0; d = 2: no = 1).
 struct RowGeo {
   int nl, hl, np, no, B, ntiles;
-  int exp_natural;  // experiment switch (FC_EXP_NATURAL_STORE), never set in production
   int tma = 0;      // transposed spectrum moved by TMA boxes {2B doubles, boxK modes} (fc_tma.cuh)
   int boxK = 0, nbox = 0;
 };

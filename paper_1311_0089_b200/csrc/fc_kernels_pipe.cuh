@@ -1,15 +1,5 @@
-// Persistent, double-buffered first sweep for power-of-three contiguous axes.
-//
-// The one-shot row kernel (fc_kernels_reg.cuh: k_row_fwd_r) loads a row block,
-// transforms it and stores it, so HBM idles whenever both resident CTAs of an
-// SM transform at the same time.  Here one CTA per SM walks the row pairs
-// (tile t, t + G, t + 2G, ...) and keeps the next pair's inputs in flight while
-// the current pair is transformed: the TMA bulk loads of tile t + G land in
-// the second shared-memory stage during the FFT of tile t.
-//
-// Row block = one complex pencil (rows 2q, 2q+1).  Same layouts, modes and
-// rounding as the staged path of k_row_fwd_r; the transposed half spectrum is
-// written with TMA tensor boxes (RowGeo::tma).
+// Persistent, double-buffered last sweep (k_row_inv_pp) and the one-component-
+// at-a-time outer sweep (k_outer_seq) for register-path axis lengths.
 #pragma once
 #include "fc_kernels_reg.cuh"
 
@@ -31,163 +21,6 @@ __device__ __forceinline__ PipeTile pipe_decode(int64_t t, int c, const RowGeo& 
   q.o = (int)(t % rg.no);
   q.r = (int)(t / rg.no);
   return q;
-}
-
-// Persistent first sweep, 2 CTAs per SM.  Shared memory: one input stage
-// U[stride] P[stride] (r / p_old, or the raw field) and one spectrum buffer Z
-// (the FFT exchange, then the split half spectra Y[k][2] written in place).
-// A is read straight from global memory (issued before the stage wait).  As
-// soon as the pointwise step has moved the inputs into registers the stage is
-// refilled with block t + G by TMA, so those loads overlap this block's FFT,
-// split and store.
-template <int L>
-__global__ void __launch_bounds__(256, 2) k_row_fwd_pp(Geo g, RowGeo rg, Coef C, InArgs ia, const RhsState* st,
-                                                       const double2* __restrict__ tw, int64_t ntile,
-                                                       const __grid_constant__ CUtensorMap tmW) {
-  constexpr int TP = RegTP<L>::value;
-  constexpr int hl = (L + 1) / 2;
-  constexpr int stride = pipe_stride<L>();
-  constexpr int zoff = (2 * stride + 15) & ~15;  // doubles: Z starts 128-byte aligned
-  extern __shared__ __align__(128) unsigned char smraw[];
-  double* S = reinterpret_cast<double*>(smraw);
-  double2* Z = reinterpret_cast<double2*>(S + zoff);
-  __shared__ uint64_t bar;
-  __shared__ double s_beta[FC_MAX_RHS_DEV];
-  __shared__ double s_alpha[FC_MAX_RHS_DEV];
-  __shared__ int s_flags[FC_MAX_RHS_DEV];  // bit 0 active, bit 1 first
-  const int c = g.dim;
-  const int j = threadIdx.x;  // one pencil per CTA: thread j = FFT lane
-  const int R = (int)(ntile / ((int64_t)c * rg.ntiles * rg.no));
-  if (threadIdx.x < R) {
-    const int r = threadIdx.x;
-    const bool act = rhs_active(st, r);
-    const bool first = ia.mode == IN_PNEW ? st[r].first != 0 : true;
-    s_flags[r] = (act ? 1 : 0) | (first ? 2 : 0);
-    s_beta[r] = ia.mode == IN_PNEW ? st[r].beta : 0.0;
-    s_alpha[r] = ia.mode == IN_PNEW ? st[r].alpha : 0.0;
-  }
-  if (threadIdx.x == 0) mbar_init(&bar, 1);
-  __syncthreads();
-
-  struct Src {
-    const double *u, *p, *A;
-    int n;
-  };
-  auto sources = [&](const PipeTile& q) {
-    Src o;
-    const int row0 = q.tile * 2;
-    o.n = min(2, rg.np - row0) * L;
-    const int64_t vbase = ((int64_t)q.o * rg.np + row0) * L;
-    const int64_t ub = (int64_t)q.r * c * g.N + (int64_t)q.a * g.N + vbase;
-    o.u = ia.u + ub;
-    o.p = (ia.mode == IN_PNEW && !(s_flags[q.r] & 2)) ? ia.p_old + ub : nullptr;
-    o.A = ia.mode != IN_RAW ? C.A + vbase : nullptr;
-    return o;
-  };
-  // first active block at or after t (inactive right-hand sides are skipped)
-  auto next_active = [&](int64_t t) {
-    while (t < ntile && !(s_flags[pipe_decode(t, c, rg).r] & 1)) t += gridDim.x;
-    return t;
-  };
-  auto prefetch = [&](int64_t t) {  // thread 0
-    if (t >= ntile) return;
-    const Src o = sources(pipe_decode(t, c, rg));
-    const int su = bulk_shift(o.u), sp = o.p ? bulk_shift(o.p) : 0;
-    mbar_expect_tx(&bar, bulk_bytes(o.n, su) + (o.p ? bulk_bytes(o.n, sp) : 0u));
-    bulk_g2s(S, o.u - su, bulk_bytes(o.n, su), &bar);
-    if (o.p) bulk_g2s(S + stride, o.p - sp, bulk_bytes(o.n, sp), &bar);
-  };
-  int64_t t = next_active(blockIdx.x);
-  if (threadIdx.x == 0) prefetch(t);
-  unsigned phase = 0u;
-  for (; t < ntile;) {
-    const PipeTile q = pipe_decode(t, c, rg);
-    const int a = q.a, r = q.r;
-    const Src o = sources(q);
-    const int nrows = o.n / L;
-    const bool pnew = ia.mode == IN_PNEW;
-    const bool first = (s_flags[r] & 2) != 0;
-    const double beta = s_beta[r];
-    // coefficient values straight from global memory, issued before the wait
-    double av[2][9];
-#pragma unroll
-    for (int s = 0; s < 9; ++s)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) av[h][s] = (o.A && h < nrows) ? __ldg(o.A + h * L + j + s * TP) : 0.0;
-    mbar_wait(&bar, phase);
-    phase ^= 1u;
-    const double* st_u = S + bulk_shift(o.u);
-    const double* st_p = S + stride + (o.p ? bulk_shift(o.p) : 0);
-    double* pw = pnew ? ia.p_new + (o.u - ia.u) : nullptr;
-    double* xw = (pnew && !first && ia.xacc) ? ia.xacc + (o.u - ia.u) : nullptr;
-    const double alpha = s_alpha[r];
-    const double A0aa = ia.mode == IN_FP ? pick3(ia.A0, a, a) : 0.0;
-    double2 v[1][9];
-#pragma unroll
-    for (int s = 0; s < 9; ++s) {
-      const int i = j + s * TP;
-      double y[2] = {0.0, 0.0};
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h < nrows) {
-          const int e = h * L + i;
-          double x = st_u[e];
-          if (pnew) {
-            x = first ? x : __dadd_rn(x, __dmul_rn(beta, st_p[e]));
-            pw[e] = x;
-            if (xw) xw[e] = __dadd_rn(xw[e], __dmul_rn(alpha, st_p[e]));
-          }
-          double val;
-          if (ia.mode == IN_RAW) val = x;
-          else if (ia.mode == IN_FP) val = __dmul_rn(__dsub_rn(av[h][s], A0aa), x);
-          else val = __dmul_rn(av[h][s], x);
-          if (ia.mode != IN_FP && ia.s != 1.0) val = __dmul_rn(ia.s, val);
-          y[h] = val;
-        }
-      }
-      v[0][s] = make_double2(y[0], y[1]);
-    }
-    const int64_t tn = next_active(t + gridDim.x);
-    __syncthreads();  // the stage has been read: refill it with the next block
-    if (threadIdx.x == 0) {
-      bulk_wait_read0();  // the previous block's spectrum store has left Z
-      prefetch(tn);
-    }
-    fft_reg<L, 1, false>(v, Z, L, j, tw);
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < 9; ++s) Z[j + s * TP] = v[0][s];
-    __syncthreads();
-    // split in place: gather (z_k, z_{L-k}) for this thread's modes, then write Y[k][2]
-    constexpr int KP = (hl + TP - 1) / TP;
-    double2 zk[KP], zm[KP];
-#pragma unroll
-    for (int m = 0; m < KP; ++m) {
-      const int k = j + m * TP;
-      if (k < hl) {
-        zk[m] = Z[k];
-        zm[m] = Z[k == 0 ? 0 : L - k];
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int m = 0; m < KP; ++m) {
-      const int k = j + m * TP;
-      if (k < hl) {
-        Z[2 * k] = make_double2(0.5 * (zk[m].x + zm[m].x), 0.5 * (zk[m].y - zm[m].y));
-        Z[2 * k + 1] = make_double2(0.5 * (zk[m].y + zm[m].y), 0.5 * (zm[m].x - zk[m].x));
-      }
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int c2 = (r * c + a) * rg.no + q.o;
-      for (int b = 0; b < rg.nbox; ++b) tma_store_3d(&tmW, 4 * q.tile, b * rg.boxK, c2, Z + (size_t)b * rg.boxK * 2);
-      bulk_commit();
-    }
-    t = tn;
-  }
-  if (threadIdx.x == 0) bulk_wait_read0();
 }
 
 // Persistent, multi-buffered last sweep (nst <= 4 stages): each CTA walks its

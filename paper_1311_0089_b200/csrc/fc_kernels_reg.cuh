@@ -184,19 +184,6 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, 
   __syncthreads();
   constexpr int hl = (L + 1) / 2;
   double2* Wb = W + ((int64_t)(r * c + a) * rg.no + o) * hl * rg.np + row0;
-  if (rg.exp_natural) {  // EXPERIMENT ONLY (wrong layout): row-major store to time the transpose cost
-    for (int idx = threadIdx.x; idx < hl * nrows; idx += blockDim.x) {
-      const int row = idx / hl, k = idx - row * hl;
-      const double2* z = sm + (size_t)(row >> 1) * L;
-      const double2 zk = z[k];
-      const double2 zm = z[k == 0 ? 0 : L - k];
-      double2 y;
-      if ((row & 1) == 0) y = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-      else y = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
-      W[((int64_t)(r * c + a) * rg.no + o) * hl * rg.np + (int64_t)(row0 + row) * hl + k] = y;
-    }
-    return;
-  }
   const int npairs = (nrows + 1) >> 1;
   if (rg.tma) {
     // split into Y[k][row] (complex) behind the pencils, then TMA-store the boxes
@@ -240,7 +227,7 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, 
 template <int L>
 __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs ea, const RhsState* st,
                                                           const double2* __restrict__ tw,
-                                                          const double2* __restrict__ W, int prefetch,
+                                                          const double2* __restrict__ W,
                                                           const __grid_constant__ CUtensorMap tmW) {
   constexpr int TP = RegTP<L>::value;
   constexpr int hl = (L + 1) / 2;
@@ -262,26 +249,10 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   const double2* Wb = W + ((int64_t)(r * c + a) * rg.no + o) * hl * rg.np + row0;
   const int64_t vbase = ((int64_t)o * rg.np + row0) * L;
   const int64_t ebase = ((int64_t)r * c + a) * g.N + vbase;
-  // epilogue input (p for EP_AP, e for EP_FP) prefetched with cp.async into the
-  // area behind the exchange buffer; it lands while the spectrum is transformed
-  const size_t ystage = rg.tma ? (size_t)rg.nbox * rg.boxK * rg.B : 0;
-  double* st_q = reinterpret_cast<double*>(sm + max((size_t)(rg.B / 2) * (L + 1), ystage));
+  // epilogue input (p for EP_AP, e for EP_FP), read in the epilogue
   const bool need_q = ea.mode == EP_AP || ea.mode == EP_FP;
   const double* qsrc = (ea.mode == EP_AP ? ea.p : ea.out) + ebase;
-  __shared__ uint64_t bar, barq;
-  int qshift = 0;
-  if (need_q && prefetch) {
-    if (rg.tma) {  // one bulk copy on its own barrier, waited for only in the epilogue
-      qshift = bulk_shift(qsrc);
-      if (threadIdx.x == 0) {
-        mbar_init(&barq, 1);
-        mbar_expect_tx(&barq, bulk_bytes(nrows * L, qshift));
-        bulk_g2s(st_q, qsrc - qshift, bulk_bytes(nrows * L, qshift), &barq);
-      }
-    } else {
-      stage_doubles(st_q, qsrc, nrows * L);
-    }
-  }
+  __shared__ uint64_t bar;
   // Y staged at sm[k * yk + row * yr]: TMA boxes give [k][row], the fallback [row][k]
   const int yk = rg.tma ? rg.B : 1;
   const int yr = rg.tma ? 1 : hl;
@@ -342,21 +313,7 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   const double Ea = ea.mode == EP_FP ? pick(ea.E, r, a) : 0.0;
   const bool he = re < nrows;
   double2 q[9];
-  if (need_q && prefetch) {
-    if (rg.tma) {
-      mbar_wait(&barq, 0);
-    } else {
-      cp_async_wait_all();
-      __syncthreads();
-    }
-    const double* sq = st_q + qshift;
-#pragma unroll
-    for (int s = 0; s < 9; ++s) {
-      const int i = j + s * TP;
-      q[s].x = he ? sq[re * L + i] : 0.0;
-      q[s].y = has_o ? sq[ro * L + i] : 0.0;
-    }
-  } else if (need_q) {
+  if (need_q) {
 #pragma unroll
     for (int s = 0; s < 9; ++s) {
       const int i = j + s * TP;
@@ -752,339 +709,3 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
 
 }  // namespace fc
 
-namespace fc {
-
-// First sweep for packed (anisotropic) coefficients: one CTA owns a row block
-// for ALL c components (thread groups per component), so r, p_old (or e / u)
-// and the packed tensor are staged once per voxel with cp.async instead of
-// being re-read by c per-component CTAs.  Thread (a, p, j): component a,
-// pencil p (rows 2p, 2p+1), FFT lane j.  Staging layout (doubles):
-//   U[b][row][i]  (b < c)   PO[b][row][i] (b < c, IN_PNEW)   A[m][row][i] (m < nsym)
-template <int L>
-__global__ void __launch_bounds__(kMaxBlock, 1) k_row_fwd_aniso_r(Geo g, RowGeo rg, Coef C, InArgs ia,
-                                                                  const RhsState* st, const double2* __restrict__ tw,
-                                                                  double2* __restrict__ W, int npen) {
-  constexpr int TP = RegTP<L>::value;
-  extern __shared__ double2 sm[];
-  const int c = g.dim;
-  const int nsym = c * (c + 1) / 2;
-  int64_t bid = blockIdx.x;
-  const int tile = bid % rg.ntiles; bid /= rg.ntiles;
-  const int o = bid % rg.no;
-  const int r = (int)(bid / rg.no);
-  if (!rhs_active(st, r)) return;
-  const int row0 = tile * rg.B;
-  const int nrows = min(rg.B, rg.np - row0);
-  const int per_a = npen * TP;
-  const int a = threadIdx.x / per_a;
-  const int t = threadIdx.x - a * per_a;
-  const int p = t / TP;
-  const int j = t - p * TP;
-  const InEval ev = make_eval(ia, g, C, st, r, a);
-  const int mode = ev.mode;
-  const bool use_u = mode != IN_CONST;
-  const bool use_p = mode == IN_PNEW && !ev.first;
-  const bool use_a = mode != IN_RAW;
-  const int blk = rg.B * L;  // doubles per staged array
-  double* S = reinterpret_cast<double*>(sm);
-  double* SU = S;
-  double* SP = SU + (use_u ? c * blk : 0);
-  double* SA = SP + (use_p ? c * blk : 0);
-  const int n = nrows * L;
-  const int64_t vbase = ((int64_t)o * rg.np + row0) * L;
-  const int64_t rbase = (int64_t)r * c * g.N;
-  for (int b = 0; b < c; ++b) {
-    if (use_u) stage_doubles(SU + b * blk, ia.u + rbase + (int64_t)b * g.N + vbase, n);
-    if (use_p) stage_doubles(SP + b * blk, ia.p_old + rbase + (int64_t)b * g.N + vbase, n);
-  }
-  if (use_a)
-    for (int m = 0; m < nsym; ++m) stage_doubles(SA + m * blk, C.A + (int64_t)m * g.N + vbase, n);
-  cp_async_wait_all();
-  __syncthreads();
-  double2 v[1][9];
-  double2 pn[9];
-#pragma unroll
-  for (int s = 0; s < 9; ++s) {
-    const int i = j + s * TP;
-    double y[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int row = 2 * p + h;
-      if (row >= nrows) continue;
-      const int e = row * L + i;
-      double acc = 0.0;
-      for (int b = 0; b < c; ++b) {
-        double x;
-        if (mode == IN_CONST) {
-          x = InEval::sel(b, ev.E0, ev.E1, ev.E2);
-        } else {
-          x = SU[b * blk + e];
-          if (mode == IN_PNEW && !ev.first) x = __dadd_rn(x, __dmul_rn(ev.beta, SP[b * blk + e]));
-        }
-        if (mode == IN_PNEW && b == a) {
-          q[h] = x;
-          if (ev.xacc) {
-            double* xw = ev.xacc + rbase + (int64_t)a * g.N + vbase + e;
-            *xw = __dadd_rn(*xw, __dmul_rn(ev.alpha, SP[b * blk + e]));
-          }
-        }
-        if (mode == IN_RAW) {
-          if (b == a) acc = x;
-          continue;
-        }
-        double Aab = SA[pidx(c, a, b) * blk + e];
-        if (mode == IN_FP) Aab = __dsub_rn(Aab, InEval::sel(b, ev.R0, ev.R1, ev.R2));
-        acc = __dadd_rn(acc, __dmul_rn(Aab, x));
-      }
-      if (mode != IN_FP && ev.s != 1.0) acc = __dmul_rn(ev.s, acc);
-      y[h] = acc;
-    }
-    v[0][s] = make_double2(y[0], y[1]);
-    pn[s] = make_double2(q[0], q[1]);
-  }
-  if (mode == IN_PNEW) {
-    double* pw = ia.p_new + rbase + (int64_t)a * g.N + vbase;
-#pragma unroll
-    for (int s = 0; s < 9; ++s) {
-      if (2 * p < nrows) pw[(int64_t)(2 * p) * L + j + s * TP] = pn[s].x;
-      if (2 * p + 1 < nrows) pw[(int64_t)(2 * p + 1) * L + j + s * TP] = pn[s].y;
-    }
-  }
-  double2* smp = sm + (size_t)(a * npen + p) * L;
-  fft_reg<L, 1, false>(v, smp, L, j, tw);
-  __syncthreads();
-#pragma unroll
-  for (int s = 0; s < 9; ++s) smp[j + s * TP] = v[0][s];
-  __syncthreads();
-  constexpr int hl = (L + 1) / 2;
-  const int per_comp = hl * nrows;
-  for (int idx = threadIdx.x; idx < c * per_comp; idx += blockDim.x) {
-    const int aa = idx / per_comp;
-    const int rem = idx - aa * per_comp;
-    const int k = rem / nrows, row = rem - k * nrows;
-    const double2* z = sm + (size_t)(aa * npen + (row >> 1)) * L;
-    const double2 zk = z[k];
-    const double2 zm = z[k == 0 ? 0 : L - k];
-    double2 y;
-    if ((row & 1) == 0) y = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-    else y = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
-    W[((int64_t)(r * c + aa) * rg.no + o) * hl * rg.np + row0 + (int64_t)k * rg.np + row] = y;
-  }
-}
-
-}  // namespace fc
-
-namespace fc {
-
-// Persistent outer sweep: one CTA per SM loops over pencil groups; the next
-// group is prefetched with cp.async into the second smem stage while the
-// current one is transformed, so HBM traffic overlaps the FFT arithmetic.
-// Stage layout: [a][qq][L] complex; the current stage doubles as the FFT
-// exchange buffer once its data sit in registers.
-template <int L, int C>
-__global__ void __launch_bounds__(kMaxBlockOuter, 1) k_outer_p(Geo g, OuterGeo og, SlabMap sm_, const RhsState* st,
-                                                               const double2* __restrict__ tw, double2* __restrict__ W) {
-  constexpr int TP = RegTP<L>::value;
-  extern __shared__ double2 sm[];
-  const int stage = og.QB * C * L;
-  const int qq = threadIdx.x / TP;
-  const int j = threadIdx.x - qq * TP;
-  const int ntiles = og.nqb * gridDim.y;  // gridDim.y = R
-  (void)ntiles;
-  const int ntile = og.nqb * og.R;
-  auto tile_src = [&](int t, int a, int s, int& ok) -> int64_t {
-    const int qb = t % og.nqb;
-    const int r = t / og.nqb;
-    const int ql = qb * og.QB + qq;
-    ok = ql < og.Q;
-    const int i0 = j + s * TP;
-    const int p = slab_of(sm_.s0, sm_.P, i0);
-    const int n0p = sm_.s0[p + 1] - sm_.s0[p];
-    return sm_.roff[p] + (int64_t)(r * C + a) * og.Q * n0p + (int64_t)(ok ? ql : 0) * n0p + (i0 - sm_.s0[p]);
-  };
-  auto prefetch = [&](int t, int buf) {
-    const int r = t / og.nqb;
-    if (st != nullptr && !st[r].active) return;
-    double2* dst = sm + (size_t)buf * stage;
-#pragma unroll
-    for (int a = 0; a < C; ++a)
-#pragma unroll
-      for (int s = 0; s < 9; ++s) {
-        int ok;
-        const int64_t off = tile_src(t, a, s, ok);
-        if (ok) cp_async16(dst + ((size_t)a * og.QB + qq) * L + j + s * TP, W + off);
-      }
-  };
-  int t = blockIdx.x;
-  int cur = 0;
-  if (t < ntile) prefetch(t, 0);
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-  for (; t < ntile; t += gridDim.x) {
-    const int tn = t + gridDim.x;
-    if (tn < ntile) prefetch(tn, cur ^ 1);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    __syncthreads();
-    const int qb = t % og.nqb;
-    const int r = t / og.nqb;
-    const bool act = st == nullptr || st[r].active;
-    const int ql = qb * og.QB + qq;
-    const bool live = ql < og.Q;
-    double2* buf = sm + (size_t)cur * stage;
-    if (act) {
-      double2 v[C][9];
-#pragma unroll
-      for (int a = 0; a < C; ++a)
-#pragma unroll
-        for (int s = 0; s < 9; ++s)
-          v[a][s] = live ? buf[((size_t)a * og.QB + qq) * L + j + s * TP] : make_double2(0.0, 0.0);
-      double2* smp = buf + (size_t)qq * L;
-      fft_reg<L, C, false>(v, smp, og.QB * L, j, tw);
-      const int q = sm_.qs[sm_.me] + (live ? ql : 0);
-      double xi1 = 0.0, xi2 = 0.0;
-      if (C == 2) {
-        xi1 = g.xi[1][q];
-      } else {
-        const int k2 = q / og.n1, k1 = q - k2 * og.n1;
-        xi1 = g.xi[1][k1];
-        xi2 = g.xi[2][k2];
-      }
-      const bool qzero = live && q == 0;
-#pragma unroll
-      for (int s = 0; s < 9; ++s) {
-        const int i0 = j + s * TP;
-        double xi[3] = {g.xi[0][i0], xi1, xi2};
-        if (qzero && i0 == 0) {
-#pragma unroll
-          for (int a = 0; a < C; ++a) v[a][s] = make_double2(0.0, 0.0);
-          continue;
-        }
-        double2 dots = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int a = 0; a < C; ++a) {
-          dots.x += xi[a] * v[a][s].x;
-          dots.y += xi[a] * v[a][s].y;
-        }
-        double den = 0.0;
-        if (og.orth) {
-#pragma unroll
-          for (int a = 0; a < C; ++a) den += xi[a] * xi[a];
-        } else {
-#pragma unroll
-          for (int a = 0; a < C; ++a)
-#pragma unroll
-            for (int b = 0; b < C; ++b) den += xi[a] * og.M[a][b] * xi[b];
-        }
-        const double inv = 1.0 / den;
-        const double2 qv = make_double2(dots.x * inv, dots.y * inv);
-#pragma unroll
-        for (int a = 0; a < C; ++a) v[a][s] = make_double2(xi[a] * qv.x, xi[a] * qv.y);
-      }
-      fft_reg<L, C, true>(v, smp, og.QB * L, j, tw);
-      if (live) {
-#pragma unroll
-        for (int a = 0; a < C; ++a)
-#pragma unroll
-          for (int s = 0; s < 9; ++s) {
-            int ok;
-            const int64_t off = tile_src(t, a, s, ok);
-            W[off] = v[a][s];
-          }
-      }
-    }
-    __syncthreads();  // this stage becomes the prefetch target of tile t + 2 gridDim.x
-    cur ^= 1;
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-}
-
-}  // namespace fc
-
-namespace fc {
-
-// Outer sweep, one component per thread: thread (a, qq, j) transforms pencil
-// (a, q); Gamma_hat needs all components of a mode, so after the forward FFT
-// the spectra meet once in shared memory.  ~1/C of the registers of k_outer_r,
-// hence C times the resident warps, for one extra shared-memory exchange.
-template <int L, int C>
-__global__ void __launch_bounds__(512, 1) k_outer_c1(Geo g, OuterGeo og, SlabMap sm_, const RhsState* st,
-                                                     const double2* __restrict__ tw, double2* __restrict__ W) {
-  constexpr int TP = RegTP<L>::value;
-  extern __shared__ double2 sm[];
-  const int qb = blockIdx.x % og.nqb;
-  const int r = blockIdx.x / og.nqb;
-  if (!rhs_active(st, r)) return;
-  const int per_a = og.QB * TP;
-  const int a = threadIdx.x / per_a;
-  const int rem = threadIdx.x - a * per_a;
-  const int qq = rem / TP;
-  const int j = rem - qq * TP;
-  const int ql = qb * og.QB + qq;
-  const bool live = ql < og.Q;
-  const int q = sm_.qs[sm_.me] + (live ? ql : 0);
-  int64_t eoff[9];
-#pragma unroll
-  for (int s = 0; s < 9; ++s) {
-    const int i0 = j + s * TP;
-    const int p = slab_of(sm_.s0, sm_.P, i0);
-    const int n0p = sm_.s0[p + 1] - sm_.s0[p];
-    eoff[s] = sm_.roff[p] + (int64_t)(r * C + a) * og.Q * n0p + (int64_t)(live ? ql : 0) * n0p + (i0 - sm_.s0[p]);
-  }
-  double2 v[1][9];
-#pragma unroll
-  for (int s = 0; s < 9; ++s) v[0][s] = live ? W[eoff[s]] : make_double2(0.0, 0.0);
-  double2* smp = sm + (size_t)(a * og.QB + qq) * L;
-  fft_reg<L, 1, false>(v, smp, L, j, tw);
-  __syncthreads();
-#pragma unroll
-  for (int s = 0; s < 9; ++s) smp[j + s * TP] = v[0][s];
-  __syncthreads();
-  double xi1 = 0.0, xi2 = 0.0;
-  if (C == 2) {
-    xi1 = g.xi[1][q];
-  } else {
-    const int k2 = q / og.n1, k1 = q - k2 * og.n1;
-    xi1 = g.xi[1][k1];
-    xi2 = g.xi[2][k2];
-  }
-  const double xia = a == 0 ? 0.0 : (a == 1 ? xi1 : xi2);  // xi_a for a >= 1 (a = 0 uses xi0 below)
-  const bool qzero = live && q == 0;
-#pragma unroll
-  for (int s = 0; s < 9; ++s) {
-    const int i0 = j + s * TP;
-    const double xi0 = g.xi[0][i0];
-    if (qzero && i0 == 0) {
-      v[0][s] = make_double2(0.0, 0.0);
-      continue;
-    }
-    double xi[3] = {xi0, xi1, xi2};
-    double2 vb[C];
-#pragma unroll
-    for (int b = 0; b < C; ++b) vb[b] = sm[(size_t)(b * og.QB + qq) * L + i0];
-    double2 dots = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int b = 0; b < C; ++b) {
-      dots.x += xi[b] * vb[b].x;
-      dots.y += xi[b] * vb[b].y;
-    }
-    double den = 0.0;
-    if (og.orth) {
-#pragma unroll
-      for (int b = 0; b < C; ++b) den += xi[b] * xi[b];
-    } else {
-#pragma unroll
-      for (int b = 0; b < C; ++b)
-#pragma unroll
-        for (int e = 0; e < C; ++e) den += xi[b] * og.M[b][e] * xi[e];
-    }
-    const double inv = 1.0 / den;
-    const double xa = a == 0 ? xi0 : xia;
-    v[0][s] = make_double2(xa * (dots.x * inv), xa * (dots.y * inv));
-  }
-  fft_reg<L, 1, true>(v, smp, L, j, tw);
-  if (!live) return;
-#pragma unroll
-  for (int s = 0; s < 9; ++s) W[eoff[s]] = v[0][s];
-}
-
-}  // namespace fc

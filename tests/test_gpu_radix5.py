@@ -1,8 +1,7 @@
 """GPU: register-path FFT lengths 5 * 3^k (45, 135, 405, 1215 -- the cfg5 axis
 class).  Operators and CG solves against the CPU oracle, against the Stockham
-path (FC_FORCE_GENERIC=1), and sharded against a single slab."""
+path (plan option force_generic), and sharded against a single slab."""
 
-import os
 
 import numpy as np
 import pytest
@@ -15,20 +14,12 @@ from paper_1311_0089_b200.grid import GridSpec
 pytestmark = pytest.mark.gpu
 
 
-def _ctx(shape, a, env=None, slabs=None):
-    old = {k: os.environ.get(k) for k in (env or {})}
-    os.environ.update(env or {})
-    try:
-        spec = GridSpec((1.0,) * len(shape), shape)
+def _ctx(shape, a, opts=None, slabs=None):
+    spec = GridSpec((1.0,) * len(shape), shape)
+    with _native.plan_options(**(opts or {})):
         ctx = _native.Context(spec, slabs=slabs) if slabs else _native.Context(spec)
-        ctx.set_coefficients(CoefficientField.isotropic(spec, a))
-        return ctx
-    finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+    ctx.set_coefficients(CoefficientField.isotropic(spec, a))
+    return ctx
 
 
 def _medium(shape, seed):
@@ -55,7 +46,7 @@ def test_cg_matches_oracle_and_generic(shape):
     ref = orc.solve_cg(orc.isotropic_full(a, d), tuple(E[0]), shape, (1.0,) * d, 1e-8, 1000)
     assert reps[0]["iterations"] == ref["iterations"]
     assert rel_l2(x[0], ref["solution"]) < 1e-9
-    rg, xg, _ = _ctx(shape, a, {"FC_FORCE_GENERIC": "1"}).solve_cg(E, 1e-8, 1000)
+    rg, xg, _ = _ctx(shape, a, {"force_generic": 1}).solve_cg(E, 1e-8, 1000)
     assert rg[0]["iterations"] == reps[0]["iterations"]
     assert rel_l2(xg, x) < 1e-12
 

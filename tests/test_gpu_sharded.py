@@ -123,16 +123,16 @@ def test_sharded_generic_lengths(P, rng):
     assert rel_l2(x1[0], ref["solution"]) < 1e-9
 
 
-def test_sharded_forced_generic_matches_register_path(monkeypatch):
-    """FC_FORCE_GENERIC=1 routes a power-of-three grid through the Stockham
+def test_sharded_forced_generic_matches_register_path():
+    """Plan option force_generic routes a power-of-three grid through the Stockham
     kernels; sharded over 3 slabs it must reproduce the register-path solve."""
     a = gen.cfg3_sphere(27)
     E = np.array([[1.0, 0.0, 0.0]])
     reg = _native.Context(a.spec)
     reg.set_coefficients(a)
     r0, x0, _ = reg.solve_cg(E, 1e-8, 500)
-    monkeypatch.setenv("FC_FORCE_GENERIC", "1")
-    gen_many = _native.Context(a.spec, slabs=[0, 0, 0])
+    with _native.plan_options(force_generic=1):
+        gen_many = _native.Context(a.spec, slabs=[0, 0, 0])
     gen_many.set_coefficients(a)
     r1, x1, _ = gen_many.solve_cg(E, 1e-8, 500)
     assert r0[0]["iterations"] == r1[0]["iterations"]
@@ -140,7 +140,7 @@ def test_sharded_forced_generic_matches_register_path(monkeypatch):
 
 
 @pytest.mark.parametrize("P", [2, 4])
-def test_fused_exchange_matches_copy_exchange(P, monkeypatch):
+def test_fused_exchange_matches_copy_exchange(P):
     """Fused exchange (the sweeps store straight into the other slabs' buffers)
     against the copy-engine exchange: same arithmetic, bitwise-identical solve."""
     a = gen.cfg3_sphere(27)
@@ -148,8 +148,8 @@ def test_fused_exchange_matches_copy_exchange(P, monkeypatch):
     fused = _native.Context(a.spec, slabs=[0] * P)
     fused.set_coefficients(a)
     rf, xf, _ = fused.solve_cg(E, 1e-8, 500)
-    monkeypatch.setenv("FC_FUSED_EXCHANGE", "0")
-    copy = _native.Context(a.spec, slabs=[0] * P)
+    with _native.plan_options(fused_exchange=0):
+        copy = _native.Context(a.spec, slabs=[0] * P)
     copy.set_coefficients(a)
     rc, xc, _ = copy.solve_cg(E, 1e-8, 500)
     assert [q["iterations"] for q in rf] == [q["iterations"] for q in rc]
@@ -184,16 +184,16 @@ def test_cfg5_device_generator_matches_host():
 
 
 @pytest.mark.parametrize("max_iter", [5, 500])
-def test_sharded_deferred_x_update_is_bitwise_identical(max_iter, monkeypatch):
+def test_sharded_deferred_x_update_is_bitwise_identical(max_iter):
     """Sharded CG with the x update deferred into the first sweep (default)
-    equals the immediate update (FC_DEFER_X=0) bit for bit, including the
-    flush of RHSs stopped by max_iter."""
+    equals the immediate update (plan option defer_x = 0) bit for bit,
+    including the flush of RHSs stopped by max_iter."""
     a = gen.cfg3_sphere(27)
     E = np.array([[1.0, 0.0, 0.0], [0.2, -0.5, 1.0]])
     _, many = _pair(a.spec, iso=a.isotropic_values, P=3)
-    monkeypatch.setenv("FC_DEFER_X", "1")
     r1, x1, _ = many.solve_cg(E, 1e-8, max_iter)
-    monkeypatch.setenv("FC_DEFER_X", "0")
-    r0, x0, _ = many.solve_cg(E, 1e-8, max_iter)
+    with _native.plan_options(defer_x=0):
+        _, imm = _pair(a.spec, iso=a.isotropic_values, P=3)
+    r0, x0, _ = imm.solve_cg(E, 1e-8, max_iter)
     assert [q["iterations"] for q in r1] == [q["iterations"] for q in r0]
     assert np.array_equal(x1, x0), rel_l2(x1, x0)

@@ -1,16 +1,15 @@
-"""GPU: every kernel variant of the row / outer sweeps gives the same CG solve.
+"""GPU: every kernel variant of the sweeps gives the same CG solve.
 
-The sweeps have alternative implementations selected by environment switches
-read when a context is created (fc_engine.cu): TMA tensor boxes for the
-transposed half spectrum (FC_ROW_TMA), bulk pencil copies in the outer sweep
-(FC_OUTER_TMA), the persistent double-buffered last sweep (FC_INV_PIPE) and
-first sweep (FC_ROW_PIPE).  They perform the same arithmetic in the same order,
-so the batched solve must agree to the last bit with the default path; the
-default path itself is checked against the CPU oracle.  A 243 x 2187 grid has
-one-pencil row blocks (rows of 2187), the case the persistent kernels handle.
+The sweeps have alternative implementations selected by plan options frozen
+into a context at creation (fc_set_plan_option, include/fftcell_b200.h): TMA
+tensor boxes for the transposed half spectrum (row_tma), bulk pencil copies in
+the outer sweep (outer_tma), the persistent double-buffered last sweep
+(inv_pipe), the fused packed first sweep (aniso_fused), the deferred x update
+(defer_x).  They perform the same arithmetic in the same order, so the batched
+solve must agree to the last bit with the default path; the default path
+itself is checked against the CPU oracle.  A 243 x 2187 grid has one-pencil row
+blocks (rows of 2187), the case the persistent kernels handle.
 """
-
-import os
 
 import numpy as np
 import pytest
@@ -35,20 +34,12 @@ def _medium():
     return np.where(smooth > np.quantile(smooth, 0.6), 100.0, 1.0)
 
 
-def _solve(a, env):
-    old = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
-    try:
+def _solve(a, opts):
+    with _native.plan_options(**opts):
         ctx = _native.Context(GridSpec((1.0, 1.0), SHAPE))
-        ctx.set_coefficients(_field(a))
-        reps, x, _ = ctx.solve_cg(LOADS, 1e-8, 1000)
-        return [r["iterations"] for r in reps], x
-    finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+    ctx.set_coefficients(_field(a))
+    reps, x, _ = ctx.solve_cg(LOADS, 1e-8, 1000)
+    return [r["iterations"] for r in reps], x
 
 
 def _field(a):
@@ -75,28 +66,24 @@ def test_default_path_matches_oracle(medium, default_solve):
     assert rel_l2(x[0], ref["solution"]) < 1e-9
 
 
-@pytest.mark.parametrize("env", [
-    {"FC_ROW_TMA": "0"},
-    {"FC_OUTER_TMA": "0"},
-    {"FC_INV_PIPE": "0"},
-    {"FC_ROW_PIPE": "1"},
-    {"FC_ROW_PIPE": "1", "FC_INV_STAGES": "3"},
-    {"FC_INV_QBUF": "0"},
-    {"FC_OUTER_PERSIST": "1"},
-    {"FC_OUTER_C1_2D": "1"},
-    {"FC_DEFER_X": "0"},
-    {"FC_DEFER_X": "0", "FC_ROW_PIPE": "1"},
+@pytest.mark.parametrize("opts", [
+    {"row_tma": 0},
+    {"outer_tma": 0},
+    {"inv_pipe": 0},
+    {"defer_x": 0},
+    {"defer_x": 0, "inv_pipe": 0},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
-def test_variant_is_bitwise_identical(medium, default_solve, env):
+def test_variant_is_bitwise_identical(medium, default_solve, opts):
     its0, x0 = default_solve
-    its, x = _solve(medium, env)
+    its, x = _solve(medium, opts)
     assert its == its0
     assert np.array_equal(x, x0), rel_l2(x, x0)
 
 
 def test_mid_sweep_variants_3d():
-    """3-D: the TMA middle sweep (FC_MID_TMA) and the outer CTA size
-    (FC_OUTER_THREADS) give a bitwise-identical CG solve."""
+    """3-D: the TMA middle sweep (mid_tma), the outer CTA size (outer_threads),
+    the outer bulk copies and the one-component outer sweep give a
+    bitwise-identical CG solve."""
     from paper_1311_0089_b200 import CoefficientField
 
     shape = (81, 81, 81)
@@ -105,98 +92,80 @@ def test_mid_sweep_variants_3d():
     a = np.where(rng.random(shape) < 0.3, 50.0, 1.0)
     coef = CoefficientField.isotropic(spec, a)
 
-    def run(env):
-        old = {k: os.environ.get(k) for k in env}
-        os.environ.update(env)
-        try:
+    def run(opts):
+        with _native.plan_options(**opts):
             ctx = _native.Context(spec)
-            ctx.set_coefficients(coef)
-            reps, x, _ = ctx.solve_cg(np.array([[1.0, 0.0, 0.0]]), 1e-8, 1000)
-            return reps[0]["iterations"], x
-        finally:
-            for k, v in old.items():
-                if v is None:
-                    os.environ.pop(k, None)
-                else:
-                    os.environ[k] = v
+        ctx.set_coefficients(coef)
+        reps, x, _ = ctx.solve_cg(np.array([[1.0, 0.0, 0.0]]), 1e-8, 1000)
+        return reps[0]["iterations"], x
 
     it0, x0 = run({})
-    for env in ({"FC_MID_TMA": "0"}, {"FC_OUTER_THREADS": "256"}, {"FC_OUTER_TMA": "0"}, {"FC_OUTER_SEQ": "1"}):
-        it, x = run(env)
-        assert it == it0, env
-        assert np.array_equal(x, x0), (env, rel_l2(x, x0))
+    for opts in ({"mid_tma": 0}, {"outer_threads": 256}, {"outer_tma": 0}, {"outer_seq": 1}):
+        it, x = run(opts)
+        assert it == it0, opts
+        assert np.array_equal(x, x0), (opts, rel_l2(x, x0))
 
 
-def test_anisotropic_first_sweep_variants():
-    """Packed coefficients: the split first sweep (pointwise kernel + staged row
-    FFT, default) and the all-components fused first sweep (FC_ANISO_SPLIT=0)
-    give a bitwise-identical CG solve."""
+@pytest.mark.parametrize("shape", [(27, 27, 81), (81, 81, 729), (45, 27, 405)])
+def test_anisotropic_first_sweep_variants(shape):
+    """Packed coefficients: the fused first sweep (pointwise step and row FFT of
+    all components in one CTA, default) and the split variant (pointwise kernel
+    writing y, then the staged row FFT; aniso_fused = 0) give a bitwise-identical
+    CG solve and fixed point; rows of 81, 729 (cfg4) and 405 (radix-5)."""
     from conftest import random_spd_packed
     from paper_1311_0089_b200 import CoefficientField
 
-    shape = (27, 27, 81)
     spec = GridSpec((1.0, 1.0, 1.0), shape)
     packed = random_spd_packed(shape, np.random.default_rng(27))
     coef = CoefficientField(spec, packed)
+    E = np.array([[1.0, 0.0, 0.0], [0.0, 0.0, 1.0]])
 
-    def run(env):
-        old = {k: os.environ.get(k) for k in env}
-        os.environ.update(env)
-        try:
+    def run(opts):
+        with _native.plan_options(**opts):
             ctx = _native.Context(spec)
-            ctx.set_coefficients(coef)
-            reps, x, _ = ctx.solve_cg(np.array([[1.0, 0.0, 0.0], [0.0, 0.0, 1.0]]), 1e-8, 1000)
-            return [r["iterations"] for r in reps], x
-        finally:
-            for k, v in old.items():
-                if v is None:
-                    os.environ.pop(k, None)
-                else:
-                    os.environ[k] = v
+        ctx.set_coefficients(coef)
+        reps, x, _ = ctx.solve_cg(E, 1e-8, 1000)
+        A0 = np.diag([4.0, 5.0, 6.0])
+        freps, fx = ctx.solve_fixed_point(E, 1e-6, 40, A0, np.ones(2))
+        return [r["iterations"] for r in reps], x, [r["iterations"] for r in freps], fx
 
-    it0, x0 = run({})
-    it1, x1 = run({"FC_ANISO_SPLIT": "0"})
+    it0, x0, fi0, fx0 = run({})
+    it1, x1, fi1, fx1 = run({"aniso_fused": 0})
     assert it0 == it1
     assert np.array_equal(x0, x1), rel_l2(x1, x0)
+    assert fi0 == fi1
+    assert np.array_equal(fx0, fx1), rel_l2(fx1, fx0)
 
 
-def _env_run(env, fn):
-    old = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
-    try:
+def _opt_run(opts, fn):
+    with _native.plan_options(**opts):
         return fn()
-    finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
 
 
-@pytest.mark.parametrize("case", ["iso2d_3k", "iso2d_generic", "aniso3d", "aniso3d_fused", "line1d"])
+@pytest.mark.parametrize("case", ["iso2d_3k", "iso2d_generic", "aniso3d", "aniso3d_split", "line1d"])
 @pytest.mark.parametrize("max_iter", [4, 1000])
 def test_deferred_x_update_is_bitwise_identical(case, max_iter):
-    """The CG x update deferred into the next first sweep (FC_DEFER_X=1, the
+    """The CG x update deferred into the next first sweep (defer_x = 1, the
     default) and flushed after the loop gives the same solution bits as the
     immediate update in k_cg_update, for RHSs stopping at different iterations,
-    at max_iter, and on every first-sweep kernel (register / generic / split and
-    fused anisotropic / 1-D line)."""
+    at max_iter, and on every first-sweep kernel (register / generic / fused and
+    split anisotropic / 1-D line)."""
     from conftest import random_spd_packed
     from paper_1311_0089_b200 import CoefficientField
 
     rng = np.random.default_rng(7)
-    env = {}
+    opts = {}
     if case == "iso2d_3k":
         shape, loads = (81, 243), np.array([[1.0, 0.0], [0.0, 1.0], [0.6, 0.8]])
         coef_fn = lambda spec: CoefficientField.isotropic(spec, np.where(rng.random(shape) < 0.4, 30.0, 1.0))
     elif case == "iso2d_generic":
         shape, loads = (25, 35), np.array([[1.0, 0.0], [0.0, 1.0]])
         coef_fn = lambda spec: CoefficientField.isotropic(spec, np.where(rng.random(shape) < 0.4, 30.0, 1.0))
-    elif case in ("aniso3d", "aniso3d_fused"):
+    elif case in ("aniso3d", "aniso3d_split"):
         shape, loads = (27, 27, 81), np.array([[1.0, 0.0, 0.0], [0.0, 0.0, 1.0]])
         coef_fn = lambda spec: CoefficientField(spec, random_spd_packed(shape, rng))
-        if case == "aniso3d_fused":
-            env = {"FC_ANISO_SPLIT": "0"}
+        if case == "aniso3d_split":
+            opts = {"aniso_fused": 0}
     else:
         # continuous values: with two phases 1-D CG stops after 2 iterations
         shape, loads = (243,), np.array([[1.0]])
@@ -210,8 +179,8 @@ def test_deferred_x_update_is_bitwise_identical(case, max_iter):
         reps, x, _ = ctx.solve_cg(loads, 1e-8, max_iter)
         return [(r["iterations"], r["converged"]) for r in reps], x
 
-    r1, x1 = _env_run({**env, "FC_DEFER_X": "1"}, run)
-    r0, x0 = _env_run({**env, "FC_DEFER_X": "0"}, run)
+    r1, x1 = _opt_run({**opts, "defer_x": 1}, run)
+    r0, x0 = _opt_run({**opts, "defer_x": 0}, run)
     assert r1 == r0
     assert np.array_equal(x1, x0), rel_l2(x1, x0)
     if max_iter == 4:
@@ -232,7 +201,7 @@ def test_outer_sequential_default_at_243():
         reps, x, _ = ctx.solve_cg(E, 1e-8, 1000)
         return reps[0]["iterations"], x
 
-    i1, x1 = _env_run({}, run)
-    i0, x0 = _env_run({"FC_OUTER_SEQ": "0"}, run)
+    i1, x1 = _opt_run({}, run)
+    i0, x0 = _opt_run({"outer_seq": 0}, run)
     assert i1 == i0 == 52
     assert np.array_equal(x1, x0), rel_l2(x1, x0)

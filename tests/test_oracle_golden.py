@@ -87,3 +87,38 @@ def test_generators_match_survey_statistics():
     assert seeds.shape == (512, 3) and packed.shape == (512, 6)
     lam_min, lam_max = orc.eigen_range(orc.unpack(packed.T, 3), 3)
     assert np.all(lam_min > 0)
+
+
+@pytest.mark.parametrize("name", ["poly27", "generic3d"])
+def test_lean_cg_matches_reference_golden(name):
+    """The memory-lean oracle (oracle/lean_cg.py: packed coefficients, half-spectrum
+    FFT, BLAS dots) that produced the 729^3 anchor reproduces the reference's own
+    solves: identical iteration counts, histories and solutions within the
+    reference's rounding floor (poly27 is the ill-conditioned 27^3 polycrystal)."""
+    from oracle import lean_cg
+
+    g = golden(name)
+    if name == "poly27":
+        shape, Y, E, tol = (27, 27, 27), (1.0, 1.0, 1.0), (1.0, 0.0, 0.0), 1e-8
+    else:
+        shape, Y = tuple(int(s) for s in g["shape"]), tuple(g["Y"])
+        E, tol = (0.3, -1.0, 0.5), 1e-9
+    op = lean_cg.LeanOperator(shape, Y, packed=g["packed"])
+    rep = lean_cg.solve_cg(op, E, tol, 2000)
+    assert rep["iterations"] == int(g["cg_iterations"])
+    h = np.array(rep["history"])
+    ref = g["cg_history"]
+    assert np.max(np.abs(h - ref) / ref[0]) <= max(1e-12, 10 * float(g["cg_floor_hist"]))
+    assert np.max(np.abs(h[:4] - ref[:4]) / ref[0]) <= 1e-13  # the anchor's iterations
+    assert rel_l2(rep["solution"], g["cg_solution"]) <= max(1e-9, 10 * float(g["cg_floor"]))
+
+
+def test_cg_stepper_is_solve_cg():
+    """bench.py's CPU sample (CGStepper) runs exactly solve_cg's iterations."""
+    g = golden("poly27")
+    st = orc.CGStepper(orc.unpack(g["packed"], 3), (1.0, 0.0, 0.0), (27,) * 3, (1.0,) * 3, 1e-8)
+    st.setup()
+    while st.step():
+        pass
+    assert st.iterations == int(g["cg_iterations"])
+    np.testing.assert_array_equal(np.array(st.history), g["cg_history"])
