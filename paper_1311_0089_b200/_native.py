@@ -8,6 +8,7 @@ no CPU fallback: if the library or a CUDA device is missing every call raises
 from __future__ import annotations
 
 import ctypes
+import mmap
 import os
 from pathlib import Path
 
@@ -247,6 +248,8 @@ class Context:
 
     def project(self, which, ref_matrix, u):
         ref = None if ref_matrix is None else _c64(ref_matrix)
+        if ref is not None and ref.shape != (self.d, self.d):
+            raise ValueError(f"reference matrix must be {self.d} x {self.d}, got shape {ref.shape}")
         return self._batched(lib().fc_project, u, which, _ptr(ref))
 
     # -- solvers -----------------------------------------------------------
@@ -265,8 +268,14 @@ class Context:
         hist = np.zeros((R, max_iter + 1))
         its = None
         n_it = ctypes.c_int64(0)
+        its_map = None
         if record_iterates:
-            its = np.empty((max_iter + 1,) + fshape)
+            # room for max_iter + 1 iterates, but only the pages of the iterates
+            # actually written get committed (anonymous MAP_NORESERVE mapping):
+            # host memory scales with the iterations run, like the reference's list
+            nbytes = (max_iter + 1) * int(np.prod(fshape)) * 8
+            its_map = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS | getattr(mmap, "MAP_NORESERVE", 0x4000))
+            its = np.frombuffer(its_map, dtype=np.float64).reshape((max_iter + 1,) + fshape)
         _check(lib().fc_solve_cg(
             self._h, R, _ptr(E), float(tol), int(max_iter), float(lam) if lam is not None else -1.0,
             _ptr(init), _ptr(x), reps, _ptr(hist), _ptr(its), 0 if its is None else its.shape[0],
@@ -276,7 +285,13 @@ class Context:
             rp = reps[r]
             out.append(dict(iterations=rp.iterations, converged=bool(rp.converged), status=rp.status,
                             detail=rp.detail, history=hist[r, :rp.hist_len].copy()))
-        iterates = None if its is None else its[: n_it.value]
+        iterates = None if its is None else its[: n_it.value].copy()
+        if its_map is not None:
+            del its
+            try:
+                its_map.close()
+            except BufferError:  # a view is still referenced: freed with it
+                pass
         return out, x, iterates
 
     def solve_fixed_point(self, E, tol, max_iter, ref_matrix, scale, want_x=True):

@@ -61,6 +61,18 @@ int set_err(int code, const char* fmt, ...) {
     if (rc_ != FC_OK) return rc_; \
   } while (0)
 
+// Scratch device buffer freed on every exit path of the C-ABI call that owns it.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
 struct DevPlan {
   FftPlan plan{};
   double2* roots = nullptr;
@@ -876,7 +888,7 @@ FinArgs fin_args(fc_ctx* c, int mode, int R, int nslot, double tol, int max_iter
   f.max_iter = max_iter;
   f.window = 10;  // solver.py:27
   f.with_init = with_init;
-  f.invN = 1.0 / (double)c->Ng;  // global voxel count (slab-local N differs)
+  f.total = (double)c->Ng;  // global voxel count (slab-local N differs)
   f.any_active = c->d_mapped;  // zero-copy: the host reads it after the iteration's event
   f.counter = c->counter;
   return f;
@@ -1539,7 +1551,7 @@ int32_t fc_energy(fc_ctx* c, int32_t R, const double* E, const double* x, double
   const int nblk = (int)((c->N + chunk - 1) / chunk);
   if ((int64_t)nblk * R * R > c->part_cap) return set_err(FC_ENOTSUP, "partial buffer too small");
   TRY(launch(c, "energy", [&] { k_energy<<<nblk, kThreads, 0, c->stream>>>(g, C, L, R, c->x, c->part, chunk); }));
-  TRY(launch(c, "fin_matrix", [&] { k_fin_matrix<<<1, kThreads, 0, c->stream>>>(c->part, nblk, R * R, 1.0 / (double)c->N, c->d_mat); }));
+  TRY(launch(c, "fin_matrix", [&] { k_fin_matrix<<<1, kThreads, 0, c->stream>>>(c->part, nblk, R * R, (double)c->N, c->d_mat); }));
   CK(cudaMemcpyAsync(out, c->d_mat, sizeof(double) * R * R, cudaMemcpyDeviceToHost, c->stream));
   return sync(c);
 }
@@ -1556,13 +1568,13 @@ int32_t fc_generate_voronoi(fc_ctx* c, int32_t n_seeds, const double* seeds, con
   if (c->dim != 3) return set_err(FC_EINVAL, "the Voronoi generator is three-dimensional");
   if (n_seeds < 1 || n_seeds > 4096) return set_err(FC_EINVAL, "n_seeds must lie in [1, 4096]");
   const int nsym = 6;
-  double *d_seeds = nullptr, *d_packed = nullptr;
-  int* d_lab = nullptr;
-  CK(cudaMalloc(&d_seeds, sizeof(double) * 3 * n_seeds));
-  CK(cudaMalloc(&d_packed, sizeof(double) * nsym * n_seeds));
-  CK(cudaMemcpy(d_seeds, seeds, sizeof(double) * 3 * n_seeds, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(d_packed, packed, sizeof(double) * nsym * n_seeds, cudaMemcpyHostToDevice));
-  if (labels_out) CK(cudaMalloc(&d_lab, sizeof(int) * c->N));
+  DevBuf<double> d_seeds, d_packed;
+  DevBuf<int> d_lab;
+  CK(cudaMalloc(&d_seeds.p, sizeof(double) * 3 * n_seeds));
+  CK(cudaMalloc(&d_packed.p, sizeof(double) * nsym * n_seeds));
+  CK(cudaMemcpy(d_seeds.p, seeds, sizeof(double) * 3 * n_seeds, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_packed.p, packed, sizeof(double) * nsym * n_seeds, cudaMemcpyHostToDevice));
+  if (labels_out) CK(cudaMalloc(&d_lab.p, sizeof(int) * c->N));
   const int64_t count = (int64_t)nsym * c->N;
   if (c->A == nullptr || c->A_count != count) {
     cudaFree(c->A);
@@ -1575,14 +1587,11 @@ int32_t fc_generate_voronoi(fc_ctx* c, int32_t n_seeds, const double* seeds, con
   const size_t sm = sizeof(double) * 3 * n_seeds;
   CK(cudaFuncSetAttribute(k_gen_voronoi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   TRY(launch(c, "gen_voronoi", [&] {
-    k_gen_voronoi<<<blocks, 256, sm, c->stream>>>(c->n0g, c->n[1], c->n[2], c->s0[c->me], n_seeds, d_seeds, d_packed,
-                                                  nsym, c->N, c->A, d_lab);
+    k_gen_voronoi<<<blocks, 256, sm, c->stream>>>(c->n0g, c->n[1], c->n[2], c->s0[c->me], n_seeds, d_seeds.p,
+                                                  d_packed.p, nsym, c->N, c->A, d_lab.p);
   }));
-  if (labels_out) CK(cudaMemcpyAsync(labels_out, d_lab, sizeof(int) * c->N, cudaMemcpyDeviceToHost, c->stream));
+  if (labels_out) CK(cudaMemcpyAsync(labels_out, d_lab.p, sizeof(int) * c->N, cudaMemcpyDeviceToHost, c->stream));
   TRY(sync(c));
-  cudaFree(d_seeds);
-  cudaFree(d_packed);
-  cudaFree(d_lab);
   return FC_OK;
 }
 
@@ -1610,17 +1619,16 @@ int32_t fc_spheres_stamp(fc_ctx* c, int32_t n, const int32_t* centres, double ra
     CK(cudaMemsetAsync(c->sphere_count, 0, sizeof(unsigned long long), c->stream));
   }
   if (n > 0) {
-    int* d_c = nullptr;
-    CK(cudaMalloc(&d_c, sizeof(int) * 3 * n));
-    CK(cudaMemcpyAsync(d_c, centres, sizeof(int) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    DevBuf<int> d_c;
+    CK(cudaMalloc(&d_c.p, sizeof(int) * 3 * n));
+    CK(cudaMemcpyAsync(d_c.p, centres, sizeof(int) * 3 * n, cudaMemcpyHostToDevice, c->stream));
     const int rad = (int)std::ceil(radius);
     const unsigned grid = (unsigned)((int64_t)n * (2 * rad + 1));
     TRY(launch(c, "stamp_spheres", [&] {
-      k_stamp_spheres<<<grid, 256, 0, c->stream>>>(c->n0g, c->n[1], c->n[2], c->s0[c->me], c->n[0], d_c, n, rad,
+      k_stamp_spheres<<<grid, 256, 0, c->stream>>>(c->n0g, c->n[1], c->n[2], c->s0[c->me], c->n[0], d_c.p, n, rad,
                                                    radius * radius, c->sphere_bits, c->sphere_count);
     }));
     TRY(sync(c));
-    cudaFree(d_c);
   }
   unsigned long long k = 0;
   CK(cudaMemcpy(&k, c->sphere_count, sizeof(k), cudaMemcpyDeviceToHost));

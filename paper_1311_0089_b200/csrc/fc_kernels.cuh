@@ -141,7 +141,7 @@ struct FinArgs {
   int max_iter;
   int window;         // fixed-point divergence window (solver.py:27)
   int with_init;      // FIN_INIT: a warm start follows
-  double invN;
+  double total;       // global voxel count |N| (inner products divide by it, solver.py:138-139)
   int* any_active;
   unsigned* counter;  // arrival counter, reset by the last CTA
   double* lsum;       // slab-local mode: per-RHS sums go here, k_fin_global finishes
@@ -530,7 +530,7 @@ __device__ double reduce_slots(const double* part, int n, double* red) {
 // (thread 0 only).  Mirrors solver.py:176-225 and solver.py:264-291.
 __device__ void fin_logic(const FinArgs& f, int r, double sum) {
   RhsState& S = f.st[r];
-  const double q = sum * f.invN;  // float(np.sum(x*y) / total), solver.py:138-139
+  const double q = __ddiv_rn(sum, f.total);  // float(np.sum(x*y) / total), solver.py:138-139
   switch (f.mode) {
     case FIN_INIT:
     case FIN_INIT2: {
@@ -1196,11 +1196,11 @@ __global__ void __launch_bounds__(kThreads) k_energy(Geo g, Coef C, Loads L, int
 
 // ---------------------------------------------------------------------------
 // Energy matrix finalize: out[i] = (sum of slots) / N in fixed order.
-__global__ void k_fin_matrix(const double* part, int nslot, int nval, double invN, double* out) {
+__global__ void k_fin_matrix(const double* part, int nslot, int nval, double total, double* out) {
   __shared__ double red[kThreads / 32];
   for (int i = 0; i < nval; ++i) {
     double s = reduce_slots(part + (int64_t)i * nslot, nslot, red);
-    if (threadIdx.x == 0) out[i] = s * invN;
+    if (threadIdx.x == 0) out[i] = __ddiv_rn(s, total);  // np.sum(...) / total (transforms.py:176)
     __syncthreads();
   }
 }

@@ -26,7 +26,7 @@ from . import _native
 from .green import ReferenceTensor
 from .grid import GridSpec
 from .material import CoefficientField, apply_A  # noqa: F401  (re-export like the reference)
-from .transforms import GridField, l2_norm
+from .transforms import GridField, l2_norm, pairwise_sum_runs
 
 _DIVERGENCE_WINDOW = 10  # solver.py:27 (the device loop uses the same window)
 _METHOD_ALIASES = {"cg": "cg", "neumann": "neumann", "fixed_point": "neumann"}
@@ -95,6 +95,8 @@ class _Projector:
     """
 
     def __init__(self, spec: GridSpec, ref: ReferenceTensor | None = None):
+        if ref is not None and ref.dim != spec.dim:  # the reference's einsum raises here (solver.py:101-104)
+            raise ValueError(f"reference tensor dimension {ref.dim} does not match grid dimension {spec.dim}")
         self.spec = spec
         self.ref = ref
         self._ctx = _native.context_for_spec(spec)
@@ -132,6 +134,8 @@ def _cg_reports(a, loads, cfg, init=None, record_iterates=False, want_solution=T
     if cfg.method != "cg":
         raise ValueError("config method is not 'cg'")
     spec = a.spec
+    if cfg.reference is not None and cfg.reference.dim != spec.dim:  # solver.py:161 builds _Projector(spec, ref)
+        raise ValueError(f"reference tensor dimension {cfg.reference.dim} does not match grid dimension {spec.dim}")
     E = _loads_array(loads, spec)
     lam = None if cfg.reference is None else cfg.reference.scalar_mode
     init_vals = None
@@ -165,11 +169,12 @@ def default_reference(a: CoefficientField) -> ReferenceTensor:
 
 
 def _fp_scale(spec, E):
-    """``max(l2_norm(E_N), tiny)`` (``solver.py:258``), summed like the reference."""
-    if spec.total * spec.dim <= (1 << 24):
-        val = l2_norm(GridField.constant(spec, E))
-    else:
-        val = float(np.sqrt(np.dot(E, E)))
+    """``max(l2_norm(E_N), tiny)`` (``solver.py:258``): the reference's
+    ``np.sum(E_N * E_N) / |N|`` reproduced bit for bit on any grid without
+    expanding E_N (transforms.pairwise_sum_runs)."""
+    E = np.asarray(E, dtype=float)
+    s = pairwise_sum_runs(E * E, [spec.total] * spec.dim)
+    val = float(np.sqrt(max(float(s / spec.total), 0.0)))
     return max(val, np.finfo(float).tiny)
 
 
