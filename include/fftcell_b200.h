@@ -109,6 +109,21 @@ int32_t fc_create_dist(fc_ctx** out, int32_t dim, const int64_t* shape, const do
 /* CoefficientField upload (material.py:90-158): count = N (isotropic) or nsym*N (packed). */
 int32_t fc_set_coefficients(fc_ctx* ctx, int32_t kind, const double* host, int64_t count);
 
+/* Voxel payload straight into HBM (material.py:194-307 format: f64le, row-major,
+ * FFT-shifted, component-major): the .bin file streams through pinned staging
+ * buffers, never held whole on the host; each slab reads only its planes.  The
+ * file must hold exactly (1 or d(d+1)/2) * |N| values (else FC_EINVAL). */
+int32_t fc_load_coefficients(fc_ctx* ctx, int32_t kind, const char* bin_path);
+
+/* c_A / C_A of the device coefficient field (CoefficientField.__post_init__,
+ * material.py:100-123: closed-form eigenvalue range, material.py:52-87) and the
+ * flat index of the first voxel attaining c_A (NULL allowed). */
+int32_t fc_coefficient_bounds(fc_ctx* ctx, double* c_A, double* C_A, int64_t* argmin);
+
+/* The solution of the last solve (nrhs fields (d, *N), the layout of
+ * save_field, material.py:238-239) streamed from HBM into a .bin payload. */
+int32_t fc_save_solution(fc_ctx* ctx, int32_t nrhs, const char* bin_path);
+
 /* apply_A (material.py:182-187): out = A u for nfields fields of shape (d, *N). */
 int32_t fc_apply_A(fc_ctx* ctx, const double* u, double* out, int32_t nfields);
 

@@ -53,6 +53,9 @@ SIGNATURES = [
       ctypes.c_void_p]),
     ("fc_destroy", None, [ctypes.c_void_p]),
     ("fc_set_coefficients", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, _dp, ctypes.c_int64]),
+    ("fc_load_coefficients", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_char_p]),
+    ("fc_coefficient_bounds", ctypes.c_int32, [ctypes.c_void_p, _dp, _dp, _i64p]),
+    ("fc_save_solution", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_char_p]),
     ("fc_apply_A", ctypes.c_int32, [ctypes.c_void_p, _dp, _dp, ctypes.c_int32]),
     ("fc_project", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, _dp, _dp, _dp, ctypes.c_int32]),
     ("fc_apply_system", ctypes.c_int32, [ctypes.c_void_p, _dp, _dp, ctypes.c_int32]),
@@ -202,6 +205,21 @@ class Context:
             kind = 1
         _check(lib().fc_set_coefficients(self._h, kind, _ptr(host), host.size))
         self.isotropic = kind == 0
+
+    def load_coefficients(self, bin_path, kind):
+        """Stream a voxel payload (.bin) into HBM: kind 0 isotropic, 1 packed."""
+        _check(lib().fc_load_coefficients(self._h, int(kind), os.fsencode(str(bin_path))))
+        self.isotropic = kind == 0
+
+    def coefficient_bounds(self):
+        """(c_A, C_A, flat index of the first c_A voxel) of the device field."""
+        lo, hi, at = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        _check(lib().fc_coefficient_bounds(self._h, ctypes.byref(lo), ctypes.byref(hi), ctypes.byref(at)))
+        return lo.value, hi.value, at.value
+
+    def save_solution(self, bin_path, nrhs=1):
+        """Stream the last solve's solution (nrhs, d, *N) from HBM into a .bin payload."""
+        _check(lib().fc_save_solution(self._h, int(nrhs), os.fsencode(str(bin_path))))
 
     def generate_voronoi(self, seeds, packed, want_labels=False):
         """Device-side cfg4 polycrystal (replaces the coefficient field)."""

@@ -898,6 +898,7 @@ FinArgs fin_args(fc_ctx* c, int mode, int R, int nslot, double tol, int max_iter
 
 #include "fc_nccl.inc"
 #include "fc_shard.inc"
+#include "fc_io.inc"
 
 // ===========================================================================
 // C ABI
