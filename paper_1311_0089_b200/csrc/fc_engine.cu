@@ -255,6 +255,7 @@ struct fc_ctx {
   bool dist = false;
   void* comm = nullptr;        // ncclComm_t
   double* gathered = nullptr;  // [P][FC_MAX_RHS] all ranks' local sums (device)
+  double* barrier = nullptr;   // [1 + P] nccl_barrier scratch (device)
 
   SlabMap slabmap(int R) const {
     SlabMap m{};
@@ -288,9 +289,26 @@ struct fc_ctx {
         m.fwd[t] = o->W2r + rf;
         m.ret[t] = o->W2 + rt;
       }
+    } else if (fused && ipc_rcap > 0) {  // same offsets in the peers' buffers mapped through CUDA IPC
+      m.fused = 1;
+      for (int t = 0; t < P; ++t) {
+        long long rf = 0, rt = 0;
+        for (int u = 0; u < me; ++u) {
+          rf += (long long)R * cdim * (qs[t + 1] - qs[t]) * (s0[u + 1] - s0[u]);
+          rt += (long long)R * cdim * (qs[u + 1] - qs[u]) * (s0[t + 1] - s0[t]);
+        }
+        double2* w2 = t == me ? W2 : static_cast<double2*>(ipc_peer[t][0]);
+        double2* w2r = t == me ? W2r : static_cast<double2*>(ipc_peer[t][1]);
+        m.fwd[t] = w2r + rf;
+        m.ret[t] = w2 + rt;
+      }
     }
     return m;
   }
+  // one process per GPU with the fused exchange: the peers' W2 / W2r mapped
+  // into this process (CUDA IPC), opened for workspace capacity ipc_rcap
+  void* ipc_peer[kMaxSlabs][2] = {};
+  int ipc_rcap = 0;
   unsigned* sphere_bits = nullptr;               // cfg5 generator coverage bitmap (fc_spheres_stamp)
   unsigned long long* sphere_count = nullptr;
   int fused = 0;                                 // fused peer-store exchange (in-process slabs)
@@ -1167,10 +1185,16 @@ int32_t fc_create_dist(fc_ctx** out, int32_t dim, const int64_t* shape, const do
     return set_err(FC_ECUDA, "ncclCommInitRank: %s", nccl().errStr(nr));
   }
   c->comm = comm;
-  if (cudaMalloc(&c->gathered, sizeof(double) * FC_MAX_RHS * nranks) != cudaSuccess) {
+  if (cudaMalloc(&c->gathered, sizeof(double) * FC_MAX_RHS * nranks) != cudaSuccess ||
+      cudaMalloc(&c->barrier, sizeof(double) * (1 + nranks)) != cudaSuccess) {
     fc_destroy(c);
     return set_err(FC_ENOMEM, "gather buffer");
   }
+  cudaMemset(c->barrier, 0, sizeof(double) * (1 + nranks));
+  // fused exchange over CUDA IPC mappings of the peers' spectrum buffers (set up
+  // with the workspace, dist_ipc_setup); plan option fused_exchange = 0 keeps
+  // the NCCL send / receive exchange
+  sl->fused = nranks > 1 && sl->opt.fused_exchange;
   *out = c;
   return FC_OK;
 }
@@ -1180,8 +1204,13 @@ void fc_destroy(fc_ctx* c) {
   for (fc_ctx* sl : c->sub) fc_destroy(sl);
   c->sub.clear();
   if (c->device < 0) {  // sharded parent holds no device resources
+    if (c->dist && !c->sub.empty()) {
+      cudaSetDevice(c->sub[0]->device);
+      dist_ipc_close(c);
+    }
     if (c->comm) nccl().commDestroy((ncclComm_t)c->comm);
     cudaFree(c->gathered);
+    cudaFree(c->barrier);
     delete c;
     return;
   }

@@ -845,6 +845,7 @@ __global__ void __launch_bounds__(kThreads) k_mid(Geo g, MidGeo mg, SlabMap sm_,
       const int k1 = idx / nr, row = idx - k1 * nr;
       *send_dst(sm_, dst, (int)rc, k2 * mg.n1 + k1, i00 + row) = res[(size_t)row * ld + k1];
     }
+    if (sm_.fused) __threadfence_system();  // peer stores ordered before the exit
   } else {
     for (int idx = threadIdx.x; idx < nr * mg.n1; idx += blockDim.x) {
       const int row = idx / mg.n1, i1 = idx - row * mg.n1;
@@ -951,6 +952,7 @@ __global__ void __launch_bounds__(kThreads) k_outer(Geo g, OuterGeo og, SlabMap 
       *outer_dst(sm_, W, og.Q, r * c + a, q0 + qq, i0) = s[idx];
     }
   }
+  if (sm_.fused) __threadfence_system();
 }
 
 // d = 1: the whole line in one CTA per RHS (full complex FFT, no pairing).

@@ -471,6 +471,7 @@ __global__ void __launch_bounds__(kMaxBlock) k_mid_r(Geo g, MidGeo mg, SlabMap s
   } else if (!INV) {
 #pragma unroll
     for (int s = 0; s < 9; ++s) *send_dst(sm_, dst, rc, k2 * L + j + s * TP, i00 + p) = v[0][s];
+    if (sm_.fused) __threadfence_system();  // peer stores (other processes' buffers) ordered before the exit
   } else {
     double2* d0 = dst + (((int64_t)rc * mg.n0 + i00 + p) * mg.h2 + k2) * L;
 #pragma unroll
@@ -614,6 +615,7 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
         else W[eoff(i0, r * C + a)] = o[a];
       }
     }
+    if (sm_.fused) __threadfence_system();
     return;
   } else {
   double2 v[C][9];
@@ -704,6 +706,7 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
       else W[eoff(j + s * TP, r * C + a)] = v[a][s];
     }
   }
+  if (sm_.fused) __threadfence_system();
   }  // C == 2
 }
 
