@@ -14,7 +14,9 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libfftcell_b200.so"
+# FC_LIB: an alternative build of the same library (A/B measurements of
+# experimental builds without touching the in-tree one)
+LIB_PATH = Path(os.environ.get("FC_LIB") or Path(__file__).resolve().parent / "libfftcell_b200.so")
 MAX_RHS = 8
 
 FC_OK, FC_EINVAL, FC_ENOMEM, FC_ECUDA, FC_ENOTSUP = 0, 1, 2, 3, 4

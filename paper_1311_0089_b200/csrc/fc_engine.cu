@@ -151,6 +151,9 @@ struct PlanOpts {
   int outer_tma = 1;       // bulk pencil copies in the outer sweep
   int outer_seq = -1;      // d = 3 outer sweep one component at a time (-1: for pencils >= 243)
   int inv_pipe = -1;       // persistent double-buffered last sweep (-1: for one-pencil row blocks)
+  int mid_threads_inv = 0; // inverse middle sweep CTA size (0: 256 for pencils <= 243, else 3 pencils)
+  int mid_map = 1;         // middle sweep transform mapping: 1 lane-fastest, 0 pencil-fastest
+  int mid_tma_fwd = 1;     // forward middle sweep through TMA boxes (0: per-thread transposed stores)
   int aniso_fused = 1;     // packed coefficients: fused first sweep (0: pointwise kernel + row FFT)
   int defer_x = 1;         // CG x update deferred into the next first sweep
   int fused_exchange = 1;  // in-process slabs: sweeps store straight into the peers' buffers
@@ -232,7 +235,9 @@ struct fc_ctx {
   int outer_seq = 0;        // d = 3 outer sweep one component at a time
   CUtensorMap tmW{};        // TMA view of the row-sweep spectrum (RowGeo::tma)
   CUtensorMap tmP{};        // the same for the fused packed first sweep's row blocks (2 pk_npen rows)
-  CUtensorMap tmM{};        // TMA view of the middle sweep's transposed side (MidGeo::tma)
+  CUtensorMap tmM{};        // TMA view of the middle sweep's transposed side (MidGeo::tma), forward tiles
+  CUtensorMap tmMi{};       // the same for the inverse sweep's tiles (mgi)
+  MidGeo mgi{};             // inverse middle sweep tiling (its own pencils per CTA)
   int inv_pipe_blocks = 0;  // persistent double-buffered last sweep: CTAs per SM (0: off)
   int inv_pipe_stage = 0;   // its stage size (complex)
   static constexpr int inv_pipe_nst = 2;   // its stages
@@ -538,23 +543,29 @@ int choose_tiles(fc_ctx* c) {
     }
   }
   if (d == 3 && is_pow3_reg(c->n[1])) {
-    MidGeo& mg = c->mg;
     const int TP = c->n[1] / 9;
-    // 256 threads for 243-point pencils (cfg3: mid_inv -8 %), 512 for longer ones (cfg4: 256 is slower)
-    const int mt = op.mid_threads > 0 ? op.mid_threads : (TP <= 27 ? 256 : 512);
-    int bp = std::max(1, std::min(16, std::min(mt, kMaxBlock) / TP));
-    bp = std::min(bp, c->n[0]);
-    mg.B = bp;
-    mg.nib = (mg.n0 + bp - 1) / bp;
-    c->mid_bp = bp;
-    // TMA boxes on the transposed side: rows * bp a multiple of 8 (128-byte boxes)
     const int L1 = c->n[1];
-    mg.nbox = (L1 + 255) / 256;
-    int rows = (L1 + mg.nbox - 1) / mg.nbox;
-    while ((rows * bp) % 8) ++rows;
-    if (rows > 256) mg.nbox = 0;  // no box shape: per-thread path
-    mg.rows = rows;
-    c->smem_mid_r = (size_t)16 * std::max(bp * L1, mg.nbox * rows * bp);
+    // pencils per CTA: 256 threads for pencils of <= 243 points (cfg3); for 729
+    // (cfg4, TMA on both sides, lane-fastest mapping) 2 pencils forward and 3
+    // inverse measured best (profiles/r02d_ab_mid_cfg4.txt)
+    auto geo = [&](MidGeo& m, int threads) {
+      int bp = std::max(1, std::min(16, std::min(threads, kMaxBlock) / TP));
+      bp = std::min(bp, c->n[0]);
+      m.B = bp;
+      m.nib = (m.n0 + bp - 1) / bp;
+      // TMA boxes on the transposed side: rows * bp a multiple of 8 (128-byte boxes)
+      m.nbox = (L1 + 255) / 256;
+      int rows = (L1 + m.nbox - 1) / m.nbox;
+      while ((rows * bp) % 8) ++rows;
+      if (rows > 256) m.nbox = 0;  // no box shape: per-thread path
+      m.rows = rows;
+      return (size_t)16 * std::max(bp * L1, m.nbox * rows * bp);
+    };
+    const int mtf = op.mid_threads > 0 ? op.mid_threads : (TP <= 27 ? 256 : (c->P > 1 ? 512 : 2 * TP));
+    const int mti = op.mid_threads_inv > 0 ? op.mid_threads_inv : (TP <= 27 ? 256 : 3 * TP);
+    c->mgi = c->mg;
+    c->smem_mid_r = std::max(geo(c->mg, mtf), geo(c->mgi, mti));
+    c->mid_bp = c->mg.B;
   }
   if (is_pow3_reg(c->n0g)) {
     OuterGeo& og = c->og;
@@ -603,7 +614,10 @@ int allow_reg_smem(int mx) {
       al(k_row_inv_r<LL>);
       al(k_mid_r<LL, false>);
       al(k_mid_r<LL, true>);
-      al(k_mid_tma<LL, true>);
+      al(k_mid_tma<LL, true, false>);
+      al(k_mid_tma<LL, true, true>);
+      al(k_mid_tma<LL, false, false>);
+      al(k_mid_tma<LL, false, true>);
       al(k_outer_r<LL, 2>);
       al(k_outer_r<LL, 3>);
       al(k_outer_seq<LL, 3>);
@@ -649,17 +663,19 @@ int make_row_tmap(fc_ctx* c) {
     if (rp != CUDA_SUCCESS) return set_err(FC_ECUDA, "cuTensorMapEncodeTiled (packed first sweep) failed (%d)", (int)rp);
   }
   // middle sweep (d = 3, one slab): W2[rc][k2][k1][i0] as doubles {2 n0, n1, R c h2}
-  MidGeo& mg = c->mg;
-  mg.tma = 0;
-  if (c->dim == 3 && c->mid_bp && c->P == 1 && mg.nbox > 0 && c->opt.mid_tma) {
-    cuuint64_t md[3] = {(cuuint64_t)2 * mg.n0, (cuuint64_t)mg.n1, (cuuint64_t)c->Rcap * c->dim * mg.h2};
-    cuuint64_t ms[2] = {(cuuint64_t)16 * mg.n0, (cuuint64_t)16 * mg.n0 * mg.n1};
-    cuuint32_t mb[3] = {(cuuint32_t)(2 * mg.B), (cuuint32_t)mg.rows, 1};
-    const CUresult rm = encode(&c->tmM, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->W2, md, ms, mb, es,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (rm != CUDA_SUCCESS) return set_err(FC_ECUDA, "cuTensorMapEncodeTiled (middle sweep) failed (%d)", (int)rm);
-    mg.tma = 1;
+  c->mg.tma = c->mgi.tma = 0;
+  if (c->dim == 3 && c->mid_bp && c->P == 1 && c->mg.nbox > 0 && c->mgi.nbox > 0 && c->opt.mid_tma) {
+    for (int k = 0; k < 2; ++k) {
+      MidGeo& mg = k == 0 ? c->mg : c->mgi;
+      cuuint64_t md[3] = {(cuuint64_t)2 * mg.n0, (cuuint64_t)mg.n1, (cuuint64_t)c->Rcap * c->dim * mg.h2};
+      cuuint64_t ms[2] = {(cuuint64_t)16 * mg.n0, (cuuint64_t)16 * mg.n0 * mg.n1};
+      cuuint32_t mb[3] = {(cuuint32_t)(2 * mg.B), (cuuint32_t)mg.rows, 1};
+      const CUresult rm = encode(k == 0 ? &c->tmM : &c->tmMi, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->W2, md, ms, mb,
+                                 es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (rm != CUDA_SUCCESS) return set_err(FC_ECUDA, "cuTensorMapEncodeTiled (middle sweep) failed (%d)", (int)rm);
+      mg.tma = 1;
+    }
   }
   return FC_OK;
 }
@@ -746,13 +762,25 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     const double2* src = inv ? c->W2 : c->W1;
     double2* dst = inv ? c->W1 : c->W2;
     if (c->mid_bp) {
-      const int nt = c->mid_bp * (c->n[1] / 9);
       const double2* tw = c->rtw(c->n[1]);
+      const bool jf = c->opt.mid_map != 0;
+      const MidGeo& mt = inv ? c->mgi : mg;
+      if ((inv || c->opt.mid_tma_fwd) && mt.tma) {
+        // TMA on both sides (bulk pencil copies, tensor boxes on the transposed side)
+        const int nt = mt.B * (c->n[1] / 9);
+        const int64_t nblk = (int64_t)R * d * mt.h2 * mt.nib;
+        const CUtensorMap& tm = inv ? c->tmMi : c->tmM;
+        return launch(c, inv ? "mid_inv" : "mid_fwd", [&] {
+          if (inv && jf) FC_POW3_SWITCH(c->n[1], (k_mid_tma<LL, true, true><<<(unsigned)nblk, nt, c->smem_mid_r, s>>>(g, mt, st, tw, src, dst, tm)))
+          else if (inv) FC_POW3_SWITCH(c->n[1], (k_mid_tma<LL, true, false><<<(unsigned)nblk, nt, c->smem_mid_r, s>>>(g, mt, st, tw, src, dst, tm)))
+          else if (jf) FC_POW3_SWITCH(c->n[1], (k_mid_tma<LL, false, true><<<(unsigned)nblk, nt, c->smem_mid_r, s>>>(g, mt, st, tw, src, dst, tm)))
+          else FC_POW3_SWITCH(c->n[1], (k_mid_tma<LL, false, false><<<(unsigned)nblk, nt, c->smem_mid_r, s>>>(g, mt, st, tw, src, dst, tm)))
+        });
+      }
+      // per-thread transposed side (slab maps of the sharded paths)
+      const int nt = c->mid_bp * (c->n[1] / 9);
       return launch(c, inv ? "mid_inv" : "mid_fwd", [&] {
-        // TMA variant for the inverse direction only (measured: the forward one,
-        // whose transposed side is the store, is not faster than per-thread stores)
-        if (inv && mg.tma) FC_POW3_SWITCH(c->n[1], (k_mid_tma<LL, true><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, st, tw, src, dst, c->tmM)))
-        else if (inv) FC_POW3_SWITCH(c->n[1], (k_mid_r<LL, true><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, smap, st, tw, src, dst)))
+        if (inv) FC_POW3_SWITCH(c->n[1], (k_mid_r<LL, true><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, smap, st, tw, src, dst)))
         else FC_POW3_SWITCH(c->n[1], (k_mid_r<LL, false><<<(unsigned)nmid, nt, c->smem_mid_r, s>>>(g, mg, smap, st, tw, src, dst)))
       });
     }
@@ -944,7 +972,8 @@ int32_t fc_set_plan_option(const char* key, int32_t value) {
       {"outer_threads", &o.outer_threads}, {"row_tma", &o.row_tma}, {"mid_tma", &o.mid_tma},
       {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"inv_pipe", &o.inv_pipe},
       {"aniso_fused", &o.aniso_fused}, {"defer_x", &o.defer_x}, {"fused_exchange", &o.fused_exchange},
-      {"sync_debug", &o.sync_debug}};
+      {"sync_debug", &o.sync_debug}, {"mid_threads_inv", &o.mid_threads_inv}, {"mid_map", &o.mid_map},
+      {"mid_tma_fwd", &o.mid_tma_fwd}};
   for (const auto& t : table)
     if (std::strcmp(t.name, key) == 0) {
       *t.field = value;

@@ -357,7 +357,10 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
 // contiguous row of L modes per i0): one bulk copy per pencil.  Transposed side
 // (W2[rc][k2][k1][i0]): tensor boxes {2 BP doubles, rows modes} = BP consecutive
 // i0 for rows consecutive k1, landing in smem as [k1][p].
-template <int L, bool INV>
+// JF: thread mapping of the transform, pencil-fastest (p = t % BP: the
+// transposed shared-memory side is conflict-free) or lane-fastest (p = t / TP:
+// the exchanges inside the FFT are conflict-free).
+template <int L, bool INV, bool JF>
 __device__ __forceinline__ void mid_tma(const Geo& g, const MidGeo& mg, const RhsState* st,
                                         const double2* __restrict__ tw, const double2* __restrict__ src,
                                         double2* __restrict__ dst, const CUtensorMap& tmM, double2* sm) {
@@ -370,8 +373,8 @@ __device__ __forceinline__ void mid_tma(const Geo& g, const MidGeo& mg, const Rh
   const int r = (int)(bid / c);
   if (!rhs_active(st, r)) return;
   const int BP = mg.B;
-  const int p = threadIdx.x % BP;
-  const int j = threadIdx.x / BP;
+  const int p = JF ? threadIdx.x / TP : threadIdx.x % BP;
+  const int j = JF ? threadIdx.x - p * TP : threadIdx.x / BP;
   const int i00 = ib * BP;
   const int np_ = min(BP, mg.n0 - i00);  // live pencils
   const int rc = r * c + a;
@@ -419,12 +422,12 @@ __device__ __forceinline__ void mid_tma(const Geo& g, const MidGeo& mg, const Rh
   }
 }
 
-template <int L, bool INV>
+template <int L, bool INV, bool JF>
 __global__ void __launch_bounds__(kMaxBlock) k_mid_tma(Geo g, MidGeo mg, const RhsState* st,
                                                         const double2* __restrict__ tw, const double2* __restrict__ src,
                                                         double2* __restrict__ dst, const __grid_constant__ CUtensorMap tmM) {
   extern __shared__ __align__(128) unsigned char smraw[];
-  mid_tma<L, INV>(g, mg, st, tw, src, dst, tmM, reinterpret_cast<double2*>(smraw));
+  mid_tma<L, INV, JF>(g, mg, st, tw, src, dst, tmM, reinterpret_cast<double2*>(smraw));
 }
 
 // Middle sweep (d = 3), thread mapping pencil-fastest (t = j * BP + p) so the

@@ -80,13 +80,14 @@ def test_variant_is_bitwise_identical(medium, default_solve, opts):
     assert np.array_equal(x, x0), rel_l2(x, x0)
 
 
-def test_mid_sweep_variants_3d():
-    """3-D: the TMA middle sweep (mid_tma), the outer CTA size (outer_threads),
-    the outer bulk copies and the one-component outer sweep give a
-    bitwise-identical CG solve."""
+@pytest.mark.parametrize("shape", [(81, 81, 81), (27, 729, 45)])
+def test_mid_sweep_variants_3d(shape):
+    """3-D: the TMA middle sweeps (mid_tma, mid_tma_fwd), their thread mapping
+    (mid_map) and CTA sizes (mid_threads, mid_threads_inv), the outer CTA size
+    (outer_threads), the outer bulk copies and the one-component outer sweep
+    give a bitwise-identical CG solve."""
     from paper_1311_0089_b200 import CoefficientField
 
-    shape = (81, 81, 81)
     spec = GridSpec((1.0, 1.0, 1.0), shape)
     rng = np.random.default_rng(81)
     a = np.where(rng.random(shape) < 0.3, 50.0, 1.0)
@@ -100,7 +101,9 @@ def test_mid_sweep_variants_3d():
         return reps[0]["iterations"], x
 
     it0, x0 = run({})
-    for opts in ({"mid_tma": 0}, {"outer_threads": 256}, {"outer_tma": 0}, {"outer_seq": 1}):
+    for opts in ({"mid_tma": 0}, {"outer_threads": 256}, {"outer_tma": 0}, {"outer_seq": 1}, {"mid_map": 0},
+                 {"mid_tma_fwd": 0}, {"mid_map": 0, "mid_tma_fwd": 0}, {"mid_threads": 512, "mid_threads_inv": 512},
+                 {"mid_threads": 81, "mid_threads_inv": 162}):
         it, x = run(opts)
         assert it == it0, opts
         assert np.array_equal(x, x0), (opts, rel_l2(x, x0))

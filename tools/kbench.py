@@ -30,13 +30,4 @@ for _ in range(reps):
     ctx.apply_system(u)
 ctx.set_profiling(False)
 prof = ctx.profile()
-out = {}
-for k, (cnt, ms) in prof.items():
-    avg = ms / cnt
-    kb = wl.kernel_bytes(k)
-    if k == "row_fwd":
-        kb = 8 * wl.N * (wl.nA + 2 * wl.d * wl.R)   # operator-only first sweep: read u (+A), write spectrum
-    if k == "row_inv":
-        kb = 8 * wl.N * 2 * wl.d * wl.R             # read spectrum, write out
-    out[k] = (round(avg, 4), round(kb / (avg / 1e3) / 1e9) if kb else None)
-print(name, wl.shape, out)
+print(name, wl.shape, {k: round(ms / cnt, 4) for k, (cnt, ms) in prof.items()})
