@@ -26,6 +26,7 @@
 #include "fc_kernels_reg.cuh"
 #include "fc_kernels_pipe.cuh"
 #include "fc_kernels_pk.cuh"
+#include "fc_kernels_fat.cuh"
 
 // Field allocations carry this many spare bytes: 16-byte-aligned bulk copies
 // (fc_tma.cuh) of a row block may read up to 8 bytes past its last element.
@@ -77,6 +78,7 @@ struct DevPlan {
   FftPlan plan{};
   double2* roots = nullptr;
   double2* rtw = nullptr;  // register-FFT twiddle table (L = 3^k only)
+  double2* ftw = nullptr;  // fat-thread FFT twiddle table (fc_fft_fat.cuh)
 };
 
 // register-path lengths (fc_fft_reg.cuh): 3^k for 9..2187 and 5 * 3^k for 45..1215
@@ -107,6 +109,23 @@ std::vector<double2> reg_twiddles(int L, const std::vector<double2>& roots) {
   if (tail)
     for (int r = 1; r < 3; ++r)
       for (int b = 0; b < L / 3; ++b) tw.push_back(roots[(int64_t)b * r % L]);
+  if (tw.empty()) tw.push_back(make_double2(1.0, 0.0));
+  return tw;
+}
+
+// Twiddle table of the fat-thread transform (layout: R27 in fc_fft_fat.cuh).
+std::vector<double2> fat_twiddles(int L, const std::vector<double2>& roots) {
+  int K = 0;
+  for (int t = L; t > 1; t /= 3) ++K;
+  const int NP = K / 3;
+  const int T = K % 3 == 0 ? 1 : (K % 3 == 1 ? 3 : 9);
+  std::vector<double2> tw;
+  if (NP >= 2)
+    for (int r = 1; r < 27; ++r)
+      for (int k = 0; k < 27; ++k) tw.push_back(roots[(int64_t)k * r * (L / 729) % L]);
+  if (T > 1)
+    for (int q = 1; q < T; ++q)
+      for (int b = 0; b < L / T; ++b) tw.push_back(roots[(int64_t)b * q % L]);
   if (tw.empty()) tw.push_back(make_double2(1.0, 0.0));
   return tw;
 }
@@ -155,6 +174,9 @@ struct PlanOpts {
   int mid_map = 1;         // middle sweep transform mapping: 1 lane-fastest, 0 pencil-fastest
   int mid_tma_fwd = 1;     // forward middle sweep through TMA boxes (0: per-thread transposed stores)
   int aniso_fused = 1;     // packed coefficients: fused first sweep (0: pointwise kernel + row FFT)
+  int inv_qpre = 1;        // last sweep: epilogue input staged by a bulk copy issued with the spectrum loads
+  int fin_split = -1;      // reductions finalized by a separate launch (-1: from 1024 partial slots on)
+  int outer_fat = 0;       // outer sweep on the fat-thread FFT (27 values per thread, warp-owned pencils)
   int defer_x = 1;         // CG x update deferred into the next first sweep
   int fused_exchange = 1;  // in-process slabs: sweeps store straight into the peers' buffers
   int sync_debug = 0;      // synchronize after every launch (error attribution)
@@ -190,6 +212,7 @@ struct fc_ctx {
   double2 *W1 = nullptr, *W2 = nullptr;
   double* part = nullptr;
   int64_t part_cap = 0;
+  double* part2 = nullptr;  // chunk sums of the split finalize (kFinChunks x FC_MAX_RHS)
   RhsState* st = nullptr;
   double* hist = nullptr;
   int* any_active = nullptr;
@@ -228,6 +251,7 @@ struct fc_ctx {
   Coef coef() const { return Coef{A, coef_kind}; }
   const FftPlan& plan(int L) const { return plans.at(L).plan; }
   const double2* rtw(int L) const { return plans.at(L).rtw; }
+  const double2* ftw(int L) const { return plans.at(L).ftw; }
   // register-path tiling per sweep (0 = generic path)
   int row_npen = 0, mid_bp = 0, outer_qb = 0;
   int pk_npen = 0;          // fused packed-coefficient first sweep: pencils per component (0: split)
@@ -439,6 +463,11 @@ int ensure_plan(fc_ctx* c, int L) {
     CK(cudaMalloc(&dp.rtw, sizeof(double2) * tw.size()));
     CK(cudaMemcpy(dp.rtw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
   }
+  if (fc::is_fat_len(L) && !c->force_generic) {
+    std::vector<double2> tw = fat_twiddles(L, roots);
+    CK(cudaMalloc(&dp.ftw, sizeof(double2) * tw.size()));
+    CK(cudaMemcpy(dp.ftw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
+  }
   c->plans[L] = dp;
   return FC_OK;
 }
@@ -531,6 +560,17 @@ int choose_tiles(fc_ctx* c) {
     const size_t ybytes = (size_t)16 * rg.nbox * rg.boxK * 2 * npen;
     c->smem_row_r = std::max(c->smem_row_r, (size_t)16 * (((size_t)npen * rg.nl + 7) & ~(size_t)7) + ybytes);
     c->smem_row_inv_r = std::max((size_t)16 * npen * (rg.nl + 1), ybytes);
+    // last sweep: the epilogue input (p / e of the row block) staged behind the
+    // spectrum by a bulk copy, if three CTAs still fit an SM
+    rg.qoff = 0;
+    if (op.inv_qpre) {
+      const size_t qoff = (c->smem_row_inv_r + 127) & ~(size_t)127;
+      const size_t tot = qoff + (size_t)8 * (2 * npen * rg.nl + 2);
+      if (3 * (tot + 1024) <= (size_t)c->smem_optin + 1024) {
+        rg.qoff = (int)qoff;
+        c->smem_row_inv_r = tot;
+      }
+    }
     // packed coefficients: fused first sweep (fc_kernels_pk.cuh), d components of
     // npk pencils per CTA (<= 256 threads), if two CTAs fit an SM
     if (op.aniso_fused && d >= 2) {
@@ -603,6 +643,16 @@ int choose_tiles(fc_ctx* c) {
     default: break;                      \
   }
 
+#define FC_FAT_SWITCH(L, ...)          \
+  switch (L) {                           \
+    case 27: { constexpr int LL = 27; __VA_ARGS__; } break;     \
+    case 81: { constexpr int LL = 81; __VA_ARGS__; } break;     \
+    case 243: { constexpr int LL = 243; __VA_ARGS__; } break;   \
+    case 729: { constexpr int LL = 729; __VA_ARGS__; } break;   \
+    case 2187: { constexpr int LL = 2187; __VA_ARGS__; } break; \
+    default: break;                      \
+  }
+
 int allow_reg_smem(int mx) {
   int rc = FC_OK;
   auto al = [&](auto k) { if (rc == FC_OK) rc = allow_smem(k, mx); };
@@ -621,6 +671,12 @@ int allow_reg_smem(int mx) {
       al(k_outer_r<LL, 2>);
       al(k_outer_r<LL, 3>);
       al(k_outer_seq<LL, 3>);
+    });
+  }
+  for (int L : {27, 81, 243, 729, 2187}) {
+    FC_FAT_SWITCH(L, {
+      al(k_outer_fat<LL, 2>);
+      al(k_outer_fat<LL, 3>);
     });
   }
   return rc;
@@ -736,6 +792,25 @@ int ensure_workspace(fc_ctx* c, int R, int hcap) {
 int64_t nslot_row(const fc_ctx* c) { return c->dim == 1 ? 1 : (int64_t)c->rg.no * c->rg.ntiles * c->dim; }
 int64_t nslot_vec(const fc_ctx* c) { return ((int64_t)c->dim * c->N + kVecTile - 1) / kVecTile; }
 
+// Reducing launches on large grids hand their finalize to k_fin_split: returns
+// the FinArgs the reducing kernel should get (FIN_NONE when split).
+constexpr int kFinChunks = 128;
+bool fin_is_split(const fc_ctx* c, const FinArgs& f) {
+  if (f.mode == FIN_NONE || f.part == nullptr) return false;
+  return c->opt.fin_split >= 0 ? c->opt.fin_split != 0 : f.nslot >= 1024;
+}
+FinArgs fin_for_kernel(const fc_ctx* c, const FinArgs& f) {
+  FinArgs k = f;
+  if (fin_is_split(c, f)) k.mode = FIN_NONE;
+  return k;
+}
+int launch_fin_split(fc_ctx* c, const FinArgs& f) {
+  if (!fin_is_split(c, f)) return FC_OK;
+  if (c->part2 == nullptr) CK(cudaMalloc(&c->part2, sizeof(double) * kFinChunks * FC_MAX_RHS));
+  const int G = std::max(1, std::min(kFinChunks, f.nslot / 2048));
+  return launch(c, "finalize", [&] { k_fin_split<<<dim3(G, f.R), 256, 0, c->stream>>>(f, c->part2, G); });
+}
+
 // One operator application over R fields, in three phases so a sharded run can
 // exchange spectra between them: 0 = first sweep (+ forward middle sweep),
 // 1 = outer sweep (Gamma_hat), 2 = inverse middle sweep + last sweep.
@@ -837,7 +912,19 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
       for (int b = 0; b < 3; ++b) og.M[a][b] = M[a][b];
     double2* Wout = c->P > 1 ? c->W2r : c->W2;
     og.R = R;
-    if (c->outer_qb && c->outer_seq && c->P == 1 && og.tma) {
+    if (c->opt.outer_fat && c->P == 1 && !c->force_generic && fc::is_fat_len(c->n0g)) {
+      // fat-thread transform, warp-owned pencils (fc_kernels_fat.cuh)
+      const double2* tw = c->ftw(c->n0g);
+      TRY(launch(c, "outer", [&] {
+        FC_FAT_SWITCH(c->n0g, {
+          constexpr int per = (kFatThreads / FatGeo<LL>::GT) * FatGeo<LL>::PPG;  // pencils per CTA
+          const dim3 grid((unsigned)((og.Q + per - 1) / per), R);
+          const size_t smem = (kFatThreads / FatGeo<LL>::GT) * FatGeo<LL>::group_bytes;
+          if (d == 2) k_outer_fat<LL, 2><<<grid, kFatThreads, smem, s>>>(g, og, st, tw, Wout);
+          else k_outer_fat<LL, 3><<<grid, kFatThreads, smem, s>>>(g, og, st, tw, Wout);
+        })
+      }));
+    } else if (c->outer_qb && c->outer_seq && c->P == 1 && og.tma) {
       const int nt = c->outer_qb * (c->n0g / 9);
       const double2* tw = c->rtw(c->n0g);
       TRY(launch(c, "outer", [&] {
@@ -859,6 +946,10 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
   }
   if (!(phases & PH_INV)) return FC_OK;
   if (d == 3) TRY(mid(true));
+  // large grids: the last sweep only stores its partials, a separate launch finalizes
+  const FinArgs fin_full = ea.fin;
+  ea.fin = fin_for_kernel(c, fin_full);
+  auto last_sweep = [&]() -> int {
   if (c->row_npen && c->rg.tma && c->inv_pipe_blocks > 0) {
     const int nt = c->row_npen * (rg.nl / 9);
     const double2* tw = c->rtw(rg.nl);
@@ -882,6 +973,9 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
   return launch(c, "row_inv", [&] {
     k_row_inv<<<(unsigned)nrow_blocks, kThreads, c->smem_row, s>>>(g, rg, ea, st, pl_last, Wrow);
   });
+  };
+  TRY(last_sweep());
+  return launch_fin_split(c, fin_full);
 }
 
 int run_operator(fc_ctx* c, int R, const InArgs& ia, EpArgs ea, int orth, const double M[3][3], const RhsState* st) {
@@ -970,7 +1064,7 @@ int32_t fc_set_plan_option(const char* key, int32_t value) {
   const struct { const char* name; int* field; } table[] = {
       {"force_generic", &o.force_generic}, {"row_threads", &o.row_threads}, {"mid_threads", &o.mid_threads},
       {"outer_threads", &o.outer_threads}, {"row_tma", &o.row_tma}, {"mid_tma", &o.mid_tma},
-      {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"inv_pipe", &o.inv_pipe},
+      {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"inv_pipe", &o.inv_pipe}, {"inv_qpre", &o.inv_qpre}, {"fin_split", &o.fin_split}, {"outer_fat", &o.outer_fat},
       {"aniso_fused", &o.aniso_fused}, {"defer_x", &o.defer_x}, {"fused_exchange", &o.fused_exchange},
       {"sync_debug", &o.sync_debug}, {"mid_threads_inv", &o.mid_threads_inv}, {"mid_map", &o.mid_map},
       {"mid_tma_fwd", &o.mid_tma_fwd}};
@@ -1248,6 +1342,7 @@ void fc_destroy(fc_ctx* c) {
   for (auto& kv : c->plans) {
     cudaFree(kv.second.roots);
     cudaFree(kv.second.rtw);
+    cudaFree(kv.second.ftw);
   }
   for (double* q : {c->xi, c->A, c->x, c->r, c->p[0], c->p[1], c->Ap, c->part, c->hist, c->d_mat}) cudaFree(q);
   cudaFree(c->W1);
@@ -1255,6 +1350,7 @@ void fc_destroy(fc_ctx* c) {
   cudaFree(c->st);
   cudaFree(c->any_active);
   cudaFree(c->counter);
+  cudaFree(c->part2);
   cudaFree(c->lsum);
   cudaFree(c->W2r);
   cudaFree(c->sphere_bits);
@@ -1461,10 +1557,12 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
     TRY(run_operator(c, R, ia, ea, orth, M, c->st));
     dim3 grid(nvec, R);
     FinArgs fb = fin_args(c, FIN_BETA, R, nvec, tol, max_iter);
+    const FinArgs fbk = fin_for_kernel(c, fb);
     TRY(launch(c, "cg_update", [&] {
       k_cg_update<<<grid, kThreads, 0, s>>>((int64_t)d * c->N, c->st, defer ? nullptr : c->x, c->r, pcur, c->Ap,
-                                            c->part, nvec, fb);
+                                            c->part, nvec, fbk);
     }));
+    TRY(launch_fin_split(c, fb));
     // the flag is monotone (an inactive RHS never reactivates), so reading a
     // later iteration's value is always a valid stop decision
     const int slot = it & 3;

@@ -686,6 +686,55 @@ __global__ void k_fin_global(FinArgs f, SlabSums ss) {
   *f.any_active = any;
 }
 
+// Split finalize for large grids: the reducing kernel only stores its partials
+// (FIN_NONE: no per-CTA fence + atomic round trip while the CTA holds its
+// shared memory), then this launch sums them in a fixed two-level order -- G
+// chunks per right-hand side, each by one CTA (thread-strided, four
+// accumulators, the fixed block tree), the chunk sums in chunk order by the
+// last CTA to arrive -- and runs the same scalar logic as finalize_block.
+__global__ void __launch_bounds__(256) k_fin_split(FinArgs f, double* part2, int G) {
+  __shared__ double red[256 / 32];
+  __shared__ int last;
+  const int r = blockIdx.y, gi = blockIdx.x;
+  const bool init = f.mode == FIN_INIT || f.mode == FIN_INIT2;
+  if (init || f.st[r].active) {
+    const int64_t chunk = ((int64_t)f.nslot + G - 1) / G;
+    const int64_t i0 = gi * chunk, i1 = min((int64_t)f.nslot, i0 + chunk);
+    const double* p = f.part + (int64_t)r * f.nslot;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t i = i0 + threadIdx.x;
+    for (; i + 768 < i1; i += 1024) {
+      a0 += __ldcg(p + i);
+      a1 += __ldcg(p + i + 256);
+      a2 += __ldcg(p + i + 512);
+      a3 += __ldcg(p + i + 768);
+    }
+    for (; i < i1; i += 256) a0 += __ldcg(p + i);
+    const double sum = block_sum((a0 + a1) + (a2 + a3), red);
+    if (threadIdx.x == 0) part2[r * G + gi] = sum;
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(f.counter, 1u) == gridDim.x * gridDim.y - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  for (int q = 0; q < f.R; ++q) {
+    if (!init && !f.st[q].active) continue;
+    double sum = 0.0;
+    for (int t = 0; t < G; ++t) sum += __ldcg(part2 + q * G + t);
+    if (f.lsum) f.lsum[q] = sum;  // slab-local: the global finalize runs in k_fin_global
+    else fin_logic(f, q, sum);
+  }
+  if (!f.lsum) {
+    int any = 0;
+    for (int q = 0; q < f.R; ++q) any |= f.st[q].active;
+    *f.any_active = any;
+  }
+  *f.counter = 0u;
+}
+
 // Row-sweep geometry: rows of length nl along the contiguous axis, grouped in
 // blocks of B consecutive rows of the previous axis (length np), for each
 // outer index o < no (d = 3: o = i0; d = 2: no = 1).
@@ -693,6 +742,7 @@ struct RowGeo {
   int nl, hl, np, no, B, ntiles;
   int tma = 0;      // transposed spectrum moved by TMA boxes {2B doubles, boxK modes} (fc_tma.cuh)
   int boxK = 0, nbox = 0;
+  int qoff = 0;     // last sweep: byte offset of the epilogue-input staging area (0: per-thread loads after the FFT)
 };
 
 // ---------------------------------------------------------------------------

@@ -252,16 +252,26 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   // epilogue input (p for EP_AP, e for EP_FP), read in the epilogue
   const bool need_q = ea.mode == EP_AP || ea.mode == EP_FP;
   const double* qsrc = (ea.mode == EP_AP ? ea.p : ea.out) + ebase;
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, barq;
   // Y staged at sm[k * yk + row * yr]: TMA boxes give [k][row], the fallback [row][k]
   const int yk = rg.tma ? rg.B : 1;
   const int yr = rg.tma ? 1 : hl;
+  // epilogue input staged by one bulk copy issued with the spectrum loads, so it
+  // lands during the transform instead of after it (the rows of a block are contiguous)
+  const bool qpre = need_q && rg.tma && rg.qoff > 0;
+  const int qsh = qpre ? bulk_shift(qsrc) : 0;
+  const double* Q = reinterpret_cast<const double*>(smraw + rg.qoff) + qsh;
   if (rg.tma) {
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
+      if (qpre) mbar_init(&barq, 1);
       mbar_expect_tx(&bar, (unsigned)(rg.nbox * rg.boxK * rg.B * 16));
       const int c2 = (r * c + a) * rg.no + o;
       for (int b = 0; b < rg.nbox; ++b) tma_load_3d(sm + (size_t)b * rg.boxK * rg.B, &tmW, 2 * row0, b * rg.boxK, c2, &bar);
+      if (qpre) {
+        mbar_expect_tx(&barq, bulk_bytes(nrows * L, qsh));
+        bulk_g2s(smraw + rg.qoff, qsrc - qsh, bulk_bytes(nrows * L, qsh), &barq);
+      }
     }
     __syncthreads();
     mbar_wait(&bar, 0);
@@ -313,7 +323,15 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   const double Ea = ea.mode == EP_FP ? pick(ea.E, r, a) : 0.0;
   const bool he = re < nrows;
   double2 q[9];
-  if (need_q) {
+  if (qpre) {
+    mbar_wait(&barq, 0);
+#pragma unroll
+    for (int s = 0; s < 9; ++s) {
+      const int i = j + s * TP;
+      q[s].x = he ? Q[re * L + i] : 0.0;
+      q[s].y = has_o ? Q[ro * L + i] : 0.0;
+    }
+  } else if (need_q) {
 #pragma unroll
     for (int s = 0; s < 9; ++s) {
       const int i = j + s * TP;
