@@ -177,6 +177,7 @@ struct PlanOpts {
   int inv_qpre = 1;        // last sweep: epilogue input staged by a bulk copy issued with the spectrum loads
   int fin_split = -1;      // reductions finalized by a separate launch (-1: from 1024 partial slots on)
   int outer_fat = 0;       // outer sweep on the fat-thread FFT (27 values per thread, warp-owned pencils)
+  int outer_direct = 0;    // d = 3 outer sweep without staging (k_outer_dir)
   int defer_x = 1;         // CG x update deferred into the next first sweep
   int fused_exchange = 1;  // in-process slabs: sweeps store straight into the peers' buffers
   int sync_debug = 0;      // synchronize after every launch (error attribution)
@@ -671,6 +672,7 @@ int allow_reg_smem(int mx) {
       al(k_outer_r<LL, 2>);
       al(k_outer_r<LL, 3>);
       al(k_outer_seq<LL, 3>);
+      al(k_outer_dir<LL>);
     });
   }
   for (int L : {27, 81, 243, 729, 2187}) {
@@ -924,6 +926,13 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
           else k_outer_fat<LL, 3><<<grid, kFatThreads, smem, s>>>(g, og, st, tw, Wout);
         })
       }));
+    } else if (c->outer_qb && c->opt.outer_direct && d == 3 && c->P == 1) {
+      const int nt = c->outer_qb * (c->n0g / 9);
+      const double2* tw = c->rtw(c->n0g);
+      const size_t smem = (size_t)32 * c->outer_qb * c->n0g;
+      TRY(launch(c, "outer", [&] {
+        FC_POW3_SWITCH(c->n0g, (k_outer_dir<LL><<<(unsigned)(R * og.nqb), nt, smem, s>>>(g, og, st, tw, Wout)))
+      }));
     } else if (c->outer_qb && c->outer_seq && c->P == 1 && og.tma) {
       const int nt = c->outer_qb * (c->n0g / 9);
       const double2* tw = c->rtw(c->n0g);
@@ -1064,7 +1073,7 @@ int32_t fc_set_plan_option(const char* key, int32_t value) {
   const struct { const char* name; int* field; } table[] = {
       {"force_generic", &o.force_generic}, {"row_threads", &o.row_threads}, {"mid_threads", &o.mid_threads},
       {"outer_threads", &o.outer_threads}, {"row_tma", &o.row_tma}, {"mid_tma", &o.mid_tma},
-      {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"inv_pipe", &o.inv_pipe}, {"inv_qpre", &o.inv_qpre}, {"fin_split", &o.fin_split}, {"outer_fat", &o.outer_fat},
+      {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"inv_pipe", &o.inv_pipe}, {"inv_qpre", &o.inv_qpre}, {"fin_split", &o.fin_split}, {"outer_fat", &o.outer_fat}, {"outer_direct", &o.outer_direct},
       {"aniso_fused", &o.aniso_fused}, {"defer_x", &o.defer_x}, {"fused_exchange", &o.fused_exchange},
       {"sync_debug", &o.sync_debug}, {"mid_threads_inv", &o.mid_threads_inv}, {"mid_map", &o.mid_map},
       {"mid_tma_fwd", &o.mid_tma_fwd}};
@@ -1075,6 +1084,14 @@ int32_t fc_set_plan_option(const char* key, int32_t value) {
     }
   return set_err(FC_EINVAL, "unknown plan option '%s'", key);
 }
+
+#ifdef FC_TRACE
+int32_t fc_debug_trace(unsigned long long* out, int32_t n) {
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyFromSymbol(out, fc::g_trace, sizeof(unsigned long long) * n));
+  return FC_OK;
+}
+#endif
 
 int32_t fc_reset_plan_options(void) {
   g_plan_opts = PlanOpts{};

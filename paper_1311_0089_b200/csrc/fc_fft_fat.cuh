@@ -114,27 +114,62 @@ struct SyncGroup {  // named barrier `id` over n threads (n a multiple of 32)
   __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 };
 
+// Exchange through the group's buffer: v[r] -> position wbase + r wstride, then
+// v[s] <- position j + s TP.  HALF: real and imaginary parts go through one
+// after the other, so the buffer holds L doubles instead of L complex (the
+// 8-byte accesses are conflict-free for the same strides).
+template <int L, bool HALF, typename Sync>
+__device__ __forceinline__ void fat_exchange(double2 (&v)[27], double2* sm, int wbase, int wstride, int j, bool act,
+                                             const Sync& sync) {
+  constexpr int TP = R27<L>::TP;
+  if constexpr (!HALF) {
+    sync();  // earlier readers of sm are done
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < 27; ++r) sm[wbase + r * wstride] = v[r];
+    }
+    sync();
+    if (act) {
+#pragma unroll
+      for (int s = 0; s < 27; ++s) v[s] = sm[j + s * TP];
+    }
+  } else {
+    double* sd = reinterpret_cast<double*>(sm);
+    sync();
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < 27; ++r) sd[wbase + r * wstride] = v[r].x;
+    }
+    sync();
+    if (act) {
+#pragma unroll
+      for (int s = 0; s < 27; ++s) v[s].x = sd[j + s * TP];
+    }
+    sync();
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < 27; ++r) sd[wbase + r * wstride] = v[r].y;
+    }
+    sync();
+    if (act) {
+#pragma unroll
+      for (int s = 0; s < 27; ++s) v[s].y = sd[j + s * TP];
+    }
+  }
+}
+
 // Full transform of one pencil.  j: index of the thread within the pencil's group;
 // threads with j >= TP (act == false) carry zeros, take part in the barriers and
-// touch no memory.  sm: the group's exchange buffer of L complex.  The last
+// touch no memory.  sm: the group's exchange buffer of L complex (HALF: L doubles).  The last
 // shared-memory access is not followed by a barrier.
-template <int L, bool INV, typename Sync>
+template <int L, bool INV, bool HALF = false, typename Sync>
 __device__ __forceinline__ void fft_fat(double2 (&v)[27], double2* sm, int j, bool act, const double2* __restrict__ tw,
                                         const Sync& sync) {
   using P = R27<L>;
   constexpr int TP = P::TP;
   bfly27<INV>(v);  // pass 0 (Ns = 1)
   if constexpr (L == 27) return;
-  sync();  // earlier readers of sm are done
-  if (act) {
-#pragma unroll
-    for (int r = 0; r < 27; ++r) sm[27 * j + r] = v[r];
-  }
-  sync();
-  if (act) {
-#pragma unroll
-    for (int s = 0; s < 27; ++s) v[s] = sm[j + s * TP];
-  }
+  fat_exchange<L, HALF>(v, sm, 27 * j, 1, j, act, sync);
   if constexpr (P::NP >= 2) {  // pass 1 (Ns = 27)
     const int k = j % 27;
     if (act) {
@@ -147,17 +182,7 @@ __device__ __forceinline__ void fft_fat(double2 (&v)[27], double2* sm, int j, bo
     }
     bfly27<INV>(v);
     if constexpr (P::TAIL > 1) {
-      const int base = (j - k) * 27 + k;
-      sync();
-      if (act) {
-#pragma unroll
-        for (int r = 0; r < 27; ++r) sm[base + r * 27] = v[r];
-      }
-      sync();
-      if (act) {
-#pragma unroll
-        for (int s = 0; s < 27; ++s) v[s] = sm[j + s * TP];
-      }
+      fat_exchange<L, HALF>(v, sm, (j - k) * 27 + k, 27, j, act, sync);
     }
   }
   if constexpr (P::TAIL == 3) {  // butterflies b = j + m TP over elements s = m, m + 9, m + 18

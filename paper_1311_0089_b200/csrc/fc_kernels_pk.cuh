@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_pk(Geo g, RowGeo rg, Coef Cf
   const double* __restrict__ A = Cf.A + vbase;
   double* __restrict__ PN = ia.p_new + rbase + vbase;
   double* __restrict__ X = ev.xacc != nullptr ? ev.xacc + rbase + vbase : nullptr;
+  trace_stamp(1, 0);
   constexpr int K = 2;  // voxels per thread in flight (all their loads issued first)
   for (int e0 = threadIdx.x; e0 < n; e0 += K * blockDim.x) {
     double u[K][C], po[K][C], xo[K][C], am[K][NSYM];
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_pk(Geo g, RowGeo rg, Coef Cf
     }
   }
   __syncthreads();
+  trace_stamp(1, 1);
 
   // ---- 2. row FFT of component a, pencil p (rows 2p, 2p+1) -------------------
   const int per_a = npk * TP;
@@ -136,6 +138,7 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_pk(Geo g, RowGeo rg, Coef Cf
   // pencil's threads only; fft_reg syncs before its first write)
   double2* smp = sm + (size_t)(a * npk + p) * L;
   fft_reg<L, 1, false>(v, smp, L, j, tw);
+  trace_stamp(1, 2);
   __syncthreads();
 #pragma unroll
   for (int s = 0; s < 9; ++s) smp[j + s * TP] = v[0][s];
@@ -167,7 +170,10 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_pk(Geo g, RowGeo rg, Coef Cf
         tma_store_3d(&tmP, 2 * row0, b * rg.boxK, c2, Y + (size_t)aa * ybox + (size_t)b * rg.boxK * B);
     }
     bulk_commit();
+    trace_stamp(1, 3);
     bulk_wait_read0();
+    trace_stamp(1, 4);
+    trace_stamp(1, 5);
   }
 }
 

@@ -10,6 +10,25 @@ namespace fc {
 
 constexpr int kMaxBlock = 512;   // row / mid sweeps
 
+#ifdef FC_TRACE  // experimental builds only (tools/exp_build.sh): per-CTA phase stamps of the sweeps
+// kernel ids: 0 outer (d = 2), 1 row_fwd_pk, 2 mid_fwd, 3 outer_seq, 4 mid_inv, 5 row_inv
+__device__ unsigned long long g_trace[6 * 8 * 8192];
+__device__ __forceinline__ void trace_stamp(int kid, int slot) {
+  if (threadIdx.x == 0 && blockIdx.x < 8192) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[(kid * 8192 + blockIdx.x) * 8 + slot] = t;
+    if (slot == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_trace[(kid * 8192 + blockIdx.x) * 8 + 7] = smid;
+    }
+  }
+}
+#else
+__device__ __forceinline__ void trace_stamp(int, int) {}
+#endif
+
 // 8-byte asynchronous global->shared copies (LDGSTS): loads stay in flight
 // without holding registers, so a CTA issues its whole input tile at once.
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -261,6 +280,7 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   const bool qpre = need_q && rg.tma && rg.qoff > 0;
   const int qsh = qpre ? bulk_shift(qsrc) : 0;
   const double* Q = reinterpret_cast<const double*>(smraw + rg.qoff) + qsh;
+  trace_stamp(5, 0);
   if (rg.tma) {
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
@@ -302,6 +322,7 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
     }
   }
   __syncthreads();
+  trace_stamp(5, 1);
   const int p = threadIdx.x / TP;
   const int j = threadIdx.x - p * TP;
   const int re = 2 * p, ro = 2 * p + 1;
@@ -320,6 +341,7 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
   // the exchange buffer overlaps the Y staging area: fft_reg syncs before its first write
   double2* smp = sm + (size_t)p * L;
   fft_reg<L, 1, true>(v, smp, L, j, tw);
+  trace_stamp(5, 2);
   const double Ea = ea.mode == EP_FP ? pick(ea.E, r, a) : 0.0;
   const bool he = re < nrows;
   double2 q[9];
@@ -358,7 +380,9 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
       ea.part[(int64_t)r * ea.nslot + slot] = sum;
     }
   }
+  trace_stamp(5, 3);
   const bool last = arrive_block(ea.fin);
+  trace_stamp(5, 4);
   {
     double* __restrict__ out = ea.out;
 #pragma unroll
@@ -368,6 +392,7 @@ __global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs e
       if (has_o) out[ebase + (int64_t)ro * L + i] = v[0][s].y;
     }
   }
+  trace_stamp(5, 5);
   if (last) finalize_block(ea.fin, red);
 }
 
@@ -400,6 +425,7 @@ __device__ __forceinline__ void mid_tma(const Geo& g, const MidGeo& mg, const Rh
   const double2* pen = (INV ? dst : src) + (((int64_t)rc * mg.n0 + i00) * mg.h2 + k2) * L;  // pencil p at + p*h2*L
   const int64_t pstride = (int64_t)mg.h2 * L;
   __shared__ uint64_t bar;
+  trace_stamp(INV ? 4 : 2, 0);
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     if (!INV) {
@@ -413,6 +439,7 @@ __device__ __forceinline__ void mid_tma(const Geo& g, const MidGeo& mg, const Rh
   }
   __syncthreads();
   mbar_wait(&bar, 0);
+  trace_stamp(INV ? 4 : 2, 1);
   double2 v[1][9];
 #pragma unroll
   for (int s = 0; s < 9; ++s) {
@@ -420,6 +447,7 @@ __device__ __forceinline__ void mid_tma(const Geo& g, const MidGeo& mg, const Rh
     v[0][s] = INV ? sm[(size_t)i * BP + p] : sm[(size_t)p * L + i];
   }
   fft_reg<L, 1, INV>(v, sm + (size_t)p * L, L, j, tw);
+  trace_stamp(INV ? 4 : 2, 2);
   __syncthreads();
 #pragma unroll
   for (int s = 0; s < 9; ++s) {
@@ -436,7 +464,10 @@ __device__ __forceinline__ void mid_tma(const Geo& g, const MidGeo& mg, const Rh
       for (int b = 0; b < mg.nbox; ++b) tma_store_3d(&tmM, 2 * i00, b * mg.rows, cz, sm + (size_t)b * mg.rows * BP);
     }
     bulk_commit();
+    trace_stamp(INV ? 4 : 2, 3);
     bulk_wait_read0();
+    trace_stamp(INV ? 4 : 2, 4);
+    trace_stamp(INV ? 4 : 2, 5);
   }
 }
 
@@ -640,8 +671,10 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
     return;
   } else {
   double2 v[C][9];
+  trace_stamp(0, 0);
   if (bulk) {
     mbar_wait(&bar, 0);
+    trace_stamp(0, 1);
 #pragma unroll
     for (int a = 0; a < C; ++a)
 #pragma unroll
@@ -657,6 +690,7 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
   }
   double2* smp = sm + (size_t)qq * C * L;
   fft_reg<L, C, false>(v, smp, L, j, tw);
+  trace_stamp(0, 2);
   // Gamma_hat(k) v = xi (xi . v) / den ; 0 at k = 0
   double xi1 = 0.0, xi2 = 0.0;
   bool qzero = live && q == 0;
@@ -700,6 +734,7 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
     for (int a = 0; a < C; ++a) v[a][s] = make_double2(xi[a] * qv.x, xi[a] * qv.y);
   }
   fft_reg<L, C, true>(v, smp, L, j, tw);
+  trace_stamp(0, 3);
   if (bulk) {  // back through smem ([a][qq][L]) and one bulk store per component
     __syncthreads();
 #pragma unroll
@@ -714,7 +749,9 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
         bulk_s2g(W + ((int64_t)(r * C + a) * og.Q + (int64_t)qb * og.QB) * L, sm + (size_t)a * og.QB * L,
                  (unsigned)(nq * L * 16));
       bulk_commit();
+      trace_stamp(0, 4);
       bulk_wait_read0();
+      trace_stamp(0, 5);
     }
     return;
   }

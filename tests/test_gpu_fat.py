@@ -105,3 +105,18 @@ def test_staged_epilogue_input_is_bitwise_identical(shape):
     f1 = _ctx(shape, a, {"inv_qpre": 1}).solve_fixed_point(E, 1e-6, 500, A0, [1.0, 1.0])
     assert [r["iterations"] for r in f0[0]] == [r["iterations"] for r in f1[0]]
     assert np.array_equal(f0[1], f1[1])
+
+
+@pytest.mark.parametrize("shape", [(81, 27, 27), (243, 9, 27), (729, 9, 9), (405, 9, 15)], ids=lambda s: "x".join(map(str, s)))
+def test_unstaged_outer_sweep_is_bitwise_identical(shape):
+    # k_outer_dir: same transforms and g3_* arithmetic as the staged kernels, loads / stores straight from registers
+    a = _medium(shape, 11)
+    u = np.random.default_rng(12).standard_normal((2, 3) + shape)
+    base = _ctx(shape, a).apply_system(u)
+    got = _ctx(shape, a, {"outer_direct": 1}).apply_system(u)
+    assert np.array_equal(got, base)
+    E = np.eye(3)[:2]
+    r0, x0, _ = _ctx(shape, a).solve_cg(E, 1e-8, 1000)
+    r1, x1, _ = _ctx(shape, a, {"outer_direct": 1}).solve_cg(E, 1e-8, 1000)
+    assert [r["iterations"] for r in r0] == [r["iterations"] for r in r1]
+    assert np.array_equal(x0, x1)
