@@ -26,7 +26,6 @@
 #include "fc_kernels_reg.cuh"
 #include "fc_kernels_pipe.cuh"
 #include "fc_kernels_pk.cuh"
-#include "fc_kernels_fat.cuh"
 
 // Field allocations carry this many spare bytes: 16-byte-aligned bulk copies
 // (fc_tma.cuh) of a row block may read up to 8 bytes past its last element.
@@ -78,7 +77,6 @@ struct DevPlan {
   FftPlan plan{};
   double2* roots = nullptr;
   double2* rtw = nullptr;  // register-FFT twiddle table (L = 3^k only)
-  double2* ftw = nullptr;  // fat-thread FFT twiddle table (fc_fft_fat.cuh)
 };
 
 // register-path lengths (fc_fft_reg.cuh): 3^k for 9..2187 and 5 * 3^k for 45..1215
@@ -109,23 +107,6 @@ std::vector<double2> reg_twiddles(int L, const std::vector<double2>& roots) {
   if (tail)
     for (int r = 1; r < 3; ++r)
       for (int b = 0; b < L / 3; ++b) tw.push_back(roots[(int64_t)b * r % L]);
-  if (tw.empty()) tw.push_back(make_double2(1.0, 0.0));
-  return tw;
-}
-
-// Twiddle table of the fat-thread transform (layout: R27 in fc_fft_fat.cuh).
-std::vector<double2> fat_twiddles(int L, const std::vector<double2>& roots) {
-  int K = 0;
-  for (int t = L; t > 1; t /= 3) ++K;
-  const int NP = K / 3;
-  const int T = K % 3 == 0 ? 1 : (K % 3 == 1 ? 3 : 9);
-  std::vector<double2> tw;
-  if (NP >= 2)
-    for (int r = 1; r < 27; ++r)
-      for (int k = 0; k < 27; ++k) tw.push_back(roots[(int64_t)k * r * (L / 729) % L]);
-  if (T > 1)
-    for (int q = 1; q < T; ++q)
-      for (int b = 0; b < L / T; ++b) tw.push_back(roots[(int64_t)b * q % L]);
   if (tw.empty()) tw.push_back(make_double2(1.0, 0.0));
   return tw;
 }
@@ -176,8 +157,6 @@ struct PlanOpts {
   int aniso_fused = 1;     // packed coefficients: fused first sweep (0: pointwise kernel + row FFT)
   int inv_qpre = 1;        // last sweep: epilogue input staged by a bulk copy issued with the spectrum loads
   int fin_split = -1;      // reductions finalized by a separate launch (-1: from 1024 partial slots on)
-  int outer_fat = 0;       // outer sweep on the fat-thread FFT (27 values per thread, warp-owned pencils)
-  int outer_direct = 0;    // d = 3 outer sweep without staging (k_outer_dir)
   int defer_x = 1;         // CG x update deferred into the next first sweep
   int fused_exchange = 1;  // in-process slabs: sweeps store straight into the peers' buffers
   int sync_debug = 0;      // synchronize after every launch (error attribution)
@@ -252,7 +231,6 @@ struct fc_ctx {
   Coef coef() const { return Coef{A, coef_kind}; }
   const FftPlan& plan(int L) const { return plans.at(L).plan; }
   const double2* rtw(int L) const { return plans.at(L).rtw; }
-  const double2* ftw(int L) const { return plans.at(L).ftw; }
   // register-path tiling per sweep (0 = generic path)
   int row_npen = 0, mid_bp = 0, outer_qb = 0;
   int pk_npen = 0;          // fused packed-coefficient first sweep: pencils per component (0: split)
@@ -464,11 +442,6 @@ int ensure_plan(fc_ctx* c, int L) {
     CK(cudaMalloc(&dp.rtw, sizeof(double2) * tw.size()));
     CK(cudaMemcpy(dp.rtw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
   }
-  if (fc::is_fat_len(L) && !c->force_generic) {
-    std::vector<double2> tw = fat_twiddles(L, roots);
-    CK(cudaMalloc(&dp.ftw, sizeof(double2) * tw.size()));
-    CK(cudaMemcpy(dp.ftw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
-  }
   c->plans[L] = dp;
   return FC_OK;
 }
@@ -644,16 +617,6 @@ int choose_tiles(fc_ctx* c) {
     default: break;                      \
   }
 
-#define FC_FAT_SWITCH(L, ...)          \
-  switch (L) {                           \
-    case 27: { constexpr int LL = 27; __VA_ARGS__; } break;     \
-    case 81: { constexpr int LL = 81; __VA_ARGS__; } break;     \
-    case 243: { constexpr int LL = 243; __VA_ARGS__; } break;   \
-    case 729: { constexpr int LL = 729; __VA_ARGS__; } break;   \
-    case 2187: { constexpr int LL = 2187; __VA_ARGS__; } break; \
-    default: break;                      \
-  }
-
 int allow_reg_smem(int mx) {
   int rc = FC_OK;
   auto al = [&](auto k) { if (rc == FC_OK) rc = allow_smem(k, mx); };
@@ -672,13 +635,6 @@ int allow_reg_smem(int mx) {
       al(k_outer_r<LL, 2>);
       al(k_outer_r<LL, 3>);
       al(k_outer_seq<LL, 3>);
-      al(k_outer_dir<LL>);
-    });
-  }
-  for (int L : {27, 81, 243, 729, 2187}) {
-    FC_FAT_SWITCH(L, {
-      al(k_outer_fat<LL, 2>);
-      al(k_outer_fat<LL, 3>);
     });
   }
   return rc;
@@ -914,26 +870,7 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
       for (int b = 0; b < 3; ++b) og.M[a][b] = M[a][b];
     double2* Wout = c->P > 1 ? c->W2r : c->W2;
     og.R = R;
-    if (c->opt.outer_fat && c->P == 1 && !c->force_generic && fc::is_fat_len(c->n0g)) {
-      // fat-thread transform, warp-owned pencils (fc_kernels_fat.cuh)
-      const double2* tw = c->ftw(c->n0g);
-      TRY(launch(c, "outer", [&] {
-        FC_FAT_SWITCH(c->n0g, {
-          constexpr int per = (kFatThreads / FatGeo<LL>::GT) * FatGeo<LL>::PPG;  // pencils per CTA
-          const dim3 grid((unsigned)((og.Q + per - 1) / per), R);
-          const size_t smem = (kFatThreads / FatGeo<LL>::GT) * FatGeo<LL>::group_bytes;
-          if (d == 2) k_outer_fat<LL, 2><<<grid, kFatThreads, smem, s>>>(g, og, st, tw, Wout);
-          else k_outer_fat<LL, 3><<<grid, kFatThreads, smem, s>>>(g, og, st, tw, Wout);
-        })
-      }));
-    } else if (c->outer_qb && c->opt.outer_direct && d == 3 && c->P == 1) {
-      const int nt = c->outer_qb * (c->n0g / 9);
-      const double2* tw = c->rtw(c->n0g);
-      const size_t smem = (size_t)32 * c->outer_qb * c->n0g;
-      TRY(launch(c, "outer", [&] {
-        FC_POW3_SWITCH(c->n0g, (k_outer_dir<LL><<<(unsigned)(R * og.nqb), nt, smem, s>>>(g, og, st, tw, Wout)))
-      }));
-    } else if (c->outer_qb && c->outer_seq && c->P == 1 && og.tma) {
+    if (c->outer_qb && c->outer_seq && c->P == 1 && og.tma) {
       const int nt = c->outer_qb * (c->n0g / 9);
       const double2* tw = c->rtw(c->n0g);
       TRY(launch(c, "outer", [&] {
@@ -1073,7 +1010,7 @@ int32_t fc_set_plan_option(const char* key, int32_t value) {
   const struct { const char* name; int* field; } table[] = {
       {"force_generic", &o.force_generic}, {"row_threads", &o.row_threads}, {"mid_threads", &o.mid_threads},
       {"outer_threads", &o.outer_threads}, {"row_tma", &o.row_tma}, {"mid_tma", &o.mid_tma},
-      {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"inv_pipe", &o.inv_pipe}, {"inv_qpre", &o.inv_qpre}, {"fin_split", &o.fin_split}, {"outer_fat", &o.outer_fat}, {"outer_direct", &o.outer_direct},
+      {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"inv_pipe", &o.inv_pipe}, {"inv_qpre", &o.inv_qpre}, {"fin_split", &o.fin_split},
       {"aniso_fused", &o.aniso_fused}, {"defer_x", &o.defer_x}, {"fused_exchange", &o.fused_exchange},
       {"sync_debug", &o.sync_debug}, {"mid_threads_inv", &o.mid_threads_inv}, {"mid_map", &o.mid_map},
       {"mid_tma_fwd", &o.mid_tma_fwd}};
@@ -1359,7 +1296,6 @@ void fc_destroy(fc_ctx* c) {
   for (auto& kv : c->plans) {
     cudaFree(kv.second.roots);
     cudaFree(kv.second.rtw);
-    cudaFree(kv.second.ftw);
   }
   for (double* q : {c->xi, c->A, c->x, c->r, c->p[0], c->p[1], c->Ap, c->part, c->hist, c->d_mat}) cudaFree(q);
   cudaFree(c->W1);

@@ -193,39 +193,41 @@ __global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, Oute
     double2* row0 = sm + ((size_t)0 * og.QB + qq) * L;
     double2* row1 = sm + ((size_t)1 * og.QB + qq) * L;
     double2* row2 = sm + ((size_t)2 * og.QB + qq) * L;
+    // F0 v0 -> row0 (parked: every thread its own nine modes), F0 (xi1 v1 + xi2 v2)
+    // stays in registers; Gamma_hat there; q is transformed back right away and
+    // rows 1, 2 leave while xi0 q (row0) is still being transformed
+    double2 v[1][9];
 #pragma unroll 1
-    for (int a = 0; a < 2; ++a) {  // F0 v0 -> row0, F0 (xi1 v1 + xi2 v2) -> row1
-      double2* row = a == 0 ? row0 : row1;
-      double2 v[1][9];
+    for (int a = 0; a < 2; ++a) {
 #pragma unroll
       for (int s = 0; s < 9; ++s) {
         const int i = j + s * TP;
         v[0][s] = !live ? make_double2(0.0, 0.0) : a == 0 ? row0[i] : g3_fold(xi1, xi2, row1[i], row2[i]);
       }
-      fft_reg<L, 1, false>(v, row, L, j, tw);
-      __syncthreads();
+      fft_reg<L, 1, false>(v, a == 0 ? row0 : row1, L, j, tw);
+      if (a == 0) {
+        __syncthreads();
 #pragma unroll
-      for (int s = 0; s < 9; ++s) row[j + s * TP] = v[0][s];
+        for (int s = 0; s < 9; ++s) row0[j + s * TP] = v[0][s];
+      }
     }
-    __syncthreads();
     trace_stamp(3, 2);
     if (live) {
 #pragma unroll
       for (int s = 0; s < 9; ++s) {
         const int i0 = j + s * TP;
-        double2 t0 = row0[i0], t1 = row1[i0];
-        g3_mode(og, g.xi[0][i0], xi1, xi2, ql == 0 && i0 == 0, t0, t1);
+        double2 t0 = row0[i0];
+        g3_mode(og, g.xi[0][i0], xi1, xi2, ql == 0 && i0 == 0, t0, v[0][s]);
         row0[i0] = t0;
-        row1[i0] = t1;
       }
     }
 #pragma unroll 1
-    for (int a = 0; a < 2; ++a) {  // row0 <- F0^-1(xi0 q); rows 1, 2 <- xi1 / xi2 F0^-1(q)
-      double2* row = a == 0 ? row0 : row1;
-      double2 v[1][9];
+    for (int a = 1; a >= 0; --a) {  // rows 1, 2 <- xi1 / xi2 F0^-1(q); row0 <- F0^-1(xi0 q)
+      if (a == 0) {
 #pragma unroll
-      for (int s = 0; s < 9; ++s) v[0][s] = row[j + s * TP];
-      fft_reg<L, 1, true>(v, row, L, j, tw);
+        for (int s = 0; s < 9; ++s) v[0][s] = row0[j + s * TP];
+      }
+      fft_reg<L, 1, true>(v, a == 0 ? row0 : row1, L, j, tw);
       __syncthreads();
       if (a == 0) {
 #pragma unroll
@@ -236,8 +238,28 @@ __global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, Oute
           row1[j + s * TP] = g3_scale(xi1, v[0][s]);
           row2[j + s * TP] = g3_scale(xi2, v[0][s]);
         }
+        fence_proxy_async();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+#pragma unroll
+          for (int b = 1; b < C; ++b)
+            bulk_s2g(W + ((int64_t)(r * C + b) * og.Q + (int64_t)qb * og.QB) * L, sm + (size_t)b * og.QB * L,
+                     (unsigned)(nq * L * 16));
+          bulk_commit();
+        }
       }
     }
+    trace_stamp(3, 3);
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_s2g(W + ((int64_t)(r * C) * og.Q + (int64_t)qb * og.QB) * L, sm, (unsigned)(nq * L * 16));
+      bulk_commit();
+      trace_stamp(3, 4);
+      bulk_wait_read0();
+      trace_stamp(3, 5);
+    }
+    return;
   } else {
 #pragma unroll 1
   for (int a = 0; a < C; ++a) {  // forward transforms, spectra back in place
@@ -322,77 +344,6 @@ __global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, Oute
     trace_stamp(3, 4);
     bulk_wait_read0();
     trace_stamp(3, 5);
-  }
-}
-
-// d = 3 outer sweep without staging (single slab): every thread loads its nine
-// points of a pencil straight from HBM into registers (runs of TP x 16 bytes),
-// folds components 1 and 2 on the way (g3_fold) and stores the results straight
-// back, so shared memory holds only the transform's exchange buffer and one
-// parked spectrum per pencil (2 L complex instead of the 3 L staged by
-// k_outer_seq): three CTAs per SM instead of two, no bulk-store drain at the
-// end of the CTA.  Same arithmetic as k_outer_seq / k_outer_r<L, 3>.
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
-
-template <int L>
-__global__ void __launch_bounds__(256, 3) k_outer_dir(Geo g, OuterGeo og, const RhsState* st,
-                                                        const double2* __restrict__ tw, double2* __restrict__ W) {
-  constexpr int TP = RegTP<L>::value;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  double2* sm = reinterpret_cast<double2*>(smraw);
-  const int qb = blockIdx.x % og.nqb;
-  const int r = blockIdx.x / og.nqb;
-  if (!rhs_active(st, r)) return;
-  const int qq = threadIdx.x / TP;
-  const int j = threadIdx.x - qq * TP;
-  const int ql = qb * og.QB + qq;
-  const bool live = ql < og.Q;
-  double2* ex = sm + (size_t)qq * 2 * L;  // exchange buffer of this pencil's transforms
-  double2* park = ex + L;                 // F0 v_0, then xi_0 q (every thread: its own nine modes)
-  const int qi = live ? ql : 0;
-  const int k2 = qi / og.n1, k1 = qi - k2 * og.n1;
-  const double xi1 = g.xi[1][k1];
-  const double xi2 = g.xi[2][k2];
-  double2* p0 = W + ((int64_t)(r * 3 + 0) * og.Q + qi) * L + j;
-  double2* p1 = W + ((int64_t)(r * 3 + 1) * og.Q + qi) * L + j;
-  double2* p2 = W + ((int64_t)(r * 3 + 2) * og.Q + qi) * L + j;
-  if (live) {  // components 1, 2 on their way to L2 while component 0 is transformed
-    for (int i = j * 8; i < L; i += TP * 8) {
-      prefetch_l2(p1 - j + i);
-      prefetch_l2(p2 - j + i);
-    }
-  }
-  const double2 zero = make_double2(0.0, 0.0);
-  double2 v[1][9];
-#pragma unroll
-  for (int s = 0; s < 9; ++s) v[0][s] = live ? p0[s * TP] : zero;
-  fft_reg<L, 1, false>(v, ex, L, j, tw);
-#pragma unroll
-  for (int s = 0; s < 9; ++s) park[j + s * TP] = v[0][s];
-#pragma unroll
-  for (int s = 0; s < 9; ++s) v[0][s] = live ? g3_fold(xi1, xi2, p1[s * TP], p2[s * TP]) : zero;
-  fft_reg<L, 1, false>(v, ex, L, j, tw);
-#pragma unroll
-  for (int s = 0; s < 9; ++s) {
-    const int i0 = j + s * TP;
-    double2 t0 = park[i0];
-    g3_mode(og, g.xi[0][i0], xi1, xi2, live && ql == 0 && i0 == 0, t0, v[0][s]);
-    park[i0] = t0;
-  }
-  fft_reg<L, 1, true>(v, ex, L, j, tw);
-  if (live) {
-#pragma unroll
-    for (int s = 0; s < 9; ++s) {
-      p1[s * TP] = g3_scale(xi1, v[0][s]);
-      p2[s * TP] = g3_scale(xi2, v[0][s]);
-    }
-  }
-#pragma unroll
-  for (int s = 0; s < 9; ++s) v[0][s] = park[j + s * TP];
-  fft_reg<L, 1, true>(v, ex, L, j, tw);
-  if (live) {
-#pragma unroll
-    for (int s = 0; s < 9; ++s) p0[s * TP] = v[0][s];
   }
 }
 

@@ -2,8 +2,7 @@
 d=2 rows of 81 (multi-pencil TMA boxes), d=2 rows of 2187 (persistent last
 sweep, one-pencil boxes), d=3 81^3 (TMA middle sweep, bulk outer), a packed
 anisotropic field (fused packed first sweep) and the fixed point; once with the
-default plan and once with the split finalize forced on these small grids and
-the fat-thread outer sweep."""
+default plan and once with the split finalize forced on these small grids."""
 import sys
 from pathlib import Path
 
@@ -14,7 +13,7 @@ from paper_1311_0089_b200 import CoefficientField, _native  # noqa: E402
 from paper_1311_0089_b200.grid import GridSpec  # noqa: E402
 
 rng = np.random.default_rng(1)
-for opts, shape in [(o, s) for o in ({}, {"fin_split": 1, "outer_fat": 1}) for s in [(81, 81), (9, 2187), (27, 27, 27)]]:
+for opts, shape in [(o, s) for o in ({}, {"fin_split": 1}) for s in [(81, 81), (9, 2187), (27, 27, 27)]]:
     _native.lib().fc_reset_plan_options()
     for k, v in opts.items():
         _native.lib().fc_set_plan_option(k.encode(), v)
