@@ -69,12 +69,19 @@ int32_t fc_device_count(int32_t* count);
  * Process-wide defaults copied into every context at creation, where the
  * kernels and tile geometry are chosen; existing contexts are unaffected.
  * Defaults are the measured-fastest choices; the alternatives perform the same
- * arithmetic and exist for bitwise variant tests and A/B measurements.  Keys:
+ * arithmetic (fin_split: the same sums in another fixed order) and exist for
+ * the variant tests and A/B measurements.  Keys:
  *   force_generic (0)  generic shared-memory FFT on every axis
- *   row_threads (256), mid_threads (0 = auto), outer_threads (0 = auto)  CTA sizes
+ *   row_threads (0 = auto), mid_threads (0 = auto), outer_threads (0 = auto)  CTA sizes
+ *   row_threads_inv (0 = auto)  last sweep CTA size (<= 512): its own row blocks and tensor boxes
  *   row_tma / mid_tma / outer_tma (1)  TMA data movement in the sweeps
  *   outer_seq (-1 = auto)  d = 3 outer sweep one component at a time
  *   inv_pipe (-1 = auto)  persistent double-buffered last sweep
+ *   inv_qpre (1)  last sweep: epilogue input staged by a bulk copy issued with the spectrum loads
+ *   fin_split (-1 = auto: from 1024 partial sums on)  reductions finalized by a
+ *     separate launch (fixed two-level order) instead of the last CTA to arrive;
+ *     agrees with the fused finalize to rounding, not bitwise
+ *   mid_threads_inv, mid_map, mid_tma_fwd  middle-sweep tiling / thread mapping
  *   aniso_fused (1)  packed coefficients: fused first sweep (0: pointwise kernel + row FFT)
  *   defer_x (1)  CG x update deferred into the next first sweep
  *   fused_exchange (1)  in-process slabs store straight into the peers' buffers

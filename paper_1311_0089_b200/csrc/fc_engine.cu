@@ -143,7 +143,8 @@ struct Prof {
 // bitwise variant tests (tests/test_gpu_variants.py) and A/B measurements.
 struct PlanOpts {
   int force_generic = 0;   // generic shared-memory Stockham FFT on every axis
-  int row_threads = 256;   // first / last sweep CTA size (pencils of the row block)
+  int row_threads = 0;     // first sweep CTA size (0: 128 for rows of 243 points, else 256)
+  int row_threads_inv = 0; // last sweep CTA size, <= 512 (0: 256): its own row blocks and tensor boxes
   int mid_threads = 0;     // middle sweep CTA size (0: 256 for pencils <= 243, else 512)
   int outer_threads = 0;   // outer sweep CTA size (0: 2 pencils for short 3-D pencils, else 256)
   int row_tma = 1;         // TMA tensor boxes for the transposed half spectrum
@@ -206,6 +207,7 @@ struct fc_ctx {
 
   // tiling
   RowGeo rg{};
+  RowGeo rgi{};            // last sweep: its own row blocks (wider tensor boxes)
   MidGeo mg{};
   OuterGeo og{};
   size_t smem_row = 0, smem_mid = 0, smem_outer = 0, smem_line = 0;
@@ -233,10 +235,12 @@ struct fc_ctx {
   const double2* rtw(int L) const { return plans.at(L).rtw; }
   // register-path tiling per sweep (0 = generic path)
   int row_npen = 0, mid_bp = 0, outer_qb = 0;
+  int row_npen_inv = 0;     // pencils per CTA of the last sweep
   int pk_npen = 0;          // fused packed-coefficient first sweep: pencils per component (0: split)
   size_t smem_pk = 0;
   int outer_seq = 0;        // d = 3 outer sweep one component at a time
-  CUtensorMap tmW{};        // TMA view of the row-sweep spectrum (RowGeo::tma)
+  CUtensorMap tmW{};        // TMA view of the row-sweep spectrum (RowGeo::tma), first sweep's boxes
+  CUtensorMap tmWi{};       // the same view with the last sweep's boxes (rgi)
   CUtensorMap tmP{};        // the same for the fused packed first sweep's row blocks (2 pk_npen rows)
   CUtensorMap tmM{};        // TMA view of the middle sweep's transposed side (MidGeo::tma), forward tiles
   CUtensorMap tmMi{};       // the same for the inverse sweep's tiles (mgi)
@@ -515,12 +519,16 @@ int choose_tiles(fc_ctx* c) {
     og.nqb = (og.Q + best - 1) / best;
     c->smem_outer = (size_t)32 * d * best * og.n0;
   }
+  c->rgi = c->rg;
   // register-resident path for power-of-three axes (fc_kernels_reg.cuh)
   const PlanOpts& op = c->opt;
   if (c->force_generic) return FC_OK;
   if (is_pow3_reg(rg.nl)) {
     const int TP = rg.nl / 9;
-    int npen = std::max(1, std::min(16, std::min(op.row_threads, 256) / TP));
+    // measured at 243^3 (profiles/r02n_ab_row_inv_threads_cfg3.txt): the first sweep runs
+    // 10 % faster in 8-row blocks, the last sweep 30 % slower, so each has its own blocks
+    const int rtf = op.row_threads > 0 ? op.row_threads : (TP == 27 ? 128 : 256);
+    int npen = std::max(1, std::min(16, std::min(rtf, 256) / TP));
     npen = std::min(npen, (rg.np + 1) / 2);
     rg.B = 2 * npen;
     rg.ntiles = (rg.np + rg.B - 1) / rg.B;
@@ -533,16 +541,31 @@ int choose_tiles(fc_ctx* c) {
     rg.boxK = ((rg.hl + rg.nbox - 1) / rg.nbox + 3) & ~3;  // boxes start 128-byte aligned in smem
     const size_t ybytes = (size_t)16 * rg.nbox * rg.boxK * 2 * npen;
     c->smem_row_r = std::max(c->smem_row_r, (size_t)16 * (((size_t)npen * rg.nl + 7) & ~(size_t)7) + ybytes);
-    c->smem_row_inv_r = std::max((size_t)16 * npen * (rg.nl + 1), ybytes);
-    // last sweep: the epilogue input (p / e of the row block) staged behind the
-    // spectrum by a bulk copy, if three CTAs still fit an SM
-    rg.qoff = 0;
-    if (op.inv_qpre) {
-      const size_t qoff = (c->smem_row_inv_r + 127) & ~(size_t)127;
-      const size_t tot = qoff + (size_t)8 * (2 * npen * rg.nl + 2);
-      if (3 * (tot + 1024) <= (size_t)c->smem_optin + 1024) {
-        rg.qoff = (int)qoff;
-        c->smem_row_inv_r = tot;
+    // last sweep: its own row blocks (up to 512 threads): wider rows in the
+    // transposed tensor boxes (16 bytes per row and mode)
+    {
+      const int rti = op.row_threads_inv > 0 ? op.row_threads_inv : 256;
+      int npi = std::max(1, std::min(16, std::min(rti, kMaxBlock) / TP));
+      npi = std::min(npi, (rg.np + 1) / 2);
+      RowGeo& ri = c->rgi;
+      ri = rg;
+      ri.B = 2 * npi;
+      ri.ntiles = (rg.np + ri.B - 1) / ri.B;
+      c->row_npen_inv = npi;
+      const size_t ybi = (size_t)16 * rg.nbox * rg.boxK * 2 * npi;
+      c->smem_row_inv_r = std::max((size_t)16 * npi * (rg.nl + 1), ybi);
+      // the epilogue input (p / e of the row block) staged behind the spectrum by
+      // a bulk copy, if the CTAs the register budget allows still fit an SM
+      ri.qoff = 0;
+      if (op.inv_qpre) {
+        const int nt = npi * TP;
+        const int want = nt <= 256 ? 3 : (nt <= 384 ? 2 : 1);
+        const size_t qoff = (c->smem_row_inv_r + 127) & ~(size_t)127;
+        const size_t tot = qoff + (size_t)8 * (2 * npi * rg.nl + 2);
+        if (want * (tot + 1024) <= (size_t)c->smem_optin + 1024) {
+          ri.qoff = (int)qoff;
+          c->smem_row_inv_r = tot;
+        }
       }
     }
     // packed coefficients: fused first sweep (fc_kernels_pk.cuh), d components of
@@ -625,7 +648,9 @@ int allow_reg_smem(int mx) {
       al(k_row_fwd_pk<LL, 2>);
       al(k_row_fwd_pk<LL, 3>);
       al(k_row_fwd_r<LL>);
-      al(k_row_inv_r<LL>);
+      al(k_row_inv_r<LL, 256>);
+      al(k_row_inv_r<LL, 384>);
+      al(k_row_inv_r<LL, 512>);
       al(k_mid_r<LL, false>);
       al(k_mid_r<LL, true>);
       al(k_mid_tma<LL, true, false>);
@@ -647,6 +672,7 @@ int allow_reg_smem(int mx) {
 int make_row_tmap(fc_ctx* c) {
   RowGeo& rg = c->rg;
   rg.tma = 0;
+  c->rgi.tma = 0;
   if (c->dim < 2 || !c->row_npen || rg.nbox == 0 || !c->opt.row_tma) {
     c->pk_npen = 0;  // the fused packed first sweep stores through its tensor map
     return FC_OK;
@@ -669,6 +695,14 @@ int make_row_tmap(fc_ctx* c) {
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rc != CUDA_SUCCESS) return set_err(FC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)rc);
   rg.tma = 1;
+  {  // same view, the last sweep's boxes
+    cuuint32_t boxi[3] = {(cuuint32_t)(2 * c->rgi.B), (cuuint32_t)rg.boxK, 1};
+    const CUresult ri = encode(&c->tmWi, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxi, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (ri != CUDA_SUCCESS) return set_err(FC_ECUDA, "cuTensorMapEncodeTiled (last sweep) failed (%d)", (int)ri);
+    c->rgi.tma = 1;
+  }
   if (c->pk_npen) {  // same view, boxes of the fused packed first sweep's 2 pk_npen rows
     cuuint32_t boxp[3] = {(cuuint32_t)(4 * c->pk_npen), (cuuint32_t)rg.boxK, 1};
     const CUresult rp = encode(&c->tmP, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxp, es,
@@ -728,7 +762,7 @@ int ensure_workspace(fc_ctx* c, int R, int hcap) {
     TRY(make_row_tmap(c));
   }
   // partial-sum slots: max over row sweeps, vector tiles, energy chunks
-  int64_t nslot_row = d == 1 ? 1 : (int64_t)c->rg.no * c->rg.ntiles * d;
+  int64_t nslot_row = d == 1 ? 1 : (int64_t)c->rgi.no * c->rgi.ntiles * d;
   int64_t nslot_vec = (field + kVecTile - 1) / kVecTile;
   int64_t nslot_en = (c->N + 8191) / 8192;
   int64_t need = std::max<int64_t>(std::max(std::max(nslot_row, nslot_vec), nslot_en), 64) * FC_MAX_RHS * FC_MAX_RHS;
@@ -747,7 +781,7 @@ int ensure_workspace(fc_ctx* c, int R, int hcap) {
   return FC_OK;
 }
 
-int64_t nslot_row(const fc_ctx* c) { return c->dim == 1 ? 1 : (int64_t)c->rg.no * c->rg.ntiles * c->dim; }
+int64_t nslot_row(const fc_ctx* c) { return c->dim == 1 ? 1 : (int64_t)c->rgi.no * c->rgi.ntiles * c->dim; }
 int64_t nslot_vec(const fc_ctx* c) { return ((int64_t)c->dim * c->N + kVecTile - 1) / kVecTile; }
 
 // Reducing launches on large grids hand their finalize to k_fin_split: returns
@@ -896,23 +930,27 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
   const FinArgs fin_full = ea.fin;
   ea.fin = fin_for_kernel(c, fin_full);
   auto last_sweep = [&]() -> int {
-  if (c->row_npen && c->rg.tma && c->inv_pipe_blocks > 0) {
-    const int nt = c->row_npen * (rg.nl / 9);
-    const double2* tw = c->rtw(rg.nl);
-    const int64_t ntile = nrow_blocks;
+  const RowGeo rgi = c->rgi;
+  const int64_t ninv_blocks = (int64_t)R * rgi.no * rgi.ntiles * d;
+  if (c->row_npen_inv && rgi.tma && c->inv_pipe_blocks > 0) {
+    const int nt = c->row_npen_inv * (rgi.nl / 9);
+    const double2* tw = c->rtw(rgi.nl);
+    const int64_t ntile = ninv_blocks;
     const unsigned grid = (unsigned)std::min<int64_t>(ntile, (int64_t)c->num_sms * c->inv_pipe_blocks);
     const int stage_c = c->inv_pipe_stage;
     const int nst = c->inv_pipe_nst;
-    const size_t smem = (size_t)nst * 16 * stage_c + (size_t)8 * (2 * c->row_npen * rg.nl + 2);
+    const size_t smem = (size_t)nst * 16 * stage_c + (size_t)8 * (2 * c->row_npen_inv * rgi.nl + 2);
     return launch(c, "row_inv", [&] {
-      FC_POW3_SWITCH(rg.nl, (k_row_inv_pp<LL><<<grid, nt, smem, s>>>(g, rg, ea, st, tw, ntile, stage_c, nst, 1, c->tmW)));
+      FC_POW3_SWITCH(rgi.nl, (k_row_inv_pp<LL><<<grid, nt, smem, s>>>(g, rgi, ea, st, tw, ntile, stage_c, nst, 1, c->tmWi)));
     });
   }
-  if (c->row_npen) {
-    const int nt = c->row_npen * (rg.nl / 9);
-    const double2* tw = c->rtw(rg.nl);
+  if (c->row_npen_inv) {
+    const int nt = c->row_npen_inv * (rgi.nl / 9);
+    const double2* tw = c->rtw(rgi.nl);
     return launch(c, "row_inv", [&] {
-      FC_POW3_SWITCH(rg.nl, (k_row_inv_r<LL><<<(unsigned)nrow_blocks, nt, c->smem_row_inv_r, s>>>(g, rg, ea, st, tw, Wrow, c->tmW)));
+      if (nt <= 256) FC_POW3_SWITCH(rgi.nl, (k_row_inv_r<LL, 256><<<(unsigned)ninv_blocks, nt, c->smem_row_inv_r, s>>>(g, rgi, ea, st, tw, Wrow, c->tmWi)))
+      else if (nt <= 384) FC_POW3_SWITCH(rgi.nl, (k_row_inv_r<LL, 384><<<(unsigned)ninv_blocks, nt, c->smem_row_inv_r, s>>>(g, rgi, ea, st, tw, Wrow, c->tmWi)))
+      else FC_POW3_SWITCH(rgi.nl, (k_row_inv_r<LL, 512><<<(unsigned)ninv_blocks, nt, c->smem_row_inv_r, s>>>(g, rgi, ea, st, tw, Wrow, c->tmWi)))
     });
   }
   const FftPlan pl_last = c->plan(rg.nl);
@@ -1008,7 +1046,7 @@ int32_t fc_set_plan_option(const char* key, int32_t value) {
   if (key == nullptr) return set_err(FC_EINVAL, "null option name");
   PlanOpts& o = g_plan_opts;
   const struct { const char* name; int* field; } table[] = {
-      {"force_generic", &o.force_generic}, {"row_threads", &o.row_threads}, {"mid_threads", &o.mid_threads},
+      {"force_generic", &o.force_generic}, {"row_threads", &o.row_threads}, {"row_threads_inv", &o.row_threads_inv}, {"mid_threads", &o.mid_threads},
       {"outer_threads", &o.outer_threads}, {"row_tma", &o.row_tma}, {"mid_tma", &o.mid_tma},
       {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"inv_pipe", &o.inv_pipe}, {"inv_qpre", &o.inv_qpre}, {"fin_split", &o.fin_split},
       {"aniso_fused", &o.aniso_fused}, {"defer_x", &o.defer_x}, {"fused_exchange", &o.fused_exchange},
@@ -1104,15 +1142,16 @@ int create_slab(fc_ctx** out, int32_t dim, const int64_t* shape, const double* h
     return fail(rc);
   // measured: faster for one pencil per block (L = 2187, cfg2), slower for the
   // short rows of cfg3 / cfg4 (L = 243 / 729: many pencils per block)
-  if (c->row_npen && (c->opt.inv_pipe >= 0 ? c->opt.inv_pipe != 0 : c->row_npen == 1)) {
-    const RowGeo& rg = c->rg;
-    const int B = 2 * c->row_npen;
-    c->inv_pipe_stage = (std::max(rg.nbox * rg.boxK * B, c->row_npen * (rg.nl + 1)) + 7) & ~7;
-    const size_t qbytes = (size_t)8 * (2 * c->row_npen * rg.nl + 2);
+  if (c->row_npen_inv && (c->opt.inv_pipe >= 0 ? c->opt.inv_pipe != 0 : c->row_npen_inv == 1) &&
+      c->row_npen_inv * (c->rgi.nl / 9) <= 256) {
+    const RowGeo& rg = c->rgi;
+    const int B = 2 * c->row_npen_inv;
+    c->inv_pipe_stage = (std::max(rg.nbox * rg.boxK * B, c->row_npen_inv * (rg.nl + 1)) + 7) & ~7;
+    const size_t qbytes = (size_t)8 * (2 * c->row_npen_inv * rg.nl + 2);
     const size_t smem = (size_t)c->inv_pipe_nst * 16 * c->inv_pipe_stage + qbytes;
     int nb = 0;
     FC_POW3_SWITCH(rg.nl, (allow_smem(k_row_inv_pp<LL>, mx),
-                           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_row_inv_pp<LL>, c->row_npen * (rg.nl / 9), smem)));
+                           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_row_inv_pp<LL>, c->row_npen_inv * (rg.nl / 9), smem)));
     c->inv_pipe_blocks = nb;
   }
   if (cudaMalloc(&c->any_active, sizeof(int)) != cudaSuccess) return fail(set_err(FC_ENOMEM, "flag alloc"));

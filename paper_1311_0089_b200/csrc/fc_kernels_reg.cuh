@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_r(Geo g, RowGeo rg, Coef C, 
 
 // Last sweep: transposed half-spectrum load into smem, two-for-one assembly
 // straight into registers, inverse FFT, epilogue from registers (coalesced).
-template <int L>
-__global__ void __launch_bounds__(256, 3) k_row_inv_r(Geo g, RowGeo rg, EpArgs ea, const RhsState* st,
+template <int L, int NT>
+__global__ void __launch_bounds__(NT, NT <= 256 ? 3 : (NT <= 384 ? 2 : 1)) k_row_inv_r(Geo g, RowGeo rg, EpArgs ea, const RhsState* st,
                                                           const double2* __restrict__ tw,
                                                           const double2* __restrict__ W,
                                                           const __grid_constant__ CUtensorMap tmW) {
