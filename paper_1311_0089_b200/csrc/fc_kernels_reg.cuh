@@ -568,6 +568,34 @@ __device__ __forceinline__ void g3_mode(const OuterGeo& og, double xi0, double x
 }
 __device__ __forceinline__ double2 g3_scale(double xi, double2 v) { return make_double2(__dmul_rn(xi, v.x), __dmul_rn(xi, v.y)); }
 
+// d = 2: (F0 v0, F0 v1) at one mode -> Gamma_hat(k) v = xi (xi . v) / den, 0 at k = 0.
+// (xi . v) / den as one reciprocal and two products (the reference divides twice,
+// solver.py:108: the results differ by at most 1 ulp).  Explicit roundings, so
+// every d = 2 outer kernel that uses it agrees bitwise.
+__device__ __forceinline__ void g2_mode(const OuterGeo& og, double xi0, double xi1, bool kzero, double2& t0, double2& t1) {
+  if (kzero) {
+    t0 = make_double2(0.0, 0.0);
+    t1 = make_double2(0.0, 0.0);
+    return;
+  }
+  double den;
+  if (og.orth) {
+    den = __fma_rn(xi1, xi1, __dmul_rn(xi0, xi0));
+  } else {
+    const double xi[2] = {xi0, xi1};
+    den = 0.0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) den = __fma_rn(__dmul_rn(xi[a], og.M[a][b]), xi[b], den);
+  }
+  const double inv = 1.0 / den;
+  const double2 qv = make_double2(__dmul_rn(__fma_rn(xi1, t1.x, __dmul_rn(xi0, t0.x)), inv),
+                                  __dmul_rn(__fma_rn(xi1, t1.y, __dmul_rn(xi0, t0.y)), inv));
+  t0 = make_double2(__dmul_rn(xi0, qv.x), __dmul_rn(xi0, qv.y));
+  t1 = make_double2(__dmul_rn(xi1, qv.x), __dmul_rn(xi1, qv.y));
+}
+
 // Outer sweep: each thread owns the C component pencils of one q so Gamma_hat
 // is applied in registers between the forward and inverse transforms.
 template <int L, int C>
@@ -691,47 +719,16 @@ __global__ void __launch_bounds__(kMaxBlockOuter, (C == 2 ? 2 : 1)) k_outer_r(Ge
   double2* smp = sm + (size_t)qq * C * L;
   fft_reg<L, C, false>(v, smp, L, j, tw);
   trace_stamp(0, 2);
-  // Gamma_hat(k) v = xi (xi . v) / den ; 0 at k = 0
-  double xi1 = 0.0, xi2 = 0.0;
-  bool qzero = live && q == 0;
-  if (C == 2) {
-    xi1 = g.xi[1][live ? q : 0];
-  } else if (C == 3) {
-    const int k2 = q / og.n1, k1 = q - k2 * og.n1;
-    xi1 = g.xi[1][live ? k1 : 0];
-    xi2 = g.xi[2][live ? k2 : 0];
-  }
+  // Gamma_hat(k) v = xi (xi . v) / den ; 0 at k = 0 (this branch is d = 2: g2_mode)
+  static_assert(C == 2, "d = 3 takes the folded branch above");
+  {
+    const double xi1 = g.xi[1][live ? q : 0];
+    const bool qzero = live && q == 0;
 #pragma unroll
-  for (int s = 0; s < 9; ++s) {
-    const int i0 = j + s * TP;
-    double xi[3] = {g.xi[0][i0], xi1, xi2};
-    if (qzero && i0 == 0) {
-#pragma unroll
-      for (int a = 0; a < C; ++a) v[a][s] = make_double2(0.0, 0.0);
-      continue;
+    for (int s = 0; s < 9; ++s) {
+      const int i0 = j + s * TP;
+      g2_mode(og, g.xi[0][i0], xi1, qzero && i0 == 0, v[0][s], v[1][s]);
     }
-    double2 dots = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int a = 0; a < C; ++a) {
-      dots.x += xi[a] * v[a][s].x;
-      dots.y += xi[a] * v[a][s].y;
-    }
-    double den = 0.0;
-    if (og.orth) {
-#pragma unroll
-      for (int a = 0; a < C; ++a) den += xi[a] * xi[a];
-    } else {
-#pragma unroll
-      for (int a = 0; a < C; ++a)
-#pragma unroll
-        for (int b = 0; b < C; ++b) den += xi[a] * og.M[a][b] * xi[b];
-    }
-    // (xi . v) / den as one reciprocal and two products (the reference divides
-    // twice, solver.py:108: the results differ by at most 1 ulp)
-    const double inv = 1.0 / den;
-    const double2 qv = make_double2(dots.x * inv, dots.y * inv);
-#pragma unroll
-    for (int a = 0; a < C; ++a) v[a][s] = make_double2(xi[a] * qv.x, xi[a] * qv.y);
   }
   fft_reg<L, C, true>(v, smp, L, j, tw);
   trace_stamp(0, 3);
