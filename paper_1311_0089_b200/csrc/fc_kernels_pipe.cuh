@@ -347,111 +347,4 @@ __global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, Oute
   }
 }
 
-// Outer sweep with the two transform sequences of a pencil side by side (single
-// slab, TMA pencils).  The Gamma_hat step couples two sequences per pencil --
-// (v_0, v_1) for d = 2, (v_0, u = xi_1 v_1 + xi_2 v_2) for d = 3 -- and each is
-// transformed forward and back.  k_outer_r holds both in one thread's registers,
-// k_outer_seq runs them one after the other; both leave an SM with 16 warps whose
-// transforms are bound by their own dependency chains (a 729-point transform
-// takes ~3.4 us whatever the occupancy).  Here each sequence has its own thread
-// group (2 x QB x TP threads per CTA, 64 registers), so twice as many transforms
-// are in flight per SM for the same shared memory.  The spectra meet in shared
-// memory for the per-mode step; every thread computes q for its own modes and
-// keeps its own sequence's share.  Same transforms and g2_ / g3_ arithmetic as
-// the other outer kernels: bitwise identical results.
-template <int L, int C>
-__global__ void __launch_bounds__(512, 2) k_outer_par(Geo g, OuterGeo og, const RhsState* st,
-                                                        const double2* __restrict__ tw, double2* __restrict__ W) {
-  constexpr int TP = RegTP<L>::value;
-  extern __shared__ __align__(128) unsigned char smraw[];
-  double2* sm = reinterpret_cast<double2*>(smraw);
-  __shared__ uint64_t bar;
-  const int qb = blockIdx.x % og.nqb;
-  const int r = blockIdx.x / og.nqb;
-  if (!rhs_active(st, r)) return;
-  const int per = og.QB * TP;  // threads per sequence group
-  const int grp = threadIdx.x / per;
-  const int t = threadIdx.x - grp * per;
-  const int qq = t / TP;
-  const int j = t - qq * TP;
-  const int ql = qb * og.QB + qq;
-  const bool live = ql < og.Q;
-  const int nq = min(og.QB, og.Q - qb * og.QB);
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    mbar_expect_tx(&bar, (unsigned)(C * nq * L * 16));
-#pragma unroll
-    for (int a = 0; a < C; ++a)
-      bulk_g2s(sm + (size_t)a * og.QB * L, W + ((int64_t)(r * C + a) * og.Q + (int64_t)qb * og.QB) * L,
-               (unsigned)(nq * L * 16), &bar);
-  }
-  __syncthreads();
-  const int qi = live ? ql : 0;
-  double xi1, xi2 = 0.0;
-  if constexpr (C == 3) {
-    const int k2 = qi / og.n1, k1 = qi - k2 * og.n1;
-    xi1 = g.xi[1][k1];
-    xi2 = g.xi[2][k2];
-  } else {
-    xi1 = g.xi[1][qi];
-  }
-  double2* row0 = sm + ((size_t)0 * og.QB + qq) * L;
-  double2* row1 = sm + ((size_t)1 * og.QB + qq) * L;
-  double2* row2 = sm + ((size_t)(C - 1) * og.QB + qq) * L;
-  double2* mine = grp == 0 ? row0 : row1;  // this sequence's row: input, exchange buffer, spectrum, result
-  mbar_wait(&bar, 0);
-  double2 v[1][9];
-#pragma unroll
-  for (int s = 0; s < 9; ++s) {
-    const int i = j + s * TP;
-    if (!live) v[0][s] = make_double2(0.0, 0.0);
-    else if (grp == 0) v[0][s] = row0[i];
-    else if constexpr (C == 3) v[0][s] = g3_fold(xi1, xi2, row1[i], row2[i]);
-    else v[0][s] = row1[i];
-  }
-  fft_reg<L, 1, false>(v, mine, L, j, tw);
-  __syncthreads();
-#pragma unroll
-  for (int s = 0; s < 9; ++s) mine[j + s * TP] = v[0][s];
-  __syncthreads();
-  if (live) {  // per mode: (F0 first, F0 second) -> this sequence's share of Gamma_hat
-#pragma unroll
-    for (int s = 0; s < 9; ++s) {
-      const int i0 = j + s * TP;
-      double2 t0 = grp == 0 ? v[0][s] : row0[i0];
-      double2 t1 = grp == 0 ? row1[i0] : v[0][s];
-      if constexpr (C == 3) g3_mode(og, g.xi[0][i0], xi1, xi2, ql == 0 && i0 == 0, t0, t1);
-      else g2_mode(og, g.xi[0][i0], xi1, ql == 0 && i0 == 0, t0, t1);
-      v[0][s] = grp == 0 ? t0 : t1;
-    }
-  }
-  // the transform's first exchange starts with a CTA barrier: every thread has read
-  // the other sequence's spectrum before any row is written again
-  fft_reg<L, 1, true>(v, mine, L, j, tw);
-  __syncthreads();
-  if (grp == 0) {
-#pragma unroll
-    for (int s = 0; s < 9; ++s) row0[j + s * TP] = v[0][s];
-  } else if constexpr (C == 3) {
-#pragma unroll
-    for (int s = 0; s < 9; ++s) {
-      row1[j + s * TP] = g3_scale(xi1, v[0][s]);
-      row2[j + s * TP] = g3_scale(xi2, v[0][s]);
-    }
-  } else {
-#pragma unroll
-    for (int s = 0; s < 9; ++s) row1[j + s * TP] = v[0][s];
-  }
-  fence_proxy_async();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int a = 0; a < C; ++a)
-      bulk_s2g(W + ((int64_t)(r * C + a) * og.Q + (int64_t)qb * og.QB) * L, sm + (size_t)a * og.QB * L,
-               (unsigned)(nq * L * 16));
-    bulk_commit();
-    bulk_wait_read0();
-  }
-}
-
 }  // namespace fc
