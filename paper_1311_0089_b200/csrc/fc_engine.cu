@@ -9,6 +9,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only: ranges cost nothing unless a tool is attached
 
 #include <algorithm>
 #include <cmath>
@@ -346,6 +347,7 @@ struct ProfSpan {
   cudaEvent_t e0 = nullptr;
 };
 ProfSpan prof_begin(fc_ctx* c) {
+  nvtxRangePushA("exchange");
   ProfSpan sp;
   if (c->prof_on) {
     sp.e0 = take_event(c);
@@ -354,6 +356,7 @@ ProfSpan prof_begin(fc_ctx* c) {
   return sp;
 }
 void prof_end(fc_ctx* c, const char* name, const ProfSpan& sp) {
+  nvtxRangePop();
   if (!c->prof_on || sp.e0 == nullptr) return;
   cudaEvent_t e1 = take_event(c);
   cudaEventRecord(e1, c->stream);
@@ -369,6 +372,14 @@ void prof_end(fc_ctx* c, const char* name, const ProfSpan& sp) {
   c->pending.push_back({idx, {sp.e0, e1}});
 }
 
+// NVTX range (nsys / ncu timelines): one per sweep launch, exchange and solver call.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Launch wrapper: counts launches and (when profiling) brackets with events.
 template <typename F>
 int launch(fc_ctx* c, const char* name, F&& f) {
@@ -378,7 +389,10 @@ int launch(fc_ctx* c, const char* name, F&& f) {
     e1 = take_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  f();
+  {
+    const NvtxRange range(name);
+    f();
+  }
   c->launches++;
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_err(FC_ECUDA, "launch of %s failed: %s", name, cudaGetErrorString(err));
@@ -1401,6 +1415,7 @@ int32_t fc_apply_A(fc_ctx* c, const double* u, double* out, int32_t nf) {
 }
 
 int32_t fc_project(fc_ctx* c, int32_t which, const double* ref, const double* u, double* out, int32_t nf) {
+  const NvtxRange nvtx_range("fc_project");
   TRY(check_ctx(c, false));
   TRY(check_R(nf));
   if (which != FC_PROJ_ORTHOGONAL && which != FC_PROJ_GAMMA_REF) return set_err(FC_EINVAL, "unknown projector %d", which);
@@ -1425,6 +1440,7 @@ int32_t fc_project(fc_ctx* c, int32_t which, const double* ref, const double* u,
 }
 
 int32_t fc_apply_system(fc_ctx* c, const double* u, double* out, int32_t nf) {
+  const NvtxRange nvtx_range("fc_apply_system");
   if (c && !c->sub.empty()) {
     TRY(check_R(nf));
     return shard_field_op(c, 1, nullptr, u, out, nf);
@@ -1448,6 +1464,7 @@ int32_t fc_apply_system(fc_ctx* c, const double* u, double* out, int32_t nf) {
 int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t max_iter, double lam,
                     const double* init, double* x_out, fc_report* rep, double* hist, double* iterates,
                     int64_t iterates_cap, int64_t* n_iterates) {
+  const NvtxRange nvtx_range("fc_solve_cg");
   TRY(check_ctx(c, true));
   TRY(check_R(R));
   if (!(tol > 0 && tol < 1)) return set_err(FC_EINVAL, "tol must lie in (0, 1), got %g", tol);
@@ -1606,6 +1623,7 @@ int32_t fc_solve_cg(fc_ctx* c, int32_t R, const double* E, double tol, int32_t m
 
 int32_t fc_solve_fixed_point(fc_ctx* c, int32_t R, const double* E, double tol, int32_t max_iter,
                              const double* ref, const double* scale, double* x_out, fc_report* rep, double* hist) {
+  const NvtxRange nvtx_range("fc_solve_fixed_point");
   TRY(check_ctx(c, true));
   TRY(check_R(R));
   if (!(tol > 0 && tol < 1)) return set_err(FC_EINVAL, "tol must lie in (0, 1), got %g", tol);
@@ -1680,6 +1698,7 @@ int32_t fc_solve_fixed_point(fc_ctx* c, int32_t R, const double* E, double tol, 
 }
 
 int32_t fc_energy(fc_ctx* c, int32_t R, const double* E, const double* x, double* out) {
+  const NvtxRange nvtx_range("fc_energy");
   if (c && !c->sub.empty()) {
     TRY(check_R(R));
     return shard_energy(c, R, E, x, out);
