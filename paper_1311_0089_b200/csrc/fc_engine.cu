@@ -814,7 +814,9 @@ int launch_fin_split(fc_ctx* c, const FinArgs& f) {
   if (!fin_is_split(c, f)) return FC_OK;
   if (c->part2 == nullptr) CK(cudaMalloc(&c->part2, sizeof(double) * kFinChunks * FC_MAX_RHS));
   const int G = std::max(1, std::min(kFinChunks, f.nslot / 2048));
-  return launch(c, "finalize", [&] { k_fin_split<<<dim3(G, f.R), 256, 0, c->stream>>>(f, c->part2, G); });
+  const dim3 grid = G == 1 ? dim3(1, 1) : dim3(G, f.R);
+  const int nt = G == 1 ? 256 * std::min(f.R, 4) : 256;
+  return launch(c, "finalize", [&] { k_fin_split<<<grid, nt, 0, c->stream>>>(f, c->part2, G); });
 }
 
 // One operator application over R fields, in three phases so a sharded run can

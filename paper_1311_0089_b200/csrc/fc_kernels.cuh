@@ -692,25 +692,65 @@ __global__ void k_fin_global(FinArgs f, SlabSums ss) {
 // chunks per right-hand side, each by one CTA (thread-strided, four
 // accumulators, the fixed block tree), the chunk sums in chunk order by the
 // last CTA to arrive -- and runs the same scalar logic as finalize_block.
-__global__ void __launch_bounds__(256) k_fin_split(FinArgs f, double* part2, int G) {
+__device__ __forceinline__ double fin_chunk_sum(const double* p, int64_t i0, int64_t i1, double* red) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t i = i0 + threadIdx.x;
+  for (; i + 768 < i1; i += 1024) {
+    a0 += __ldcg(p + i);
+    a1 += __ldcg(p + i + 256);
+    a2 += __ldcg(p + i + 512);
+    a3 += __ldcg(p + i + 768);
+  }
+  for (; i < i1; i += 256) a0 += __ldcg(p + i);
+  return block_sum((a0 + a1) + (a2 + a3), red);  // thread 0
+}
+
+__global__ void __launch_bounds__(1024) k_fin_split(FinArgs f, double* part2, int G) {
   __shared__ double red[256 / 32];
   __shared__ int last;
-  const int r = blockIdx.y, gi = blockIdx.x;
   const bool init = f.mode == FIN_INIT || f.mode == FIN_INIT2;
+  if (G == 1) {
+    // few partials: one CTA, a group of 256 threads per right-hand side (up to four
+    // side by side), no second level, no arrival.  Same sums in the same order as a
+    // 256-thread block_sum of the chunk.
+    __shared__ double gred[4][8];
+    const int grp = threadIdx.x >> 8, ngrp = blockDim.x >> 8, tl = threadIdx.x & 255;
+    for (int q = grp; q < f.R; q += ngrp) {
+      if (!init && !f.st[q].active) continue;
+      const double* p = f.part + (int64_t)q * f.nslot;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int64_t i = tl;
+      for (; i + 768 < f.nslot; i += 1024) {
+        a0 += __ldcg(p + i);
+        a1 += __ldcg(p + i + 256);
+        a2 += __ldcg(p + i + 512);
+        a3 += __ldcg(p + i + 768);
+      }
+      for (; i < f.nslot; i += 256) a0 += __ldcg(p + i);
+      const double w = warp_sum((a0 + a1) + (a2 + a3));
+      asm volatile("bar.sync %0, 256;\n" ::"r"(1 + grp) : "memory");
+      if ((tl & 31) == 0) gred[grp][tl >> 5] = w;
+      asm volatile("bar.sync %0, 256;\n" ::"r"(1 + grp) : "memory");
+      if (tl == 0) {
+        double sum = 0.0;
+        for (int k = 0; k < 8; ++k) sum += gred[grp][k];
+        if (f.lsum) f.lsum[q] = sum;
+        else fin_logic(f, q, sum);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && !f.lsum) {
+      int any = 0;
+      for (int q = 0; q < f.R; ++q) any |= f.st[q].active;
+      *f.any_active = any;
+    }
+    return;
+  }
+  const int r = blockIdx.y, gi = blockIdx.x;
   if (init || f.st[r].active) {
     const int64_t chunk = ((int64_t)f.nslot + G - 1) / G;
     const int64_t i0 = gi * chunk, i1 = min((int64_t)f.nslot, i0 + chunk);
-    const double* p = f.part + (int64_t)r * f.nslot;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int64_t i = i0 + threadIdx.x;
-    for (; i + 768 < i1; i += 1024) {
-      a0 += __ldcg(p + i);
-      a1 += __ldcg(p + i + 256);
-      a2 += __ldcg(p + i + 512);
-      a3 += __ldcg(p + i + 768);
-    }
-    for (; i < i1; i += 256) a0 += __ldcg(p + i);
-    const double sum = block_sum((a0 + a1) + (a2 + a3), red);
+    const double sum = fin_chunk_sum(f.part + (int64_t)r * f.nslot, i0, i1, red);
     if (threadIdx.x == 0) part2[r * G + gi] = sum;
   }
   if (threadIdx.x == 0) {
