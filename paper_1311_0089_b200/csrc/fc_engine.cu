@@ -152,7 +152,6 @@ struct PlanOpts {
   int mid_tma = 1;         // TMA inverse middle sweep
   int outer_tma = 1;       // bulk pencil copies in the outer sweep
   int outer_seq = -1;      // d = 3 outer sweep one component at a time (-1: for pencils >= 243)
-  int outer_pipe = 0;      // outer sweep as a role-split persistent pipeline (k_outer_pipe); value = stages (2..4), 1 = as many as fit
   int inv_pipe = -1;       // persistent double-buffered last sweep (-1: for one-pencil row blocks)
   int mid_threads_inv = 0; // inverse middle sweep CTA size (0: 256 for pencils <= 243, else 3 pencils)
   int mid_map = 1;         // middle sweep transform mapping: 1 lane-fastest, 0 pencil-fastest
@@ -675,8 +674,6 @@ int allow_reg_smem(int mx) {
       al(k_outer_r<LL, 2>);
       al(k_outer_r<LL, 3>);
       al(k_outer_seq<LL, 3>);
-      al(k_outer_pipe<LL, 2>);
-      al(k_outer_pipe<LL, 3>);
     });
   }
   return rc;
@@ -923,19 +920,7 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
       for (int b = 0; b < 3; ++b) og.M[a][b] = M[a][b];
     double2* Wout = c->P > 1 ? c->W2r : c->W2;
     og.R = R;
-    const size_t stage_bytes = (size_t)16 * d * c->outer_qb * c->n0g;
-    const int ns_fit = stage_bytes ? (int)std::min<size_t>(4, ((size_t)c->smem_optin - 2048) / stage_bytes) : 0;
-    const int ns = c->opt.outer_pipe >= 2 ? std::min(c->opt.outer_pipe, ns_fit) : ns_fit;
-    if (c->outer_qb && c->opt.outer_pipe && c->P == 1 && og.tma && d >= 2 && ns >= 2 &&
-        c->outer_qb * (c->n0g / 9) <= kPipeGroup) {
-      const double2* tw = c->rtw(c->n0g);
-      const unsigned grid = (unsigned)std::min<int64_t>((int64_t)R * og.nqb, c->num_sms);
-      const size_t smem = (size_t)ns * stage_bytes;
-      TRY(launch(c, "outer", [&] {
-        if (d == 2) FC_POW3_SWITCH(c->n0g, (k_outer_pipe<LL, 2><<<grid, 2 * kPipeGroup + 128, smem, s>>>(g, og, st, tw, Wout, ns)))
-        else FC_POW3_SWITCH(c->n0g, (k_outer_pipe<LL, 3><<<grid, 2 * kPipeGroup + 128, smem, s>>>(g, og, st, tw, Wout, ns)))
-      }));
-    } else if (c->outer_qb && c->outer_seq && c->P == 1 && og.tma) {
+    if (c->outer_qb && c->outer_seq && c->P == 1 && og.tma) {
       const int nt = c->outer_qb * (c->n0g / 9);
       const double2* tw = c->rtw(c->n0g);
       TRY(launch(c, "outer", [&] {
@@ -1079,7 +1064,7 @@ int32_t fc_set_plan_option(const char* key, int32_t value) {
   const struct { const char* name; int* field; } table[] = {
       {"force_generic", &o.force_generic}, {"row_threads", &o.row_threads}, {"row_threads_inv", &o.row_threads_inv}, {"mid_threads", &o.mid_threads},
       {"outer_threads", &o.outer_threads}, {"row_tma", &o.row_tma}, {"mid_tma", &o.mid_tma},
-      {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"outer_pipe", &o.outer_pipe}, {"inv_pipe", &o.inv_pipe}, {"inv_qpre", &o.inv_qpre}, {"fin_split", &o.fin_split},
+      {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"inv_pipe", &o.inv_pipe}, {"inv_qpre", &o.inv_qpre}, {"fin_split", &o.fin_split},
       {"aniso_fused", &o.aniso_fused}, {"defer_x", &o.defer_x}, {"fused_exchange", &o.fused_exchange},
       {"sync_debug", &o.sync_debug}, {"mid_threads_inv", &o.mid_threads_inv}, {"mid_map", &o.mid_map},
       {"mid_tma_fwd", &o.mid_tma_fwd}};

@@ -38,16 +38,6 @@ struct R9 {
   static constexpr int table = offT + (TAIL ? 2 * (L / 3) : 0);
 };
 
-// Barrier of the threads that share the exchange buffers: the whole CTA, or a
-// named barrier over a warp-aligned group of it (role-split kernels).
-struct SyncCta {
-  __device__ __forceinline__ void operator()() const { __syncthreads(); }
-};
-struct SyncNamed {  // named barrier `id` (1..15) over n threads, n a multiple of 32
-  int id, n;
-  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
-};
-
 // --- one radix-9 pass on CPT pencils held by this thread ---------------------
 template <int L, int CPT, bool INV, int S>
 __device__ __forceinline__ void r9_compute(double2 (&v)[CPT][9], int j, const double2* __restrict__ tw) {
@@ -71,21 +61,18 @@ __device__ __forceinline__ void r9_compute(double2 (&v)[CPT][9], int j, const do
 
 // Exchange after pass S: write Stockham output positions, read natural j + s*TP.
 // sm points at this thread's first pencil; pencils of the thread are pstride apart.
-template <int L, int CPT, int S, typename Sync>
-__device__ __forceinline__ void r9_exchange(double2 (&v)[CPT][9], double2* sm, int pstride, int j, const Sync& sync,
-                                            bool act) {
+template <int L, int CPT, int S>
+__device__ __forceinline__ void r9_exchange(double2 (&v)[CPT][9], double2* sm, int pstride, int j) {
   constexpr int Ns = ipow9(S);
   constexpr int TP = R9<L>::TP;
   const int k = j % Ns;
   const int base = (j - k) * 9 + k;
-  sync();
-  if (act) {
+  __syncthreads();
 #pragma unroll
-    for (int c = 0; c < CPT; ++c)
+  for (int c = 0; c < CPT; ++c)
 #pragma unroll
-      for (int r = 0; r < 9; ++r) sm[c * pstride + base + r * Ns] = v[c][r];
-  }
-  sync();
+    for (int r = 0; r < 9; ++r) sm[c * pstride + base + r * Ns] = v[c][r];
+  __syncthreads();
 #pragma unroll
   for (int c = 0; c < CPT; ++c)
 #pragma unroll
@@ -115,12 +102,11 @@ __device__ __forceinline__ void r3_tail(double2 (&v)[CPT][9], int j, const doubl
 
 template <int L, int CPT, bool INV, int S>
 struct R9Driver {
-  template <typename Sync>
   __device__ __forceinline__ static void run(double2 (&v)[CPT][9], double2* sm, int pstride, int j,
-                                             const double2* __restrict__ tw, const Sync& sync, bool act) {
+                                             const double2* __restrict__ tw) {
     r9_compute<L, CPT, INV, S>(v, j, tw);
-    if constexpr (S + 1 < R9<L>::NP9 || R9<L>::TAIL) r9_exchange<L, CPT, S>(v, sm, pstride, j, sync, act);
-    if constexpr (S + 1 < R9<L>::NP9) R9Driver<L, CPT, INV, S + 1>::run(v, sm, pstride, j, tw, sync, act);
+    if constexpr (S + 1 < R9<L>::NP9 || R9<L>::TAIL) r9_exchange<L, CPT, S>(v, sm, pstride, j);
+    if constexpr (S + 1 < R9<L>::NP9) R9Driver<L, CPT, INV, S + 1>::run(v, sm, pstride, j, tw);
   }
 };
 
@@ -142,9 +128,9 @@ __host__ __device__ constexpr int reg_table() {
   else return R9<L / 5>::table + 4 * (L / 5);
 }
 
-template <int L, int CPT, bool INV, typename Sync>
+template <int L, int CPT, bool INV>
 __device__ __forceinline__ void fft_reg(double2 (&v)[CPT][9], double2* sm, int pstride, int j,
-                                        const double2* __restrict__ tw, const Sync& sync, bool act = true);
+                                        const double2* __restrict__ tw);
 
 // L = 5 M (M = 3^k >= 9), decimation in time.  Thread j's elements j + s TP all
 // lie in the sub-sequence r = j mod 5 (TP = L/9 is a multiple of 5), at
@@ -154,23 +140,21 @@ __device__ __forceinline__ void fft_reg(double2 (&v)[CPT][9], double2* sm, int p
 // place: X[k2 + M k1] = sum_r w5^{r k1} (w_L^{r k2} Y_r[k2]), k2 < M (radix-5
 // butterflies; constant input still gives exact zeros: the sub-transforms leave
 // only Y_r[0] = M x, and the k2 = 0 butterfly of five equal values is exact).
-template <int L, int CPT, bool INV, typename Sync>
+template <int L, int CPT, bool INV>
 __device__ __forceinline__ void fft_reg_5m(double2 (&v)[CPT][9], double2* sm, int pstride, int j,
-                                           const double2* __restrict__ tw, const Sync& sync, bool act) {
+                                           const double2* __restrict__ tw) {
   constexpr int M = L / 5;
   constexpr int TP = L / 9;
   const int r = j % 5;
-  fft_reg<M, CPT, INV>(v, sm + r * M, pstride, j / 5, tw, sync, act);
-  sync();
-  if (act) {
+  fft_reg<M, CPT, INV>(v, sm + r * M, pstride, j / 5, tw);
+  __syncthreads();
 #pragma unroll
-    for (int c = 0; c < CPT; ++c)
+  for (int c = 0; c < CPT; ++c)
 #pragma unroll
-      for (int s = 0; s < 9; ++s) sm[c * pstride + r * M + j / 5 + s * (TP / 5)] = v[c][s];
-  }
-  sync();
+    for (int s = 0; s < 9; ++s) sm[c * pstride + r * M + j / 5 + s * (TP / 5)] = v[c][s];
+  __syncthreads();
   const double2* twc = tw + R9<M>::table;  // w_L^{r k2} at twc[(r - 1) M + k2]
-  for (int k2 = act ? j : M; k2 < M; k2 += TP) {
+  for (int k2 = j; k2 < M; k2 += TP) {
     double2 w[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -195,7 +179,7 @@ __device__ __forceinline__ void fft_reg_5m(double2 (&v)[CPT][9], double2* sm, in
       b[4 * M] = x4;
     }
   }
-  sync();
+  __syncthreads();
 #pragma unroll
   for (int c = 0; c < CPT; ++c)
 #pragma unroll
@@ -203,24 +187,17 @@ __device__ __forceinline__ void fft_reg_5m(double2 (&v)[CPT][9], double2* sm, in
 }
 
 // Full transform of CPT pencils: on entry v[c][s] = x_c[j + s*TP], on exit X_c[j + s*TP].
-// All threads of the barrier group (the CTA by default) must call it; threads
-// of the group that hold no data pass act = false (any valid j): they take part in
-// the barriers and write nothing.  The last smem access is followed by no
-// barrier, so callers reusing sm must sync first.
-template <int L, int CPT, bool INV, typename Sync>
-__device__ __forceinline__ void fft_reg(double2 (&v)[CPT][9], double2* sm, int pstride, int j,
-                                        const double2* __restrict__ tw, const Sync& sync, bool act) {
-  if constexpr (is_pow3(L)) {
-    R9Driver<L, CPT, INV, 0>::run(v, sm, pstride, j, tw, sync, act);
-    if constexpr (R9<L>::TAIL) r3_tail<L, CPT, INV>(v, j, tw);
-  } else {
-    fft_reg_5m<L, CPT, INV>(v, sm, pstride, j, tw, sync, act);
-  }
-}
+// All threads of the block must call it (it contains block barriers); its last
+// smem access is followed by no barrier, so callers reusing sm must sync first.
 template <int L, int CPT, bool INV>
 __device__ __forceinline__ void fft_reg(double2 (&v)[CPT][9], double2* sm, int pstride, int j,
                                         const double2* __restrict__ tw) {
-  fft_reg<L, CPT, INV>(v, sm, pstride, j, tw, SyncCta{});
+  if constexpr (is_pow3(L)) {
+    R9Driver<L, CPT, INV, 0>::run(v, sm, pstride, j, tw);
+    if constexpr (R9<L>::TAIL) r3_tail<L, CPT, INV>(v, j, tw);
+  } else {
+    fft_reg_5m<L, CPT, INV>(v, sm, pstride, j, tw);
+  }
 }
 
 }  // namespace fc

@@ -347,170 +347,4 @@ __global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, Oute
   }
 }
 
-// Outer sweep as a role-split persistent pipeline (single slab): one CTA per SM
-// walks its pencil blocks through a ring of NS shared-memory stages with three
-// roles -- a copy thread (bulk loads into a free stage, bulk stores out of a
-// finished one; its warpgroup gives its registers to the others), a forward group (both sequences of every pencil of the block
-// in registers, F0, spectra back to the stage) and an inverse group (Gamma_hat
-// per mode, F0^-1, results back to the stage) -- handing stages over through
-// mbarriers.  The two groups are always one block apart, so the forward
-// transforms of block n+1 overlap the inverse transforms of block n: different
-// work in different phases, where two CTAs of k_outer_r run the same phases side
-// by side and queue on the same shared-memory and FP64 pipes in turn.  Each
-// group has its own named barrier for the exchanges of its transforms.  Same
-// transforms and g2_ / g3_ arithmetic as k_outer_r: bitwise identical results.
-constexpr int kPipeGroup = 256;  // threads per transform group (QB TP <= 256 of them hold data)
-
-template <int L, int C>
-__global__ void __launch_bounds__(2 * kPipeGroup + 128, 1) k_outer_pipe(Geo g, OuterGeo og, const RhsState* st,
-                                                                        const double2* __restrict__ tw,
-                                                                        double2* __restrict__ W, int NS) {
-  constexpr int TP = RegTP<L>::value;
-  extern __shared__ __align__(128) unsigned char smraw[];
-  double2* sm = reinterpret_cast<double2*>(smraw);
-  __shared__ uint64_t b_load[4], b_spec[4], b_out[4];
-  __shared__ int s_act[FC_MAX_RHS_DEV];
-  const int stage_c = C * og.QB * L;  // complex per stage: rows [a][qq][L]
-  const int total = og.R * og.nqb;
-  if (threadIdx.x < og.R) s_act[threadIdx.x] = rhs_active(st, threadIdx.x) ? 1 : 0;
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < NS; ++b) {
-      mbar_init(&b_load[b], 1);
-      mbar_init(&b_spec[b], kPipeGroup);
-      mbar_init(&b_out[b], kPipeGroup);
-    }
-  }
-  __syncthreads();
-  const int role = threadIdx.x / kPipeGroup;  // 0 forward, 1 inverse, 2 copies
-  const int t = threadIdx.x - role * kPipeGroup;
-  auto row_ptr = [&](int it, int a) -> double2* {
-    const int r = it / og.nqb, qb = it - r * og.nqb;
-    return W + ((int64_t)(r * C + a) * og.Q + (int64_t)qb * og.QB) * L;
-  };
-  auto nq_of = [&](int it) { return min(og.QB, og.Q - (it % og.nqb) * og.QB); };
-  // 640 threads leave 96 registers each at launch; the copy warpgroup hands most of
-  // its share to the four transform warpgroups (two transforms of nine complex values
-  // per thread need ~112; the total must stay within the launch allocation: 512 x 112 + 128 x 24 <= 640 x 96)
-  if (role == 2) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n");
-    if (t != 0) return;
-    int hist[4] = {0, 0, 0, 0};
-    int k = 0;
-    auto store = [&](int it, int s) {
-      const unsigned bytes = (unsigned)(nq_of(it) * L * 16);
-#pragma unroll
-      for (int a = 0; a < C; ++a) bulk_s2g(row_ptr(it, a), sm + (size_t)s * stage_c + (size_t)a * og.QB * L, bytes);
-      bulk_commit();
-    };
-    for (int it = blockIdx.x; it < total; it += gridDim.x) {
-      if (!s_act[it / og.nqb]) continue;
-      const int s = k % NS;
-      if (k >= NS) {  // the block that used this stage NS blocks ago leaves first
-        mbar_wait(&b_out[s], (unsigned)((k / NS - 1) & 1));
-        store(hist[s], s);
-        bulk_wait_read0();
-      }
-      hist[s] = it;
-      const unsigned bytes = (unsigned)(nq_of(it) * L * 16);
-      mbar_expect_tx(&b_load[s], C * bytes);
-#pragma unroll
-      for (int a = 0; a < C; ++a) bulk_g2s(sm + (size_t)s * stage_c + (size_t)a * og.QB * L, row_ptr(it, a), bytes, &b_load[s]);
-      ++k;
-    }
-    for (int kk = max(0, k - NS); kk < k; ++kk) {
-      const int s = kk % NS;
-      mbar_wait(&b_out[s], (unsigned)((kk / NS) & 1));
-      store(hist[s], s);
-    }
-    bulk_wait_read0();
-    return;
-  }
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 112;\n");
-  const bool actv = t < og.QB * TP;
-  const int qq = actv ? t / TP : 0;
-  const int j = actv ? t - qq * TP : 0;
-  const SyncNamed gsync{1 + role, kPipeGroup};
-  int k = 0;
-  for (int it = blockIdx.x; it < total; it += gridDim.x) {
-    const int r = it / og.nqb, qb = it - r * og.nqb;
-    if (!s_act[r]) continue;
-    const int s = k % NS;
-    const unsigned ph = (unsigned)((k / NS) & 1);
-    double2* base = sm + (size_t)s * stage_c;
-    const int ql = qb * og.QB + qq;
-    const bool live = actv && ql < og.Q;
-    const int qi = live ? ql : 0;
-    double xi1, xi2 = 0.0;
-    if constexpr (C == 3) {
-      const int k2 = qi / og.n1, k1 = qi - k2 * og.n1;
-      xi1 = g.xi[1][k1];
-      xi2 = g.xi[2][k2];
-    } else {
-      xi1 = g.xi[1][qi];
-    }
-    double2* row0 = base + ((size_t)0 * og.QB + qq) * L;
-    double2* row1 = base + ((size_t)1 * og.QB + qq) * L;
-    double2* row2 = base + ((size_t)(C - 1) * og.QB + qq) * L;
-    double2* ex = base + (size_t)qq * C * L;  // this pencil's exchange area (2 L complex)
-    double2 v[2][9];
-    if (role == 0) {
-      mbar_wait(&b_load[s], ph);
-#pragma unroll
-      for (int q = 0; q < 9; ++q) {
-        const int i = j + q * TP;
-        if (!live) {
-          v[0][q] = make_double2(0.0, 0.0);
-          v[1][q] = make_double2(0.0, 0.0);
-        } else {
-          v[0][q] = row0[i];
-          if constexpr (C == 3) v[1][q] = g3_fold(xi1, xi2, row1[i], row2[i]);
-          else v[1][q] = row1[i];
-        }
-      }
-      fft_reg<L, 2, false>(v, ex, L, j, tw, gsync, actv);
-      gsync();
-      if (actv) {
-#pragma unroll
-        for (int q = 0; q < 9; ++q) {
-          row0[j + q * TP] = v[0][q];
-          row1[j + q * TP] = v[1][q];
-        }
-      }
-      mbar_arrive(&b_spec[s]);
-    } else {
-      mbar_wait(&b_spec[s], ph);
-#pragma unroll
-      for (int q = 0; q < 9; ++q) {
-        const int i0 = j + q * TP;
-        if (!live) {
-          v[0][q] = make_double2(0.0, 0.0);
-          v[1][q] = make_double2(0.0, 0.0);
-        } else {
-          v[0][q] = row0[i0];
-          v[1][q] = row1[i0];
-          if constexpr (C == 3) g3_mode(og, g.xi[0][i0], xi1, xi2, ql == 0 && i0 == 0, v[0][q], v[1][q]);
-          else g2_mode(og, g.xi[0][i0], xi1, ql == 0 && i0 == 0, v[0][q], v[1][q]);
-        }
-      }
-      fft_reg<L, 2, true>(v, ex, L, j, tw, gsync, actv);
-      gsync();
-      if (actv) {
-#pragma unroll
-        for (int q = 0; q < 9; ++q) {
-          row0[j + q * TP] = v[0][q];
-          if constexpr (C == 3) {
-            row1[j + q * TP] = g3_scale(xi1, v[1][q]);
-            row2[j + q * TP] = g3_scale(xi2, v[1][q]);
-          } else {
-            row1[j + q * TP] = v[1][q];
-          }
-        }
-      }
-      fence_proxy_async();
-      mbar_arrive(&b_out[s]);
-    }
-    ++k;
-  }
-}
-
 }  // namespace fc

@@ -72,8 +72,6 @@ def test_default_path_matches_oracle(medium, default_solve):
     {"inv_pipe": 0},
     {"defer_x": 0},
     {"defer_x": 0, "inv_pipe": 0},
-    {"outer_pipe": 1},
-    {"outer_pipe": 2},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_variant_is_bitwise_identical(medium, default_solve, opts):
     its0, x0 = default_solve
@@ -103,8 +101,7 @@ def test_mid_sweep_variants_3d(shape):
         return reps[0]["iterations"], x
 
     it0, x0 = run({})
-    for opts in ({"mid_tma": 0}, {"outer_threads": 256}, {"outer_tma": 0}, {"outer_seq": 1}, {"outer_seq": 0}, {"outer_pipe": 1}, {"outer_pipe": 2}, {"outer_pipe": 1, "outer_threads": 256},
-                 {"mid_map": 0},
+    for opts in ({"mid_tma": 0}, {"outer_threads": 256}, {"outer_tma": 0}, {"outer_seq": 1}, {"outer_seq": 0}, {"mid_map": 0},
                  {"mid_tma_fwd": 0}, {"mid_map": 0, "mid_tma_fwd": 0}, {"mid_threads": 512, "mid_threads_inv": 512},
                  {"mid_threads": 81, "mid_threads_inv": 162}):
         it, x = run(opts)
