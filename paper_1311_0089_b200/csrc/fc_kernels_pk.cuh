@@ -71,7 +71,10 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_pk(Geo g, RowGeo rg, Coef Cf
   double* __restrict__ PN = ia.p_new + rbase + vbase;
   double* __restrict__ X = ev.xacc != nullptr ? ev.xacc + rbase + vbase : nullptr;
   trace_stamp(1, 0);
-  constexpr int K = 2;  // voxels per thread in flight (all their loads issued first)
+  // voxels per thread in flight (all their loads issued first).  Measured at 729^3
+  // (profiles/r02z_ab_pk_k.txt): 2 -> 13.73 ms, 3 -> 13.37 ms (a row pair of 729 is
+  // exactly two rounds of 243 threads), 6 -> 32.9 ms (spills)
+  constexpr int K = 3;
   for (int e0 = threadIdx.x; e0 < n; e0 += K * blockDim.x) {
     double u[K][C], po[K][C], xo[K][C], am[K][NSYM];
 #pragma unroll
