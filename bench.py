@@ -214,7 +214,7 @@ class Workload:
             return gen.cfg3_sphere(self.n)
         return None
 
-    def setup(self, ctx, host_field=None, count_fn=None, want_labels=False):
+    def setup(self, ctx, host_field=None, count_fn=None, want_labels=False, compress=True):
         """Coefficient field into HBM (upload, or the device generator for cfg4 / cfg5)."""
         from paper_1311_0089_b200 import generators as gen
 
@@ -223,7 +223,7 @@ class Workload:
             return None
         if self.name == "cfg4":
             seeds, packed = gen.cfg4_grains(512, gen.SEEDS["cfg4"], self.n)
-            return ctx.generate_voronoi(seeds, packed, want_labels=want_labels), packed
+            return ctx.generate_voronoi(seeds, packed, want_labels=want_labels, compress=compress), packed
         if self.name == "cfg5":
             gen.cfg5_device(ctx, self.n, count_fn=count_fn)
             return None

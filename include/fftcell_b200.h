@@ -35,6 +35,7 @@ extern "C" {
 #define FC_ENOTSUP 4  /* shape outside the supported envelope */
 
 #define FC_MAX_RHS 8
+#define FC_MAX_PHASES 4096 /* distinct tensors of a phase-indexed coefficient field */
 
 /* Coefficient kinds (material.py:147-158 isotropic, material.py:90-145 packed). */
 #define FC_COEF_ISOTROPIC 0
@@ -115,6 +116,22 @@ int32_t fc_create_dist(fc_ctx** out, int32_t dim, const int64_t* shape, const do
 
 /* CoefficientField upload (material.py:90-158): count = N (isotropic) or nsym*N (packed). */
 int32_t fc_set_coefficients(fc_ctx* ctx, int32_t kind, const double* host, int64_t count);
+
+/* Phase-indexed form of a piecewise-constant packed field (no reference counterpart
+ * in storage; the values are those of CoefficientField.components, material.py:90-158):
+ * voxel v of the FFT-shifted row-major grid holds the packed tensor
+ * table[m * n_phases + labels[v]], m < d(d+1)/2.  count = |N| labels.  The solver
+ * reads 2 instead of 8 d(d+1)/2 coefficient bytes per voxel and application; every
+ * result is bit-identical to the packed field's.  FC_EINVAL for a label >= n_phases. */
+int32_t fc_set_coefficients_indexed(fc_ctx* ctx, int32_t n_phases, const double* table, const uint16_t* labels,
+                                    int64_t count);
+
+/* Turn the resident packed field into the indexed form on the device: exact
+ * (bitwise) deduplication of the per-voxel tensors, per slab.  *n_phases = the
+ * number of distinct tensors (largest slab), 0 when the field is isotropic or has
+ * more than max_phases (<= FC_MAX_PHASES) of them and stays as it is.  keep_packed
+ * = 0 frees the packed copy (rebuilt on demand by the consumers that need it). */
+int32_t fc_compress_coefficients(fc_ctx* ctx, int32_t max_phases, int32_t keep_packed, int32_t* n_phases);
 
 /* Voxel payload straight into HBM (material.py:194-307 format: f64le, row-major,
  * FFT-shifted, component-major): the .bin file streams through pinned staging

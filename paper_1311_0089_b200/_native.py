@@ -18,6 +18,7 @@ import numpy as np
 # experimental builds without touching the in-tree one)
 LIB_PATH = Path(os.environ.get("FC_LIB") or Path(__file__).resolve().parent / "libfftcell_b200.so")
 MAX_RHS = 8
+MAX_PHASES = 4096  # FC_MAX_PHASES
 
 FC_OK, FC_EINVAL, FC_ENOMEM, FC_ECUDA, FC_ENOTSUP = 0, 1, 2, 3, 4
 ST_OK, ST_MAXITER, ST_BREAKDOWN, ST_DIVERGENT = 0, 1, 2, 3
@@ -55,6 +56,10 @@ SIGNATURES = [
       ctypes.c_void_p]),
     ("fc_destroy", None, [ctypes.c_void_p]),
     ("fc_set_coefficients", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, _dp, ctypes.c_int64]),
+    ("fc_set_coefficients_indexed", ctypes.c_int32,
+     [ctypes.c_void_p, ctypes.c_int32, _dp, ctypes.POINTER(ctypes.c_uint16), ctypes.c_int64]),
+    ("fc_compress_coefficients", ctypes.c_int32,
+     [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]),
     ("fc_load_coefficients", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_char_p]),
     ("fc_coefficient_bounds", ctypes.c_int32, [ctypes.c_void_p, _dp, _dp, _i64p]),
     ("fc_save_solution", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_char_p]),
@@ -190,6 +195,7 @@ class Context:
                                            dev.size, dev.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
         self.slabs = slabs
         self.isotropic = None
+        self.n_phases = 0
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -198,7 +204,17 @@ class Context:
             self._h = ctypes.c_void_p()
 
     # -- coefficients ------------------------------------------------------
-    def set_coefficients(self, a):
+    def set_coefficients(self, a, compress=True):
+        """Upload a CoefficientField.  A field built by ``CoefficientField.from_phases``
+        goes up as labels + table (2 bytes per voxel); any other packed field is
+        uploaded whole and, with ``compress``, deduplicated on the device
+        (``compress_coefficients``).  ``n_phases`` = distinct tensors of the indexed
+        form, 0 when the full field is resident."""
+        self.n_phases = 0
+        phases = getattr(a, "phases", None)
+        if phases is not None and compress:
+            self.set_coefficients_indexed(phases[0], phases[1])
+            return
         if a.isotropic_values is not None:
             host = _c64(a.isotropic_values)
             kind = 0
@@ -207,6 +223,30 @@ class Context:
             kind = 1
         _check(lib().fc_set_coefficients(self._h, kind, _ptr(host), host.size))
         self.isotropic = kind == 0
+        if kind == 1 and compress and self.d >= 2:
+            self.compress_coefficients()
+
+    def set_coefficients_indexed(self, labels, table):
+        """Piecewise-constant packed field as ``labels`` (uint16, grid shape) and
+        ``table`` (``(d(d+1)/2, n_phases)`` packed tensors): voxel v holds
+        ``table[:, labels[v]]``."""
+        labels = np.ascontiguousarray(labels, dtype=np.uint16)
+        table = _c64(table)
+        nsym = self.d * (self.d + 1) // 2
+        if table.ndim != 2 or table.shape[0] != nsym:
+            raise ValueError(f"table shape {table.shape} != ({nsym}, n_phases)")
+        _check(lib().fc_set_coefficients_indexed(self._h, table.shape[1], _ptr(table),
+                                                 labels.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16)), labels.size))
+        self.isotropic = False
+        self.n_phases = int(table.shape[1])
+
+    def compress_coefficients(self, max_phases=MAX_PHASES, keep_packed=False):
+        """Deduplicate the resident packed field on the device (exact, bitwise);
+        returns the number of distinct tensors, 0 if the field stays as it is."""
+        n = ctypes.c_int32(0)
+        _check(lib().fc_compress_coefficients(self._h, int(max_phases), int(bool(keep_packed)), ctypes.byref(n)))
+        self.n_phases = n.value
+        return n.value
 
     def load_coefficients(self, bin_path, kind):
         """Stream a voxel payload (.bin) into HBM: kind 0 isotropic, 1 packed."""
@@ -223,14 +263,18 @@ class Context:
         """Stream the last solve's solution (nrhs, d, *N) from HBM into a .bin payload."""
         _check(lib().fc_save_solution(self._h, int(nrhs), os.fsencode(str(bin_path))))
 
-    def generate_voronoi(self, seeds, packed, want_labels=False):
-        """Device-side cfg4 polycrystal (replaces the coefficient field)."""
+    def generate_voronoi(self, seeds, packed, want_labels=False, compress=True):
+        """Device-side cfg4 polycrystal (replaces the coefficient field; kept in the
+        phase-indexed form with ``compress``)."""
         seeds = _c64(seeds)
         packed = _c64(packed)
         labels = np.empty(self.shape, dtype=np.int32) if want_labels else None
         lp = labels.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)) if want_labels else None
         _check(lib().fc_generate_voronoi(self._h, seeds.shape[0], _ptr(seeds), _ptr(packed), lp))
         self.isotropic = False
+        self.n_phases = 0
+        if compress:
+            self.compress_coefficients()
         return labels
 
     def spheres_stamp(self, centres, radius):

@@ -186,6 +186,10 @@ struct fc_ctx {
   double* A = nullptr;
   int coef_kind = -1;
   int64_t A_count = 0;
+  // phase-indexed form of a packed field (fc_coef.inc); A may be null while it is resident
+  uint16_t* lab = nullptr;
+  double* tab = nullptr;
+  int nph = 0;
 
   // workspace
   int Rcap = 0;
@@ -231,7 +235,7 @@ struct fc_ctx {
     for (int a = 0; a < dim; ++a) g.xi[a] = xi + xi_off[a];
     return g;
   }
-  Coef coef() const { return Coef{A, coef_kind}; }
+  Coef coef() const { return Coef{A, coef_kind, lab, tab, nph}; }
   const FftPlan& plan(int L) const { return plans.at(L).plan; }
   const double2* rtw(int L) const { return plans.at(L).rtw; }
   // register-path tiling per sweep (0 = generic path)
@@ -659,8 +663,10 @@ int allow_reg_smem(int mx) {
   auto al = [&](auto k) { if (rc == FC_OK) rc = allow_smem(k, mx); };
   for (int L : {9, 27, 81, 243, 729, 2187, 45, 135, 405, 1215}) {
     FC_POW3_SWITCH(L, {
-      al(k_row_fwd_pk<LL, 2>);
-      al(k_row_fwd_pk<LL, 3>);
+      al(k_row_fwd_pk<LL, 2, false>);
+      al(k_row_fwd_pk<LL, 3, false>);
+      al(k_row_fwd_pk<LL, 2, true>);
+      al(k_row_fwd_pk<LL, 3, true>);
       al(k_row_fwd_r<LL>);
       al(k_row_inv_r<LL, 256>);
       al(k_row_inv_r<LL, 384>);
@@ -819,6 +825,8 @@ int launch_fin_split(fc_ctx* c, const FinArgs& f) {
   return launch(c, "finalize", [&] { k_fin_split<<<grid, nt, 0, c->stream>>>(f, c->part2, G); });
 }
 
+#include "fc_coef.inc"
+
 // One operator application over R fields, in three phases so a sharded run can
 // exchange spectra between them: 0 = first sweep (+ forward middle sweep),
 // 1 = outer sweep (Gamma_hat), 2 = inverse middle sweep + last sweep.
@@ -826,8 +834,11 @@ enum Phase { PH_FWD = 1, PH_OUTER = 2, PH_INV = 4, PH_ALL = 7 };
 int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int orth, const double M[3][3],
                const RhsState* st) {
   const Geo g = c->geo();
-  const Coef C = c->coef();
   const int d = c->dim;
+  // indexed coefficients are read by the fused packed first sweep only
+  if ((phases & PH_FWD) && c->lab != nullptr && c->A == nullptr && ia.mode != IN_RAW && !(d >= 2 && c->pk_npen))
+    TRY(ensure_expanded(c));
+  const Coef C = c->coef();
   cudaStream_t s = c->stream;
   if (ea.part != nullptr) ea.nslot = (int)nslot_row(c);
   const SlabMap smap = c->slabmap(R);
@@ -882,8 +893,17 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
       const int64_t nb = (int64_t)R * rg.no * ((rg.np + 2 * npk - 1) / (2 * npk));
       const int nt = d * npk * (rg.nl / 9);
       TRY(launch(c, "row_fwd", [&] {
-        if (d == 2) FC_POW3_SWITCH(rg.nl, (k_row_fwd_pk<LL, 2><<<(unsigned)nb, nt, c->smem_pk, s>>>(g, rg, C, ia, st, twr, npk, c->tmP)))
-        else FC_POW3_SWITCH(rg.nl, (k_row_fwd_pk<LL, 3><<<(unsigned)nb, nt, c->smem_pk, s>>>(g, rg, C, ia, st, twr, npk, c->tmP)))
+        if (C.lab != nullptr) {
+          size_t smi = c->smem_pk;
+#if FC_PK_IDX_SMEM
+          if ((size_t)C.nph * (d * (d + 1) / 2) * 8 <= 32768) smi += (size_t)C.nph * (d * (d + 1) / 2) * 8;
+#endif
+          if (d == 2) FC_POW3_SWITCH(rg.nl, (k_row_fwd_pk<LL, 2, true><<<(unsigned)nb, nt, smi, s>>>(g, rg, C, ia, st, twr, npk, c->tmP)))
+          else FC_POW3_SWITCH(rg.nl, (k_row_fwd_pk<LL, 3, true><<<(unsigned)nb, nt, smi, s>>>(g, rg, C, ia, st, twr, npk, c->tmP)))
+        } else {
+          if (d == 2) FC_POW3_SWITCH(rg.nl, (k_row_fwd_pk<LL, 2, false><<<(unsigned)nb, nt, c->smem_pk, s>>>(g, rg, C, ia, st, twr, npk, c->tmP)))
+          else FC_POW3_SWITCH(rg.nl, (k_row_fwd_pk<LL, 3, false><<<(unsigned)nb, nt, c->smem_pk, s>>>(g, rg, C, ia, st, twr, npk, c->tmP)))
+        }
       }));
     } else if (C.kind == 1 && c->row_npen && ia.mode != IN_RAW) {
       // packed coefficients, split: pointwise y = M(x) u (+ p') at streaming
@@ -988,7 +1008,7 @@ int check_ctx(fc_ctx* c, bool need_coef) {
     if (need_coef && c->coef_kind < 0) return set_err(FC_EINVAL, "coefficients not set");
     return FC_OK;
   }
-  if (need_coef && c->A == nullptr) return set_err(FC_EINVAL, "coefficients not set");
+  if (need_coef && c->A == nullptr && c->lab == nullptr) return set_err(FC_EINVAL, "coefficients not set");
   CK(cudaSetDevice(c->device));
   return FC_OK;
 }
@@ -1353,6 +1373,7 @@ void fc_destroy(fc_ctx* c) {
     cudaFree(kv.second.rtw);
   }
   for (double* q : {c->xi, c->A, c->x, c->r, c->p[0], c->p[1], c->Ap, c->part, c->hist, c->d_mat}) cudaFree(q);
+  free_indexed(c);
   cudaFree(c->W1);
   cudaFree(c->W2);
   cudaFree(c->st);
@@ -1388,6 +1409,7 @@ int32_t fc_set_coefficients(fc_ctx* c, int32_t kind, const double* host, int64_t
   int64_t expect = kind == FC_COEF_ISOTROPIC ? c->N : (kind == FC_COEF_PACKED ? nsym * c->N : -1);
   if (expect < 0) return set_err(FC_EINVAL, "unknown coefficient kind %d", kind);
   if (count != expect) return set_err(FC_EINVAL, "coefficient count %lld != expected %lld", (long long)count, (long long)expect);
+  free_indexed(c);
   if (c->A == nullptr || c->A_count != count) {
     cudaFree(c->A);
     c->A = nullptr;
@@ -1397,6 +1419,44 @@ int32_t fc_set_coefficients(fc_ctx* c, int32_t kind, const double* host, int64_t
   CK(cudaMemcpyAsync(c->A, host, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
   c->coef_kind = kind;
   return sync(c);
+}
+
+int32_t fc_set_coefficients_indexed(fc_ctx* c, int32_t n_phases, const double* table, const uint16_t* labels,
+                                    int64_t count) {
+  if (c == nullptr) return set_err(FC_EINVAL, "null context");
+  if (table == nullptr || labels == nullptr) return set_err(FC_EINVAL, "null argument");
+  if (n_phases < 1 || n_phases > FC_MAX_PHASES)
+    return set_err(FC_EINVAL, "n_phases must lie in [1, %d], got %d", FC_MAX_PHASES, n_phases);
+  if (c->dim < 2) return set_err(FC_EINVAL, "indexed coefficients need dim >= 2");
+  if (count != c->Ng) return set_err(FC_EINVAL, "label count %lld != grid size %lld", (long long)count, (long long)c->Ng);
+  if (!c->sub.empty()) {
+    const int64_t plane = c->Ng / c->n0g;
+    for (fc_ctx* sl : c->sub) TRY(set_indexed_slab(sl, n_phases, table, labels + (int64_t)sl->s0[sl->me] * plane));
+    c->coef_kind = FC_COEF_PACKED;
+    return FC_OK;
+  }
+  TRY(check_ctx(c, false));
+  return set_indexed_slab(c, n_phases, table, labels);
+}
+
+int32_t fc_compress_coefficients(fc_ctx* c, int32_t max_phases, int32_t keep_packed, int32_t* n_phases) {
+  if (c == nullptr) return set_err(FC_EINVAL, "null context");
+  if (max_phases < 1 || max_phases > FC_MAX_PHASES)
+    return set_err(FC_EINVAL, "max_phases must lie in [1, %d], got %d", FC_MAX_PHASES, max_phases);
+  if (c->coef_kind < 0) return set_err(FC_EINVAL, "coefficients not set");
+  int most = 0;
+  if (!c->sub.empty()) {
+    for (fc_ctx* sl : c->sub) {
+      int nph = 0;
+      TRY(compress_slab(sl, max_phases, keep_packed, &nph));
+      most = std::max(most, nph);
+    }
+  } else {
+    TRY(check_ctx(c, true));
+    TRY(compress_slab(c, max_phases, keep_packed, &most));
+  }
+  if (n_phases != nullptr) *n_phases = most;
+  return FC_OK;
 }
 
 int32_t fc_apply_A(fc_ctx* c, const double* u, double* out, int32_t nf) {
@@ -1746,6 +1806,7 @@ int32_t fc_generate_voronoi(fc_ctx* c, int32_t n_seeds, const double* seeds, con
   CK(cudaMemcpy(d_packed.p, packed, sizeof(double) * nsym * n_seeds, cudaMemcpyHostToDevice));
   if (labels_out) CK(cudaMalloc(&d_lab.p, sizeof(int) * c->N));
   const int64_t count = (int64_t)nsym * c->N;
+  free_indexed(c);
   if (c->A == nullptr || c->A_count != count) {
     cudaFree(c->A);
     c->A = nullptr;
@@ -1814,6 +1875,7 @@ int32_t fc_spheres_finish(fc_ctx* c, double high, double low) {
   }
   TRY(check_ctx(c, false));
   if (c->sphere_bits == nullptr) return set_err(FC_EINVAL, "no spheres stamped");
+  free_indexed(c);
   if (c->A == nullptr || c->A_count != c->N) {
     cudaFree(c->A);
     c->A = nullptr;

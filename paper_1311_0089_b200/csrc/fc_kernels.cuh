@@ -104,8 +104,15 @@ __device__ __forceinline__ double2* send_dst(const SlabMap& m, double2* base, in
 }
 
 struct Coef {
-  const double* A;   // iso: (N) ; packed: (nsym, N)
+  const double* A;   // iso: (N) ; packed: (nsym, N); null while only the phase-indexed form is resident
   int kind;          // 0 isotropic scalar, 1 packed symmetric
+  // phase-indexed form of a piecewise-constant packed field (kind 1): voxel v holds
+  // tab[m * nph + lab[v]], bit for bit the packed value (fc_set_coefficients_indexed /
+  // fc_compress_coefficients).  Read by coef() and the fused packed first sweep;
+  // every other consumer takes the expanded field A.
+  const uint16_t* lab = nullptr;
+  const double* tab = nullptr;
+  int nph = 0;
 };
 
 struct InArgs {
@@ -166,6 +173,7 @@ __device__ __forceinline__ int pidx(int d, int a, int b) {
 
 __device__ __forceinline__ double coef(const Coef& C, int d, int a, int b, int64_t v, int64_t N) {
   if (C.kind == 0) return a == b ? C.A[v] : 0.0;
+  if (C.lab != nullptr) return __ldg(C.tab + pidx(d, a, b) * C.nph + C.lab[v]);
   return C.A[(int64_t)pidx(d, a, b) * N + v];
 }
 

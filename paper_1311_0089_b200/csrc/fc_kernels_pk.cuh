@@ -29,7 +29,20 @@ __host__ __device__ inline size_t pk_smem(int L, int C, int npk, int nbox, int b
   return pen + (size_t)C * nbox * boxK * 2 * npk * 16;
 }
 
-template <int L, int C>
+#ifndef FC_PK_IDX_SMEM
+#define FC_PK_IDX_SMEM 0  // experiment: phase table staged in shared memory (nph * NSYM * 8 <= 32 KB)
+#endif
+#ifndef FC_PK_IDX_K
+#define FC_PK_IDX_K 3  // voxels per thread in flight, indexed variant
+#endif
+#ifndef FC_PK_IDX_LATE
+#define FC_PK_IDX_LATE 0  // experiment: table reads (L1 hits) in the compute loop, not held across the loads
+#endif
+#ifndef FC_PK_IDX_CS
+#define FC_PK_IDX_CS 0  // experiment: streaming (evict-first) loads beside the cached table
+#endif
+
+template <int L, int C, bool IDX>
 __global__ void __launch_bounds__(256, 2) k_row_fwd_pk(Geo g, RowGeo rg, Coef Cf, InArgs ia, const RhsState* st,
                                                        const double2* __restrict__ tw, int npk,
                                                        const __grid_constant__ CUtensorMap tmP) {
@@ -68,32 +81,73 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd_pk(Geo g, RowGeo rg, Coef Cf
   const double* __restrict__ U = ia.u + rbase + vbase;
   const double* __restrict__ PO = ia.p_old + rbase + vbase;
   const double* __restrict__ A = Cf.A + vbase;
+  // phase-indexed coefficients: one 2-byte label per voxel and the phases' packed
+  // tensors from a table that stays in L1 (same values, 2 instead of 8 NSYM bytes
+  // per voxel from HBM)
+  const uint16_t* __restrict__ LB = IDX ? Cf.lab + vbase : nullptr;
+  const double* __restrict__ TB = Cf.tab;
+  const int nph = Cf.nph;
+#if FC_PK_IDX_SMEM
+  if (IDX && nph * NSYM * 8 <= 32768) {
+    double* TS = reinterpret_cast<double*>(smraw + pk_smem(L, C, npk, rg.nbox, rg.boxK));
+    for (int i = threadIdx.x; i < nph * NSYM; i += blockDim.x) TS[i] = __ldg(Cf.tab + i);
+    __syncthreads();
+    TB = TS;
+  }
+#endif
   double* __restrict__ PN = ia.p_new + rbase + vbase;
   double* __restrict__ X = ev.xacc != nullptr ? ev.xacc + rbase + vbase : nullptr;
   trace_stamp(1, 0);
   // voxels per thread in flight (all their loads issued first).  Measured at 729^3
   // (profiles/r02z_ab_pk_k.txt): 2 -> 13.73 ms, 3 -> 13.37 ms (a row pair of 729 is
   // exactly two rounds of 243 threads), 6 -> 32.9 ms (spills)
-  constexpr int K = 3;
+  constexpr int K = IDX ? FC_PK_IDX_K : 3;
   for (int e0 = threadIdx.x; e0 < n; e0 += K * blockDim.x) {
     double u[K][C], po[K][C], xo[K][C], am[K][NSYM];
+    // indexed: the labels first, so their latency hides behind the field loads and
+    // the table reads (L1 hits) find them ready
+    int ph[K];
+    if constexpr (IDX) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int e = e0 + k * blockDim.x;
+        ph[k] = e < n ? (int)__ldg(LB + e) : 0;
+      }
+    }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int e = e0 + k * blockDim.x;
       const bool ok = e < n;
 #pragma unroll
       for (int b = 0; b < C; ++b) {
-        u[k][b] = (ok && use_u) ? __ldg(U + b * N + e) : Ev[b];
-        po[k][b] = (ok && use_p) ? __ldg(PO + b * N + e) : 0.0;
+        if constexpr (IDX && FC_PK_IDX_CS) {
+          u[k][b] = (ok && use_u) ? __ldcs(U + b * N + e) : Ev[b];
+          po[k][b] = (ok && use_p) ? __ldcs(PO + b * N + e) : 0.0;
+        } else {
+          u[k][b] = (ok && use_u) ? __ldg(U + b * N + e) : Ev[b];
+          po[k][b] = (ok && use_p) ? __ldg(PO + b * N + e) : 0.0;
+        }
         xo[k][b] = (ok && X != nullptr) ? X[b * N + e] : 0.0;
       }
+      if constexpr (!IDX) {
 #pragma unroll
-      for (int m = 0; m < NSYM; ++m) am[k][m] = ok ? __ldg(A + m * N + e) : 0.0;
+        for (int m = 0; m < NSYM; ++m) am[k][m] = ok ? __ldg(A + m * N + e) : 0.0;
+      }
+    }
+    if constexpr (IDX && !FC_PK_IDX_LATE) {
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int m = 0; m < NSYM; ++m) am[k][m] = FC_PK_IDX_SMEM ? TB[m * nph + ph[k]] : __ldg(TB + m * nph + ph[k]);
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int e = e0 + k * blockDim.x;
       if (e >= n) break;
+      if constexpr (IDX && FC_PK_IDX_LATE) {
+#pragma unroll
+        for (int m = 0; m < NSYM; ++m) am[k][m] = __ldg(TB + m * nph + ph[k]);
+      }
       double x[C];
 #pragma unroll
       for (int b = 0; b < C; ++b) {

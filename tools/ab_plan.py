@@ -18,9 +18,10 @@ variants = sys.argv[3:] or [""]
 wl = bench.Workload(name, n)
 for var in variants:
     opts = dict((kv.split("=")[0], int(kv.split("=")[1])) for kv in var.split(",") if kv)
+    compress = bool(opts.pop("compress", 1))  # 0: keep the packed field (no phase index)
     with _native.plan_options(**opts):
         ctx = _native.Context(GridSpec((1.0,) * wl.d, wl.shape))
-    wl.setup(ctx, wl.host_field())
+    wl.setup(ctx, wl.host_field(), compress=compress)
     reps, _, _ = ctx.solve_cg(wl.loads, bench.TOL, bench.MAX_ITER, want_x=False)
     its = max(r["iterations"] for r in reps)
     ctx.timer_mark(0)
@@ -34,5 +35,5 @@ for var in variants:
     ctx.set_profiling(False)
     prof = ctx.profile()
     ks = " ".join(f"{k}={v[1] / max(v[0], 1):.3f}" for k, v in prof.items() if not k.endswith("_rhs"))
-    print(f"{name} [{var or 'default'}] iterations {its} {ms / its:.4f} ms/iter | {ks}", flush=True)
+    print(f"{name} [{var or 'default'}] phases {ctx.n_phases} iterations {its} {ms / its:.4f} ms/iter | {ks}", flush=True)
     del ctx
