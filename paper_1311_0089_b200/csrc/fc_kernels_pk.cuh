@@ -38,12 +38,15 @@ __host__ __device__ inline size_t pk_smem(int L, int C, int npk, int nbox, int b
 #ifndef FC_PK_IDX_LATE
 #define FC_PK_IDX_LATE 0  // experiment: table reads (L1 hits) in the compute loop, not held across the loads
 #endif
+#ifndef FC_PK_IDX_MINB
+#define FC_PK_IDX_MINB 2  // resident CTAs per SM the indexed variant is compiled for
+#endif
 #ifndef FC_PK_IDX_CS
 #define FC_PK_IDX_CS 0  // experiment: streaming (evict-first) loads beside the cached table
 #endif
 
 template <int L, int C, bool IDX>
-__global__ void __launch_bounds__(256, 2) k_row_fwd_pk(Geo g, RowGeo rg, Coef Cf, InArgs ia, const RhsState* st,
+__global__ void __launch_bounds__(256, IDX ? FC_PK_IDX_MINB : 2) k_row_fwd_pk(Geo g, RowGeo rg, Coef Cf, InArgs ia, const RhsState* st,
                                                        const double2* __restrict__ tw, int npk,
                                                        const __grid_constant__ CUtensorMap tmP) {
   constexpr int TP = RegTP<L>::value;
