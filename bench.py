@@ -230,8 +230,10 @@ class Workload:
             return out
         if self.name == "cfg5":
             gen.cfg5_device(ctx, self.n, count_fn=count_fn)
+            self.note_coefficients(ctx)
             return None
         ctx.set_coefficients(self.host_field())
+        self.note_coefficients(ctx)
         return None
 
     def note_coefficients(self, ctx):
@@ -239,6 +241,9 @@ class Workload:
         field's nsym, or a 2-byte label when the context holds the phase-indexed form."""
         if getattr(ctx, "n_phases", 0) > 0:
             self.nA = 2.0 / W
+        # outer sweep storing F0^-1 q once (plan two_field): one spectrum word per voxel
+        # and RHS less written; the inverse middle sweep still reads it for both components
+        self.two_field = bool(ctx.plan_info("two_field")) if hasattr(ctx, "plan_info") else False
         return self.nA
 
     # ---- byte model (SURVEY 8(d)) ----------------------------------------------
@@ -246,7 +251,7 @@ class Workload:
         """Fixed SURVEY model per CG iteration (B_iter) or fixed-point iteration (B_fp)."""
         c, R, S = self.d, self.R, 2 * self.d - 1
         extra = c * R if self.method == "fixed_point" else 9 * c * R
-        return W * self.N * (self.nA + 2 * S * c * R + extra)
+        return W * self.N * (self.nA + 2 * S * c * R + extra - (R if getattr(self, "two_field", False) else 0))
 
     def launch_words(self, kernel, phase, split):
         """(coefficient words read once per launch, words per active RHS) per voxel.
@@ -264,6 +269,8 @@ class Workload:
             return first_sweep[phase]
         if kernel == "row_fwd":
             return (0, 2 * c) if split else first_sweep[phase]
+        if kernel == "outer" and getattr(self, "two_field", False):
+            return (0, 2 * c - 1)                # c fields in, F0^-1 (xi0 q) and F0^-1 q out
         if kernel in ("mid_fwd", "outer", "mid_inv"):
             return (0, 2 * c)
         if kernel == "row_inv":
@@ -574,6 +581,7 @@ def run_gpu(args):
 
     with ClockSampler(local) as clk:
         res = measure(wl, ctx, args, world, args.steps)
+    wl.note_coefficients(ctx)  # the plan is complete once the workspace exists
     value, roof, per_kernel, operator, iteration = summarize(wl, res, args.steps, world, sharded, peak, peak_kind)
 
     # ---- e2e: host buffers through the C-ABI binding ----------------------------
@@ -661,6 +669,7 @@ def run_gpu(args):
             octx = _native.Context(GridSpec((1.0,) * ow.d, ow.shape), local)
             ow.setup(octx, ow.host_field())
             ores = measure(ow, octx, args, world, args.steps, fp_ref=25.5 * np.eye(3))
+            ow.note_coefficients(octx)
             ov, oroof, okern, oop, oit = summarize(ow, ores, args.steps, 1, False, peak, peak_kind)
             others[name] = {"config": config_dict(ow, "single"), "value": ov, "unit": UNIT,
                             "ms_per_step": ores["ms"] / args.steps, "iterations": ores["iters"],

@@ -84,6 +84,8 @@ int32_t fc_device_count(int32_t* count);
  *     agrees with the fused finalize to rounding, not bitwise
  *   mid_threads_inv, mid_map, mid_tma_fwd  middle-sweep tiling / thread mapping
  *   aniso_fused (1)  packed coefficients: fused first sweep (0: pointwise kernel + row FFT)
+ *   two_field (1)    d = 3, one slab: the outer sweep stores F0^-1 q once, the inverse middle
+ *                    sweep rebuilds components 1 and 2 from it (0: three fields; same bits)
  *   defer_x (1)  CG x update deferred into the next first sweep
  *   fused_exchange (1)  in-process slabs store straight into the peers' buffers
  *   sync_debug (0)  synchronize after every launch
@@ -210,6 +212,9 @@ int32_t fc_profile_count(fc_ctx* ctx);
 int32_t fc_profile_get(fc_ctx* ctx, int32_t i, char* name, int32_t name_cap, int64_t* launches, double* total_ms);
 int32_t fc_profile_reset(fc_ctx* ctx);
 int64_t fc_launch_count(fc_ctx* ctx);
+/* What the context's plan selected (no reference counterpart; the bench's byte model reads it):
+ * "two_field", "packed_fused", "n_phases" (0: full field resident), "slabs". */
+int32_t fc_plan_info(fc_ctx* ctx, const char* key, int32_t* value);
 /* CUDA-event timers on the context's stream: mark slot (0..7); elapsed between two marks (syncs on b). */
 int32_t fc_timer_mark(fc_ctx* ctx, int32_t slot);
 int32_t fc_timer_elapsed(fc_ctx* ctx, int32_t a, int32_t b, double* ms);

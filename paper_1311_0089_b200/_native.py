@@ -84,6 +84,7 @@ SIGNATURES = [
      [ctypes.c_void_p, ctypes.c_int32, ctypes.c_char_p, ctypes.c_int32, _i64p, _dp]),
     ("fc_profile_reset", ctypes.c_int32, [ctypes.c_void_p]),
     ("fc_launch_count", ctypes.c_int64, [ctypes.c_void_p]),
+    ("fc_plan_info", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32)]),
     ("fc_timer_mark", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32]),
     ("fc_timer_elapsed", ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, _dp]),
 ]
@@ -252,6 +253,12 @@ class Context:
         """Stream a voxel payload (.bin) into HBM: kind 0 isotropic, 1 packed."""
         _check(lib().fc_load_coefficients(self._h, int(kind), os.fsencode(str(bin_path))))
         self.isotropic = kind == 0
+
+    def plan_info(self, key):
+        """What the plan selected: "two_field", "packed_fused", "n_phases", "slabs"."""
+        v = ctypes.c_int32(0)
+        _check(lib().fc_plan_info(self._h, key.encode(), ctypes.byref(v)))
+        return v.value
 
     def coefficient_bounds(self):
         """(c_A, C_A, flat index of the first c_A voxel) of the device field."""

@@ -157,6 +157,7 @@ struct PlanOpts {
   int mid_map = 1;         // middle sweep transform mapping: 1 lane-fastest, 0 pencil-fastest
   int mid_tma_fwd = 1;     // forward middle sweep through TMA boxes (0: per-thread transposed stores)
   int aniso_fused = 1;     // packed coefficients: fused first sweep (0: pointwise kernel + row FFT)
+  int two_field = 1;       // d = 3, one slab: two spectrum fields from the outer to the inverse middle sweep
   int inv_qpre = 1;        // last sweep: epilogue input staged by a bulk copy issued with the spectrum loads
   int fin_split = -1;      // reductions finalized by a separate launch (-1: from 1024 partial slots on)
   int defer_x = 1;         // CG x update deferred into the next first sweep
@@ -244,6 +245,7 @@ struct fc_ctx {
   int pk_npen = 0;          // fused packed-coefficient first sweep: pencils per component (0: split)
   size_t smem_pk = 0;
   int outer_seq = 0;        // d = 3 outer sweep one component at a time
+  bool two_field = false;   // outer sweep stores t once, inverse middle sweep rebuilds xi1 t, xi2 t (MidGeo::rebuild)
   CUtensorMap tmW{};        // TMA view of the row-sweep spectrum (RowGeo::tma), first sweep's boxes
   CUtensorMap tmWi{};       // the same view with the last sweep's boxes (rgi)
   CUtensorMap tmP{};        // the same for the fused packed first sweep's row blocks (2 pk_npen rows)
@@ -680,6 +682,7 @@ int allow_reg_smem(int mx) {
       al(k_outer_r<LL, 2>);
       al(k_outer_r<LL, 3>);
       al(k_outer_seq<LL, 3>);
+      al(k_outer_seq<LL, 3, true>);
     });
   }
   return rc;
@@ -745,6 +748,7 @@ int make_row_tmap(fc_ctx* c) {
       mg.tma = 1;
     }
   }
+  c->two_field = c->dim == 3 && c->P == 1 && c->opt.two_field && c->mgi.tma && c->outer_qb && c->outer_seq && c->og.tma;
   return FC_OK;
 }
 
@@ -858,7 +862,8 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
     if (c->mid_bp) {
       const double2* tw = c->rtw(c->n[1]);
       const bool jf = c->opt.mid_map != 0;
-      const MidGeo& mt = inv ? c->mgi : mg;
+      MidGeo mt = inv ? c->mgi : mg;
+      mt.rebuild = inv && c->two_field;
       if ((inv || c->opt.mid_tma_fwd) && mt.tma) {
         // TMA on both sides (bulk pencil copies, tensor boxes on the transposed side)
         const int nt = mt.B * (c->n[1] / 9);
@@ -944,7 +949,8 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
       const int nt = c->outer_qb * (c->n0g / 9);
       const double2* tw = c->rtw(c->n0g);
       TRY(launch(c, "outer", [&] {
-        FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
+        if (c->two_field) FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3, true><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
+        else FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
       }));
     } else if (c->outer_qb) {
       const int nt = c->outer_qb * (c->n0g / 9);
@@ -1085,7 +1091,7 @@ int32_t fc_set_plan_option(const char* key, int32_t value) {
       {"force_generic", &o.force_generic}, {"row_threads", &o.row_threads}, {"row_threads_inv", &o.row_threads_inv}, {"mid_threads", &o.mid_threads},
       {"outer_threads", &o.outer_threads}, {"row_tma", &o.row_tma}, {"mid_tma", &o.mid_tma},
       {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"inv_pipe", &o.inv_pipe}, {"inv_qpre", &o.inv_qpre}, {"fin_split", &o.fin_split},
-      {"aniso_fused", &o.aniso_fused}, {"defer_x", &o.defer_x}, {"fused_exchange", &o.fused_exchange},
+      {"aniso_fused", &o.aniso_fused}, {"two_field", &o.two_field}, {"defer_x", &o.defer_x}, {"fused_exchange", &o.fused_exchange},
       {"sync_debug", &o.sync_debug}, {"mid_threads_inv", &o.mid_threads_inv}, {"mid_map", &o.mid_map},
       {"mid_tma_fwd", &o.mid_tma_fwd}};
   for (const auto& t : table)
@@ -1931,6 +1937,18 @@ int32_t fc_profile_reset(fc_ctx* c) {
   c->prof_idx.clear();
   return FC_OK;
 }
+int32_t fc_plan_info(fc_ctx* c, const char* key, int32_t* value) {
+  if (c == nullptr || key == nullptr || value == nullptr) return set_err(FC_EINVAL, "null argument");
+  const fc_ctx* p = c->sub.empty() ? c : c->sub[0];
+  const std::string k(key);
+  if (k == "two_field") *value = p->two_field;
+  else if (k == "packed_fused") *value = p->pk_npen > 0;
+  else if (k == "n_phases") *value = p->lab != nullptr ? p->nph : 0;
+  else if (k == "slabs") *value = c->sub.empty() ? 1 : (int32_t)c->sub.size();
+  else return set_err(FC_EINVAL, "unknown plan key %s", key);
+  return FC_OK;
+}
+
 int64_t fc_launch_count(fc_ctx* c) {
   if (c && !c->sub.empty()) {
     int64_t n = 0;

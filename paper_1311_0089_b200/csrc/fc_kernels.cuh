@@ -903,6 +903,7 @@ struct MidGeo {
   int n0, n1, h2, B, nib;
   int tma = 0;          // single slab: bulk pencil copies + TMA boxes on the transposed side
   int rows = 0, nbox = 0;  // box {2B doubles, rows modes}, nbox boxes per CTA
+  int rebuild = 0;         // inverse sweep: components 1, 2 = xi1 t, xi2 t from t in component 1's planes
 };
 
 template <bool INV>

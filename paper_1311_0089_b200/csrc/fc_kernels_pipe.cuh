@@ -158,7 +158,10 @@ __global__ void __launch_bounds__(256, 2) k_row_inv_pp(Geo g, RowGeo rg, EpArgs 
 // Gamma_hat from shared memory and transforms back.  Fewer registers, so more
 // resident warps than k_outer_r, for one extra shared-memory pass per
 // component.  Same arithmetic as k_outer_r.
-template <int L, int C>
+// TF (C = 3): two fields leave, F0^-1 (xi0 q) in row 0 and t = F0^-1 q in row 1; the
+// inverse middle sweep rebuilds xi1 t and xi2 t (the same g3_scale products) as it
+// loads them (MidGeo::rebuild), so row 2 is neither scaled nor stored here.
+template <int L, int C, bool TF = false>
 __global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, OuterGeo og, const RhsState* st,
                                                                       const double2* __restrict__ tw,
                                                                       double2* __restrict__ W) {
@@ -235,14 +238,18 @@ __global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, Oute
       } else {
 #pragma unroll
         for (int s = 0; s < 9; ++s) {
-          row1[j + s * TP] = g3_scale(xi1, v[0][s]);
-          row2[j + s * TP] = g3_scale(xi2, v[0][s]);
+          if constexpr (TF) {
+            row1[j + s * TP] = v[0][s];
+          } else {
+            row1[j + s * TP] = g3_scale(xi1, v[0][s]);
+            row2[j + s * TP] = g3_scale(xi2, v[0][s]);
+          }
         }
         fence_proxy_async();
         __syncthreads();
         if (threadIdx.x == 0) {
 #pragma unroll
-          for (int b = 1; b < C; ++b)
+          for (int b = 1; b < (TF ? 2 : C); ++b)
             bulk_s2g(W + ((int64_t)(r * C + b) * og.Q + (int64_t)qb * og.QB) * L, sm + (size_t)b * og.QB * L,
                      (unsigned)(nq * L * 16));
           bulk_commit();

@@ -396,6 +396,8 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 3 : (NT <= 384 ? 2 : 1)) k_row
   if (last) finalize_block(ea.fin, red);
 }
 
+__device__ __forceinline__ double2 g3_scale(double xi, double2 v);  // defined below
+
 // Middle sweep through TMA (one slab).  Pencil side (W1[rc][i0][k2][:], one
 // contiguous row of L modes per i0): one bulk copy per pencil.  Transposed side
 // (W2[rc][k2][k1][i0]): tensor boxes {2 BP doubles, rows modes} = BP consecutive
@@ -406,22 +408,21 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 3 : (NT <= 384 ? 2 : 1)) k_row
 template <int L, bool INV, bool JF>
 __device__ __forceinline__ void mid_tma(const Geo& g, const MidGeo& mg, const RhsState* st,
                                         const double2* __restrict__ tw, const double2* __restrict__ src,
-                                        double2* __restrict__ dst, const CUtensorMap& tmM, double2* sm) {
+                                        double2* __restrict__ dst, const CUtensorMap& tmM, double2* sm,
+                                        int ib, int k2, int a, int r) {
   constexpr int TP = RegTP<L>::value;
   const int c = g.dim;
-  int64_t bid = blockIdx.x;
-  const int ib = bid % mg.nib; bid /= mg.nib;
-  const int k2 = bid % mg.h2; bid /= mg.h2;
-  const int a = bid % c;
-  const int r = (int)(bid / c);
-  if (!rhs_active(st, r)) return;
   const int BP = mg.B;
   const int p = JF ? threadIdx.x / TP : threadIdx.x % BP;
   const int j = JF ? threadIdx.x - p * TP : threadIdx.x / BP;
   const int i00 = ib * BP;
   const int np_ = min(BP, mg.n0 - i00);  // live pencils
   const int rc = r * c + a;
-  const int cz = rc * mg.h2 + k2;        // tensor coordinate of the (rc, k2) plane
+  // mg.rebuild (inverse sweep behind k_outer_seq<L, 3, true>): the outer sweep left
+  // t = F0^-1 q in component 1's planes instead of xi1 t and xi2 t in planes 1 and
+  // 2; both components are rebuilt from it on the way into the registers
+  const bool reb = INV && mg.rebuild && a >= 1;
+  const int cz = (reb ? r * c + 1 : rc) * mg.h2 + k2;  // tensor coordinate of the source plane
   const double2* pen = (INV ? dst : src) + (((int64_t)rc * mg.n0 + i00) * mg.h2 + k2) * L;  // pencil p at + p*h2*L
   const int64_t pstride = (int64_t)mg.h2 * L;
   __shared__ uint64_t bar;
@@ -445,6 +446,7 @@ __device__ __forceinline__ void mid_tma(const Geo& g, const MidGeo& mg, const Rh
   for (int s = 0; s < 9; ++s) {
     const int i = j + s * TP;
     v[0][s] = INV ? sm[(size_t)i * BP + p] : sm[(size_t)p * L + i];
+    if (reb) v[0][s] = g3_scale(a == 1 ? g.xi[1][i] : g.xi[2][k2], v[0][s]);
   }
   fft_reg<L, 1, INV>(v, sm + (size_t)p * L, L, j, tw);
   trace_stamp(INV ? 4 : 2, 2);
@@ -476,7 +478,19 @@ __global__ void __launch_bounds__(kMaxBlock) k_mid_tma(Geo g, MidGeo mg, const R
                                                         const double2* __restrict__ tw, const double2* __restrict__ src,
                                                         double2* __restrict__ dst, const __grid_constant__ CUtensorMap tmM) {
   extern __shared__ __align__(128) unsigned char smraw[];
-  mid_tma<L, INV, JF>(g, mg, st, tw, src, dst, tmM, reinterpret_cast<double2*>(smraw));
+  int64_t bid = blockIdx.x;
+  int a = 0;
+  if (INV && mg.rebuild) {  // the CTAs of components 1 and 2 read the same planes: side by side (L2)
+    a = bid % g.dim; bid /= g.dim;
+  }
+  const int ib = bid % mg.nib; bid /= mg.nib;
+  const int k2 = bid % mg.h2; bid /= mg.h2;
+  if (!(INV && mg.rebuild)) {
+    a = bid % g.dim; bid /= g.dim;
+  }
+  const int r = (int)bid;
+  if (!rhs_active(st, r)) return;
+  mid_tma<L, INV, JF>(g, mg, st, tw, src, dst, tmM, reinterpret_cast<double2*>(smraw), ib, k2, a, r);
 }
 
 // Middle sweep (d = 3), thread mapping pencil-fastest (t = j * BP + p) so the

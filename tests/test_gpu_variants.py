@@ -101,12 +101,48 @@ def test_mid_sweep_variants_3d(shape):
         return reps[0]["iterations"], x
 
     it0, x0 = run({})
-    for opts in ({"mid_tma": 0}, {"outer_threads": 256}, {"outer_tma": 0}, {"outer_seq": 1}, {"outer_seq": 0}, {"mid_map": 0},
+    for opts in ({"two_field": 0}, {"mid_tma": 0}, {"outer_threads": 256}, {"outer_tma": 0}, {"outer_seq": 1}, {"outer_seq": 0}, {"mid_map": 0},
                  {"mid_tma_fwd": 0}, {"mid_map": 0, "mid_tma_fwd": 0}, {"mid_threads": 512, "mid_threads_inv": 512},
                  {"mid_threads": 81, "mid_threads_inv": 162}):
         it, x = run(opts)
         assert it == it0, opts
         assert np.array_equal(x, x0), (opts, rel_l2(x, x0))
+
+
+@pytest.mark.parametrize("shape", [(81, 81, 27), (243, 81, 81), (45, 135, 27), (729, 243, 27), (35, 243, 81)])
+def test_two_field_sweeps_match_three_field(shape):
+    """d = 3, one slab: the outer sweep stores t = F0^-1 q once instead of xi1 t and
+    xi2 t, and the inverse middle sweep rebuilds both components from it as it loads
+    them (two_field = 1, the default: 8 bytes per voxel less written and, with the two
+    components' CTAs side by side, read).  Same products in the same order as the
+    three-field sweeps: CG with several loads, the fixed point and both projectors
+    agree bit for bit.  Shapes: power-of-three and radix-5 middle and outer axes,
+    ragged pencil blocks, and an outer axis off the register path (35: two_field
+    stays off, the option must be harmless)."""
+    from conftest import random_spd_packed
+    from paper_1311_0089_b200 import CoefficientField
+
+    spec = GridSpec((1.0, 0.7, 1.3), shape)
+    rng = np.random.default_rng(5)
+    coef = CoefficientField(spec, random_spd_packed(shape, rng))
+    E = np.array([[1.0, 0.0, 0.0], [0.0, 1.0, 0.0], [0.3, 0.4, 0.5]])
+    u = rng.standard_normal((2, 3) + shape)
+    ref = np.array([[2.0, 0.3, 0.1], [0.3, 3.0, 0.2], [0.1, 0.2, 4.0]])
+
+    def run(opts):
+        with _native.plan_options(**opts):
+            ctx = _native.Context(spec)
+        ctx.set_coefficients(coef)
+        reps, x, hist = ctx.solve_cg(E, 1e-8, 60)
+        freps, fx = ctx.solve_fixed_point(E[:2], 1e-6, 25, np.diag([4.0, 5.0, 6.0]), np.ones(2))
+        return ([r["iterations"] for r in reps], x, hist, [r["iterations"] for r in freps], fx,
+                ctx.project(0, None, u), ctx.project(1, ref, u), ctx.apply_system(u))
+
+    two = run({})
+    three = run({"two_field": 0})
+    assert two[0] == three[0] and two[3] == three[3]
+    for k in (1, 2, 4, 5, 6, 7):
+        assert np.array_equal(two[k], three[k]), (k, rel_l2(two[k], three[k]))
 
 
 @pytest.mark.parametrize("shape", [(27, 27, 81), (81, 81, 729), (45, 27, 405)])
