@@ -244,6 +244,7 @@ class Workload:
         # outer sweep storing F0^-1 q once (plan two_field): one spectrum word per voxel
         # and RHS less written, and one less read by the inverse middle sweep
         self.two_field = bool(ctx.plan_info("two_field")) if hasattr(ctx, "plan_info") else False
+        self.fold_fwd = bool(ctx.plan_info("fold_fwd")) if hasattr(ctx, "plan_info") else False
         return self.nA
 
     # ---- byte model ----------------------------------------------
@@ -251,7 +252,8 @@ class Workload:
         """Fixed SURVEY model per CG iteration (B_iter) or fixed-point iteration (B_fp)."""
         c, R, S = self.d, self.R, 2 * self.d - 1
         extra = c * R if self.method == "fixed_point" else 9 * c * R
-        return W * self.N * (self.nA + 2 * S * c * R + extra - (2 * R if getattr(self, "two_field", False) else 0))
+        return W * self.N * (self.nA + 2 * S * c * R + extra - (2 * R if getattr(self, "two_field", False) else 0)
+                                 - (2 * R if getattr(self, "fold_fwd", False) else 0))
 
     def launch_words(self, kernel, phase, split):
         """(coefficient words read once per launch, words per active RHS) per voxel.
@@ -269,6 +271,9 @@ class Workload:
             return first_sweep[phase]
         if kernel == "row_fwd":
             return (0, 2 * c) if split else first_sweep[phase]
+        if getattr(self, "fold_fwd", False) and kernel in ("mid_fwd", "outer"):
+            # mid_fwd: c fields in, v0 and the folded u = xi1 v1 + xi2 v2 out; outer: 2 in, 2 out
+            return (0, 2 * c - 1) if kernel == "mid_fwd" else (0, 2 * c - 2)
         if kernel in ("outer", "mid_inv") and getattr(self, "two_field", False):
             # outer: c fields in, F0^-1 (xi0 q) and t = F0^-1 q out; mid_inv: those two in
             # (t feeds components 1 and 2: ncu sees it come from DRAM once), c fields out

@@ -158,6 +158,7 @@ struct PlanOpts {
   int mid_tma_fwd = 1;     // forward middle sweep through TMA boxes (0: per-thread transposed stores)
   int aniso_fused = 1;     // packed coefficients: fused first sweep (0: pointwise kernel + row FFT)
   int two_field = 1;       // d = 3, one slab: two spectrum fields from the outer to the inverse middle sweep
+  int fold_fwd = -1;       // ... and from the forward middle sweep to the outer sweep (needs two_field; -1: middle pencils >= 729)
   int inv_qpre = 1;        // last sweep: epilogue input staged by a bulk copy issued with the spectrum loads
   int fin_split = -1;      // reductions finalized by a separate launch (-1: from 1024 partial slots on)
   int defer_x = 1;         // CG x update deferred into the next first sweep
@@ -246,6 +247,7 @@ struct fc_ctx {
   size_t smem_pk = 0;
   int outer_seq = 0;        // d = 3 outer sweep one component at a time
   bool two_field = false;   // outer sweep stores t once, inverse middle sweep rebuilds xi1 t, xi2 t (MidGeo::rebuild)
+  bool fold_fwd = false;    // forward middle sweep stores u = xi1 v1 + xi2 v2 (mid_tma_fold)
   CUtensorMap tmW{};        // TMA view of the row-sweep spectrum (RowGeo::tma), first sweep's boxes
   CUtensorMap tmWi{};       // the same view with the last sweep's boxes (rgi)
   CUtensorMap tmP{};        // the same for the fused packed first sweep's row blocks (2 pk_npen rows)
@@ -591,7 +593,8 @@ int choose_tiles(fc_ctx* c) {
     // packed coefficients: fused first sweep (fc_kernels_pk.cuh), d components of
     // npk pencils per CTA (<= 256 threads), if two CTAs fit an SM
     if (op.aniso_fused && d >= 2) {
-      const int npk = std::max(1, std::min((rg.np + 1) / 2, 256 / (d * TP)));
+      // (a tensor box holds 4 npk doubles per row: at most 256, so npk <= 64)
+      const int npk = std::max(1, std::min((rg.np + 1) / 2, std::min(64, 256 / (d * TP))));
       const size_t sm = pk_smem(rg.nl, d, npk, rg.nbox, rg.boxK);
       if (d * TP <= 256 && 2 * (sm + 1024) <= (size_t)c->smem_optin + 1024 && sm <= 110 * 1024) {
         c->pk_npen = npk;
@@ -683,6 +686,9 @@ int allow_reg_smem(int mx) {
       al(k_outer_r<LL, 3>);
       al(k_outer_seq<LL, 3>);
       al(k_outer_seq<LL, 3, true>);
+      al(k_outer_seq<LL, 3, true, true>);
+      al(k_mid_tma_fold<LL, false>);
+      al(k_mid_tma_fold<LL, true>);
     });
   }
   return rc;
@@ -749,6 +755,9 @@ int make_row_tmap(fc_ctx* c) {
     }
   }
   c->two_field = c->dim == 3 && c->P == 1 && c->opt.two_field && c->mgi.tma && c->outer_qb && c->outer_seq && c->og.tma;
+  // (long pencils only: at 243 the folding sweep loses more than the outer sweep gains)
+  c->fold_fwd = c->two_field && c->mg.tma && c->opt.mid_tma_fwd &&
+                (c->opt.fold_fwd >= 0 ? c->opt.fold_fwd != 0 : c->n[1] / 9 >= 81);
   return FC_OK;
 }
 
@@ -864,6 +873,16 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
       const bool jf = c->opt.mid_map != 0;
       MidGeo mt = inv ? c->mgi : mg;
       mt.rebuild = inv && c->two_field;
+      if (!inv && c->fold_fwd) {
+        const int nt = mt.B * (c->n[1] / 9);
+        const int64_t nblk = (int64_t)R * 2 * mt.h2 * mt.nib;
+        mt.regA = (int)(c->smem_mid_r / 16);
+        const size_t smem = 2 * c->smem_mid_r;  // pencils of component 1 | pencils of component 2, then the boxes
+        return launch(c, "mid_fwd", [&] {
+          if (jf) FC_POW3_SWITCH(c->n[1], (k_mid_tma_fold<LL, true><<<(unsigned)nblk, nt, smem, s>>>(g, mt, st, tw, src, dst, c->tmM)))
+          else FC_POW3_SWITCH(c->n[1], (k_mid_tma_fold<LL, false><<<(unsigned)nblk, nt, smem, s>>>(g, mt, st, tw, src, dst, c->tmM)))
+        });
+      }
       if ((inv || c->opt.mid_tma_fwd) && mt.tma) {
         // TMA on both sides (bulk pencil copies, tensor boxes on the transposed side)
         const int nt = mt.B * (c->n[1] / 9);
@@ -949,7 +968,10 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
       const int nt = c->outer_qb * (c->n0g / 9);
       const double2* tw = c->rtw(c->n0g);
       TRY(launch(c, "outer", [&] {
-        if (c->two_field) FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3, true><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
+        // folded input: rows 0 and 1 only (three CTAs fit an SM)
+        const size_t sm2 = FC_OUTER_TFI_OCC3 ? c->smem_outer_r / 3 * 2 : c->smem_outer_r;
+        if (c->fold_fwd) FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3, true, true><<<(unsigned)(R * og.nqb), nt, sm2, s>>>(g, og, st, tw, Wout)))
+        else if (c->two_field) FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3, true><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
         else FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
       }));
     } else if (c->outer_qb) {
@@ -1091,7 +1113,7 @@ int32_t fc_set_plan_option(const char* key, int32_t value) {
       {"force_generic", &o.force_generic}, {"row_threads", &o.row_threads}, {"row_threads_inv", &o.row_threads_inv}, {"mid_threads", &o.mid_threads},
       {"outer_threads", &o.outer_threads}, {"row_tma", &o.row_tma}, {"mid_tma", &o.mid_tma},
       {"outer_tma", &o.outer_tma}, {"outer_seq", &o.outer_seq}, {"inv_pipe", &o.inv_pipe}, {"inv_qpre", &o.inv_qpre}, {"fin_split", &o.fin_split},
-      {"aniso_fused", &o.aniso_fused}, {"two_field", &o.two_field}, {"defer_x", &o.defer_x}, {"fused_exchange", &o.fused_exchange},
+      {"aniso_fused", &o.aniso_fused}, {"two_field", &o.two_field}, {"fold_fwd", &o.fold_fwd}, {"defer_x", &o.defer_x}, {"fused_exchange", &o.fused_exchange},
       {"sync_debug", &o.sync_debug}, {"mid_threads_inv", &o.mid_threads_inv}, {"mid_map", &o.mid_map},
       {"mid_tma_fwd", &o.mid_tma_fwd}};
   for (const auto& t : table)
@@ -1942,6 +1964,7 @@ int32_t fc_plan_info(fc_ctx* c, const char* key, int32_t* value) {
   const fc_ctx* p = c->sub.empty() ? c : c->sub[0];
   const std::string k(key);
   if (k == "two_field") *value = p->two_field;
+  else if (k == "fold_fwd") *value = p->fold_fwd;
   else if (k == "packed_fused") *value = p->pk_npen > 0;
   else if (k == "n_phases") *value = p->lab != nullptr ? p->nph : 0;
   else if (k == "slabs") *value = c->sub.empty() ? 1 : (int32_t)c->sub.size();

@@ -904,6 +904,7 @@ struct MidGeo {
   int tma = 0;          // single slab: bulk pencil copies + TMA boxes on the transposed side
   int rows = 0, nbox = 0;  // box {2B doubles, rows modes}, nbox boxes per CTA
   int rebuild = 0;         // inverse sweep: components 1, 2 = xi1 t, xi2 t from t in component 1's planes
+  int regA = 0;            // forward fold: elements of the first shared-memory region (pencils / boxes)
 };
 
 template <bool INV>

@@ -161,14 +161,20 @@ __global__ void __launch_bounds__(256, 2) k_row_inv_pp(Geo g, RowGeo rg, EpArgs 
 // TF (C = 3): two fields leave, F0^-1 (xi0 q) in row 0 and t = F0^-1 q in row 1; the
 // inverse middle sweep rebuilds xi1 t and xi2 t (the same g3_scale products) as it
 // loads them (MidGeo::rebuild), so row 2 is neither scaled nor stored here.
-template <int L, int C, bool TF = false>
-__global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, OuterGeo og, const RhsState* st,
+#ifndef FC_OUTER_TFI_OCC3
+#define FC_OUTER_TFI_OCC3 1  // TFI: two shared-memory rows and <= 84 registers, three resident CTAs per SM
+#endif
+// TFI (C = 3): the forward middle sweep folded components 1 and 2 (mid_tma_fold):
+// row 1 holds u = xi1 v1 + xi2 v2 already, row 2 is not loaded.
+template <int L, int C, bool TF = false, bool TFI = false>
+__global__ void __launch_bounds__(256, (C == 2 || (TFI && FC_OUTER_TFI_OCC3) ? 3 : 2)) k_outer_seq(Geo g, OuterGeo og, const RhsState* st,
                                                                       const double2* __restrict__ tw,
                                                                       double2* __restrict__ W) {
   constexpr int TP = RegTP<L>::value;
   extern __shared__ __align__(128) unsigned char smraw[];
   double2* sm = reinterpret_cast<double2*>(smraw);
   __shared__ uint64_t bar;
+  __shared__ int zero;  // TFI: read per transform so ptxas cannot hoist the next transform's twiddle loads
   const int qb = blockIdx.x % og.nqb;
   const int r = blockIdx.x / og.nqb;
   if (!rhs_active(st, r)) return;
@@ -179,10 +185,12 @@ __global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, Oute
   const int nq = min(og.QB, og.Q - qb * og.QB);
   trace_stamp(3, 0);
   if (threadIdx.x == 0) {
+    zero = 0;
     mbar_init(&bar, 1);
-    mbar_expect_tx(&bar, (unsigned)(C * nq * L * 16));
+    constexpr int NIN = TFI ? 2 : C;
+    mbar_expect_tx(&bar, (unsigned)(NIN * nq * L * 16));
 #pragma unroll
-    for (int a = 0; a < C; ++a)
+    for (int a = 0; a < NIN; ++a)
       bulk_g2s(sm + (size_t)a * og.QB * L, W + ((int64_t)(r * C + a) * og.Q + (int64_t)qb * og.QB) * L,
                (unsigned)(nq * L * 16), &bar);
   }
@@ -205,9 +213,9 @@ __global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, Oute
 #pragma unroll
       for (int s = 0; s < 9; ++s) {
         const int i = j + s * TP;
-        v[0][s] = !live ? make_double2(0.0, 0.0) : a == 0 ? row0[i] : g3_fold(xi1, xi2, row1[i], row2[i]);
+        v[0][s] = !live ? make_double2(0.0, 0.0) : a == 0 ? row0[i] : TFI ? row1[i] : g3_fold(xi1, xi2, row1[i], row2[i]);
       }
-      fft_reg<L, 1, false>(v, a == 0 ? row0 : row1, L, j, tw);
+      fft_reg<L, 1, false>(v, a == 0 ? row0 : row1, L, j, (TFI && FC_OUTER_TFI_OCC3) ? tw + *reinterpret_cast<volatile int*>(&zero) : tw);
       if (a == 0) {
         __syncthreads();
 #pragma unroll
@@ -230,7 +238,7 @@ __global__ void __launch_bounds__(256, (C == 2 ? 3 : 2)) k_outer_seq(Geo g, Oute
 #pragma unroll
         for (int s = 0; s < 9; ++s) v[0][s] = row0[j + s * TP];
       }
-      fft_reg<L, 1, true>(v, a == 0 ? row0 : row1, L, j, tw);
+      fft_reg<L, 1, true>(v, a == 0 ? row0 : row1, L, j, (TFI && FC_OUTER_TFI_OCC3) ? tw + *reinterpret_cast<volatile int*>(&zero) : tw);
       __syncthreads();
       if (a == 0) {
 #pragma unroll

@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 3 : (NT <= 384 ? 2 : 1)) k_row
 }
 
 __device__ __forceinline__ double2 g3_scale(double xi, double2 v);  // defined below
+__device__ __forceinline__ double2 g3_fold(double xi1, double xi2, double2 v1, double2 v2);
 
 // Middle sweep through TMA (one slab).  Pencil side (W1[rc][i0][k2][:], one
 // contiguous row of L modes per i0): one bulk copy per pencil.  Transposed side
@@ -491,6 +492,90 @@ __global__ void __launch_bounds__(kMaxBlock) k_mid_tma(Geo g, MidGeo mg, const R
   const int r = (int)bid;
   if (!rhs_active(st, r)) return;
   mid_tma<L, INV, JF>(g, mg, st, tw, src, dst, tmM, reinterpret_cast<double2*>(smraw), ib, k2, a, r);
+}
+
+// Forward middle sweep that folds components 1 and 2 (MidGeo::fold, with
+// k_outer_seq<L, 3, *, true>).  Gamma_hat needs xi . v_hat = xi0 v0 + (xi1 v1 + xi2 v2);
+// once axes 2 and 1 are transformed xi1 (k1) and xi2 (k2) are known, so this sweep
+// stores u = xi1 F1 v1 + xi2 F1 v2 (g3_fold: the products and the sum the outer sweep
+// would form after loading both fields) in component 1's planes of W2 and nothing
+// in component 2's.  One CTA, components one after the other (nine complex in
+// registers at a time, as mid_tma): both pencil sets are fetched at the start, F1 v1
+// is parked transposed in shared memory by the thread that will fold it.
+template <int L, bool JF>
+__device__ __forceinline__ void mid_tma_fold(const Geo& g, const MidGeo& mg, const double2* __restrict__ tw,
+                                             const double2* __restrict__ src, const CUtensorMap& tmM, double2* sm,
+                                             int ib, int k2, int r) {
+  constexpr int TP = RegTP<L>::value;
+  const int BP = mg.B;
+  const int p = JF ? threadIdx.x / TP : threadIdx.x % BP;
+  const int j = JF ? threadIdx.x - p * TP : threadIdx.x / BP;
+  const int i00 = ib * BP;
+  const int np_ = min(BP, mg.n0 - i00);
+  const int rc1 = r * 3 + 1;
+  const int cz1 = rc1 * mg.h2 + k2;
+  const double2* pen1 = src + (((int64_t)rc1 * mg.n0 + i00) * mg.h2 + k2) * L;
+  const double2* pen2 = pen1 + (int64_t)mg.n0 * mg.h2 * L;
+  const int64_t pstride = (int64_t)mg.h2 * L;
+  double2* smB = sm + mg.regA;  // component 2's pencils, behind the box region
+  __shared__ uint64_t bar;
+  __shared__ int zero;
+  if (threadIdx.x == 0) {
+    zero = 0;
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, (unsigned)(2 * np_ * L * 16));
+    for (int q = 0; q < np_; ++q) bulk_g2s(sm + (size_t)q * L, pen1 + q * pstride, (unsigned)(L * 16), &bar);
+    for (int q = 0; q < np_; ++q) bulk_g2s(smB + (size_t)q * L, pen2 + q * pstride, (unsigned)(L * 16), &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  double2 v[1][9];
+  const double xi2 = g.xi[2][k2];
+#pragma unroll 1
+  for (int a = 0; a < 2; ++a) {  // one transform body: registers as mid_tma
+    double2* pen = (a == 0 ? sm : smB) + (size_t)p * L;
+    // ptxas would hoist the second transform's 16 twiddle loads (64 registers) above
+    // the first transform to hide their latency, doubling the registers per thread:
+    // tie the table's address to a shared-memory word read in this iteration
+    const double2* twa = tw + *reinterpret_cast<volatile int*>(&zero);
+#pragma unroll
+    for (int s = 0; s < 9; ++s) v[0][s] = pen[j + s * TP];
+    fft_reg<L, 1, false>(v, pen, L, j, twa);
+    __syncthreads();  // this component's exchange buffers are free
+    if (a == 0) {     // park F1 v1 in the pencil's own row (conflict-free, read back by this thread)
+#pragma unroll
+      for (int s = 0; s < 9; ++s) pen[j + s * TP] = v[0][s];
+    } else {          // fold and store transposed into component 2's region
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+        const int i = j + s * TP;
+        smB[(size_t)i * BP + p] = g3_fold(g.xi[1][i], xi2, sm[(size_t)p * L + i], v[0][s]);
+      }
+    }
+  }
+  sm = smB;  // the boxes leave from component 2's region
+  fence_proxy_async();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < mg.nbox; ++b) tma_store_3d(&tmM, 2 * i00, b * mg.rows, cz1, sm + (size_t)b * mg.rows * BP);
+    bulk_commit();
+    bulk_wait_read0();
+  }
+}
+
+template <int L, bool JF>
+__global__ void __launch_bounds__(kMaxBlock) k_mid_tma_fold(Geo g, MidGeo mg, const RhsState* st,
+                                                             const double2* __restrict__ tw, const double2* __restrict__ src,
+                                                             double2* __restrict__ dst, const __grid_constant__ CUtensorMap tmM) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  int64_t bid = blockIdx.x;
+  const int ib = bid % mg.nib; bid /= mg.nib;
+  const int k2 = bid % mg.h2; bid /= mg.h2;
+  const int ap = bid % 2;
+  const int r = (int)(bid / 2);
+  if (!rhs_active(st, r)) return;
+  if (ap == 0) mid_tma<L, false, JF>(g, mg, st, tw, src, dst, tmM, reinterpret_cast<double2*>(smraw), ib, k2, 0, r);
+  else mid_tma_fold<L, JF>(g, mg, tw, src, tmM, reinterpret_cast<double2*>(smraw), ib, k2, r);
 }
 
 // Middle sweep (d = 3), thread mapping pencil-fastest (t = j * BP + p) so the
