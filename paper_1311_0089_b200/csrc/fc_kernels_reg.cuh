@@ -563,8 +563,15 @@ __device__ __forceinline__ void mid_tma_fold(const Geo& g, const MidGeo& mg, con
   }
 }
 
+// CTA size the folding sweep is compiled for (the planner's defaults: 256 threads for
+// pencils <= 243, two pencils above) and the resident CTAs that keep it at <= 84 registers
+__host__ __device__ constexpr int fold_threads(int L) { return L / 9 <= 27 ? 256 : (2 * (L / 9) + 31) / 32 * 32; }
+__host__ __device__ constexpr int fold_ctas(int L) {
+  return 65536 / (84 * fold_threads(L)) < 1 ? 1 : (65536 / (84 * fold_threads(L)) > 4 ? 4 : 65536 / (84 * fold_threads(L)));
+}
+
 template <int L, bool JF>
-__global__ void __launch_bounds__(kMaxBlock) k_mid_tma_fold(Geo g, MidGeo mg, const RhsState* st,
+__global__ void __launch_bounds__(fold_threads(L), fold_ctas(L)) k_mid_tma_fold(Geo g, MidGeo mg, const RhsState* st,
                                                              const double2* __restrict__ tw, const double2* __restrict__ src,
                                                              double2* __restrict__ dst, const __grid_constant__ CUtensorMap tmM) {
   extern __shared__ __align__(128) unsigned char smraw[];
