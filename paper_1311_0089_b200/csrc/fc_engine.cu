@@ -642,7 +642,7 @@ int choose_tiles(fc_ctx* c) {
     og.tma = op.outer_tma;
     // d = 3 with long pencils: one component at a time (measured at 729^3: -19 %;
     // slower for the small 243-length CTAs and for d = 2)
-    c->outer_seq = d == 3 && (op.outer_seq >= 0 ? op.outer_seq : TP >= 27);
+    c->outer_seq = d == 3 ? (op.outer_seq >= 0 ? op.outer_seq : TP >= 27) : (d == 2 && op.outer_seq > 0);
   }
   return FC_OK;
 }
@@ -684,6 +684,7 @@ int allow_reg_smem(int mx) {
       al(k_mid_tma<LL, false, true>);
       al(k_outer_r<LL, 2>);
       al(k_outer_r<LL, 3>);
+      al(k_outer_seq<LL, 2>);
       al(k_outer_seq<LL, 3>);
       al(k_outer_seq<LL, 3, true>);
       al(k_outer_seq<LL, 3, true, true>);
@@ -970,7 +971,8 @@ int run_phases(fc_ctx* c, int phases, int R, const InArgs& ia, EpArgs ea, int or
       TRY(launch(c, "outer", [&] {
         // folded input: rows 0 and 1 only (three CTAs fit an SM)
         const size_t sm2 = FC_OUTER_TFI_OCC3 ? c->smem_outer_r / 3 * 2 : c->smem_outer_r;
-        if (c->fold_fwd) FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3, true, true><<<(unsigned)(R * og.nqb), nt, sm2, s>>>(g, og, st, tw, Wout)))
+        if (d == 2) FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 2><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
+        else if (c->fold_fwd) FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3, true, true><<<(unsigned)(R * og.nqb), nt, sm2, s>>>(g, og, st, tw, Wout)))
         else if (c->two_field) FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3, true><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
         else FC_POW3_SWITCH(c->n0g, (k_outer_seq<LL, 3><<<(unsigned)(R * og.nqb), nt, c->smem_outer_r, s>>>(g, og, st, tw, Wout)))
       }));

@@ -276,72 +276,46 @@ __global__ void __launch_bounds__(256, (C == 2 || (TFI && FC_OUTER_TFI_OCC3) ? 3
     }
     return;
   } else {
+  // d = 2: F0 v0 parked in its row (every thread its own nine modes), F0 v1 stays in
+  // registers; Gamma_hat there (g2_mode, as k_outer_r<L, 2>); xi1 q is transformed back
+  // at once, then xi0 q.  One transform body at a time: <= 84 registers, three CTAs
+  // per SM (the twiddle table's address is tied to a shared-memory word per transform,
+  // or ptxas hoists the next transform's loads and doubles the registers).
+  static_assert(C == 2, "d = 3 takes the branch above");
+  double2* row0 = sm + ((size_t)0 * og.QB + qq) * L;
+  double2* row1 = sm + ((size_t)1 * og.QB + qq) * L;
+  double2 v[1][9];
 #pragma unroll 1
-  for (int a = 0; a < C; ++a) {  // forward transforms, spectra back in place
-    double2* row = sm + ((size_t)a * og.QB + qq) * L;
-    double2 v[1][9];
+  for (int a = 0; a < 2; ++a) {
+    double2* row = a == 0 ? row0 : row1;
 #pragma unroll
     for (int s = 0; s < 9; ++s) v[0][s] = live ? row[j + s * TP] : make_double2(0.0, 0.0);
-    fft_reg<L, 1, false>(v, row, L, j, tw);
-    __syncthreads();
+    fft_reg<L, 1, false>(v, row, L, j, tw + *reinterpret_cast<volatile int*>(&zero));
+    if (a == 0) {
+      __syncthreads();
 #pragma unroll
-    for (int s = 0; s < 9; ++s) row[j + s * TP] = v[0][s];
-  }
-  __syncthreads();
-  if (live) {  // Gamma_hat(k) v = xi (xi . v) / den, 0 at k = 0 (per thread: its own modes)
-    const int q = ql;
-    double xi1 = 0.0, xi2 = 0.0;
-    if (C == 2) {
-      xi1 = g.xi[1][q];
-    } else {
-      const int k2 = q / og.n1, k1 = q - k2 * og.n1;
-      xi1 = g.xi[1][k1];
-      xi2 = g.xi[2][k2];
+      for (int s = 0; s < 9; ++s) row0[j + s * TP] = v[0][s];
     }
+  }
+  {
+    const double xi1 = g.xi[1][live ? ql : 0];
+    const bool qzero = live && ql == 0;
 #pragma unroll
     for (int s = 0; s < 9; ++s) {
       const int i0 = j + s * TP;
-      double2 v[C];
-#pragma unroll
-      for (int a = 0; a < C; ++a) v[a] = sm[((size_t)a * og.QB + qq) * L + i0];
-      const double xi[3] = {g.xi[0][i0], xi1, xi2};
-      double2 out[C];
-      if (q == 0 && i0 == 0) {
-#pragma unroll
-        for (int a = 0; a < C; ++a) out[a] = make_double2(0.0, 0.0);
-      } else {
-        double2 dots = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int a = 0; a < C; ++a) {
-          dots.x += xi[a] * v[a].x;
-          dots.y += xi[a] * v[a].y;
-        }
-        double den = 0.0;
-        if (og.orth) {
-#pragma unroll
-          for (int a = 0; a < C; ++a) den += xi[a] * xi[a];
-        } else {
-#pragma unroll
-          for (int a = 0; a < C; ++a)
-#pragma unroll
-            for (int b = 0; b < C; ++b) den += xi[a] * og.M[a][b] * xi[b];
-        }
-        const double inv = 1.0 / den;
-        const double2 qv = make_double2(dots.x * inv, dots.y * inv);
-#pragma unroll
-        for (int a = 0; a < C; ++a) out[a] = make_double2(xi[a] * qv.x, xi[a] * qv.y);
-      }
-#pragma unroll
-      for (int a = 0; a < C; ++a) sm[((size_t)a * og.QB + qq) * L + i0] = out[a];
+      double2 t0 = row0[i0];
+      g2_mode(og, g.xi[0][i0], xi1, qzero && i0 == 0, t0, v[0][s]);
+      row0[i0] = t0;
     }
   }
 #pragma unroll 1
-  for (int a = 0; a < C; ++a) {  // inverse transforms (each thread reads the modes it wrote)
-    double2* row = sm + ((size_t)a * og.QB + qq) * L;
-    double2 v[1][9];
+  for (int a = 1; a >= 0; --a) {
+    double2* row = a == 0 ? row0 : row1;
+    if (a == 0) {
 #pragma unroll
-    for (int s = 0; s < 9; ++s) v[0][s] = row[j + s * TP];
-    fft_reg<L, 1, true>(v, row, L, j, tw);
+      for (int s = 0; s < 9; ++s) v[0][s] = row0[j + s * TP];
+    }
+    fft_reg<L, 1, true>(v, row, L, j, tw + *reinterpret_cast<volatile int*>(&zero));
     __syncthreads();
 #pragma unroll
     for (int s = 0; s < 9; ++s) row[j + s * TP] = v[0][s];

@@ -72,6 +72,8 @@ def test_default_path_matches_oracle(medium, default_solve):
     {"inv_pipe": 0},
     {"defer_x": 0},
     {"defer_x": 0, "inv_pipe": 0},
+    {"outer_seq": 1},
+    {"outer_seq": 0},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_variant_is_bitwise_identical(medium, default_solve, opts):
     its0, x0 = default_solve
