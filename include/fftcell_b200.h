@@ -215,7 +215,7 @@ int32_t fc_profile_get(fc_ctx* ctx, int32_t i, char* name, int32_t name_cap, int
 int32_t fc_profile_reset(fc_ctx* ctx);
 int64_t fc_launch_count(fc_ctx* ctx);
 /* What the context's plan selected (no reference counterpart; the bench's byte model reads it):
- * "two_field", "packed_fused", "n_phases" (0: full field resident), "slabs". */
+ * "two_field", "fold_fwd", "packed_fused", "n_phases" (0: full field resident), "slabs". */
 int32_t fc_plan_info(fc_ctx* ctx, const char* key, int32_t* value);
 /* CUDA-event timers on the context's stream: mark slot (0..7); elapsed between two marks (syncs on b). */
 int32_t fc_timer_mark(fc_ctx* ctx, int32_t slot);

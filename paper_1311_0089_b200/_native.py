@@ -255,7 +255,7 @@ class Context:
         self.isotropic = kind == 0
 
     def plan_info(self, key):
-        """What the plan selected: "two_field", "packed_fused", "n_phases", "slabs"."""
+        """What the plan selected: "two_field", "fold_fwd", "packed_fused", "n_phases", "slabs"."""
         v = ctypes.c_int32(0)
         _check(lib().fc_plan_info(self._h, key.encode(), ctypes.byref(v)))
         return v.value
