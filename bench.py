@@ -324,6 +324,11 @@ def config_dict(wl, parallelism):
             "l2": "inputs larger than L2 (per-iteration working set > 126 MB)"}
 
 
+def copies_table(world, sharded):
+    """How many times the phase table goes up per step (once per rank of a sharded run)."""
+    return world if sharded else 1
+
+
 def parallelism_label(world, wl, replicas):
     if world == 1:
         return "single"
@@ -603,53 +608,63 @@ def run_gpu(args):
         pin[...] = host.components
         field = SimpleNamespace(isotropic_values=pin[0] if host.isotropic_values is not None else None,
                                 components=pin)
-    elif wl.name == "cfg4" and gen_out is not None and gen_out[0] is not None:
+    elif wl.name == "cfg4" and gen_out is not None and gen_out[0] is not None and not args.scratch_labels:
         labels, grains = gen_out
         pin = torch.empty((6,) + wl.shape, dtype=torch.float64, pin_memory=True).numpy()
         for m in range(6):
             np.take(grains[:, m], labels, out=pin[m])
         del labels
         field = SimpleNamespace(isotropic_values=None, components=pin)
+    if wl.name == "cfg4" and (sharded or args.scratch_labels):
+        # the sharded generator keeps no labels: take the whole grid's from a scratch
+        # single-device context (every rank for itself), then release it
+        from paper_1311_0089_b200 import generators as gen
+
+        scratch = _native.Context(spec, local)
+        seeds, grains = gen.cfg4_grains(512, gen.SEEDS["cfg4"], wl.n)
+        gen_out = (scratch.generate_voronoi(seeds, grains, want_labels=True, compress=False), grains)
+        del scratch
     e2e = None
-    if field is not None:
-        e2e_steps = min(args.steps, args.e2e_steps)
-        h2d = field.components.nbytes if field.isotropic_values is None else field.isotropic_values.nbytes
-        h2d += wl.loads.nbytes
-        ctx.set_coefficients(field)
+    e2e_steps = min(args.steps, args.e2e_steps)
+    copies = 1 if sharded else world
+
+    def timed_e2e(upload):
+        upload()
         ctx.solve_cg(wl.loads, TOL, MAX_ITER, out=x_out)
         barrier(world)
         ctx.timer_mark(2)
         for _ in range(e2e_steps):
-            ctx.set_coefficients(field)
+            upload()
             ctx.solve_cg(wl.loads, TOL, MAX_ITER, out=x_out)
         ctx.timer_mark(3)
-        ms_e2e = max_over_ranks(world, ctx.timer_elapsed(2, 3))
-        copies = 1 if sharded else world
-        e2e = {"value": copies * wl.N * sum(res["iters"]) * e2e_steps / (ms_e2e / 1000.0), "unit": UNIT,
+        ms = max_over_ranks(world, ctx.timer_elapsed(2, 3))
+        return copies * wl.N * sum(res["iters"]) * e2e_steps / (ms / 1000.0)
+
+    if field is not None:
+        h2d = field.components.nbytes if field.isotropic_values is None else field.isotropic_values.nbytes
+        h2d += wl.loads.nbytes
+        e2e = {"value": timed_e2e(lambda: ctx.set_coefficients(field)), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(x_out.nbytes), "steps": e2e_steps,
-               "path": "Context.set_coefficients (pinned host field) + Context.solve_cg(out=pinned host array)"}
-        if wl.name == "cfg4" and gen_out is not None and gen_out[0] is not None and getattr(ctx, "n_phases", 0) > 0:
-            # the same step from the phase form a generator or segmentation holds:
-            # labels + table go up instead of the expanded field
-            lab16 = torch.empty(wl.shape, dtype=torch.uint16, pin_memory=True).numpy()
-            lab16[...] = gen_out[0]
-            table = np.ascontiguousarray(gen_out[1].T)
-            ctx.set_coefficients_indexed(lab16, table)
-            ctx.solve_cg(wl.loads, TOL, MAX_ITER, out=x_out)
-            barrier(world)
-            ctx.timer_mark(2)
-            for _ in range(e2e_steps):
-                ctx.set_coefficients_indexed(lab16, table)
-                ctx.solve_cg(wl.loads, TOL, MAX_ITER, out=x_out)
-            ctx.timer_mark(3)
-            ms_idx = max_over_ranks(world, ctx.timer_elapsed(2, 3))
-            e2e["indexed_upload"] = {
-                "value": copies * wl.N * sum(res["iters"]) * e2e_steps / (ms_idx / 1000.0), "unit": UNIT,
-                "h2d_bytes_per_step": int(lab16.nbytes + table.nbytes + wl.loads.nbytes),
-                "d2h_bytes_per_step": int(x_out.nbytes),
-                "path": "Context.set_coefficients_indexed (pinned uint16 labels + tensor table) + "
-                        "Context.solve_cg(out=pinned host array)"}
-            del lab16
+               "path": "Context.set_coefficients (pinned host field in the reference's packed layout, deduplicated on "
+                       "the device every step) + Context.solve_cg(out=pinned host array)"}
+    if wl.name == "cfg4" and gen_out is not None and gen_out[0] is not None and getattr(ctx, "n_phases", 0) > 0:
+        # the same step from the phase form a generator or segmentation holds: labels +
+        # table go up instead of the expanded field (sharded: the only host form small
+        # enough to keep per rank; every rank uploads its own planes)
+        lab16 = torch.empty(wl.shape, dtype=torch.uint16, pin_memory=True).numpy()
+        lab16[...] = gen_out[0]
+        table = np.ascontiguousarray(gen_out[1].T)
+        idx = {"value": timed_e2e(lambda: ctx.set_coefficients_indexed(lab16, table)), "unit": UNIT,
+               "h2d_bytes_per_step": int(lab16.nbytes + copies_table(world, sharded) * table.nbytes + wl.loads.nbytes),
+               "d2h_bytes_per_step": int(x_out.nbytes), "steps": e2e_steps,
+               "path": "Context.set_coefficients_indexed (pinned uint16 labels + tensor table) + "
+                       "Context.solve_cg(out=pinned host array)"}
+        if e2e is None:
+            e2e = idx
+        else:
+            e2e["indexed_upload"] = idx
+        del lab16
+    if field is not None:
         del field, pin
     del x_out
 
@@ -717,6 +732,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override the grid size (0 = BASELINE size)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scratch-labels", action="store_true",
+                    help="cfg4 on one GPU: take the e2e labels the way a sharded run does (scratch context), for testing")
     ap.add_argument("--no-others", action="store_true", help="skip the other single-GPU configurations")
     ap.add_argument("--profile-steps", type=int, default=3, help="steps of the per-kernel profiled region")
     ap.add_argument("--e2e-steps", type=int, default=5, help="steps of the e2e region (<= --steps)")
