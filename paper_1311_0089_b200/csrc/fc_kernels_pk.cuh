@@ -38,6 +38,12 @@ __host__ __device__ inline size_t pk_smem(int L, int C, int npk, int nbox, int b
 #ifndef FC_PK_IDX_LATE
 #define FC_PK_IDX_LATE 0  // experiment: table reads (L1 hits) in the compute loop, not held across the loads
 #endif
+#ifndef FC_PK_MINB
+#define FC_PK_MINB 2  // resident CTAs per SM the packed variant is compiled for
+#endif
+#ifndef FC_PK_K
+#define FC_PK_K 3
+#endif
 #ifndef FC_PK_IDX_MINB
 #define FC_PK_IDX_MINB 2  // resident CTAs per SM the indexed variant is compiled for
 #endif
@@ -46,7 +52,7 @@ __host__ __device__ inline size_t pk_smem(int L, int C, int npk, int nbox, int b
 #endif
 
 template <int L, int C, bool IDX>
-__global__ void __launch_bounds__(256, IDX ? FC_PK_IDX_MINB : 2) k_row_fwd_pk(Geo g, RowGeo rg, Coef Cf, InArgs ia, const RhsState* st,
+__global__ void __launch_bounds__(256, IDX ? FC_PK_IDX_MINB : FC_PK_MINB) k_row_fwd_pk(Geo g, RowGeo rg, Coef Cf, InArgs ia, const RhsState* st,
                                                        const double2* __restrict__ tw, int npk,
                                                        const __grid_constant__ CUtensorMap tmP) {
   constexpr int TP = RegTP<L>::value;
@@ -104,7 +110,7 @@ __global__ void __launch_bounds__(256, IDX ? FC_PK_IDX_MINB : 2) k_row_fwd_pk(Ge
   // voxels per thread in flight (all their loads issued first).  Measured at 729^3
   // (profiles/r02z_ab_pk_k.txt): 2 -> 13.73 ms, 3 -> 13.37 ms (a row pair of 729 is
   // exactly two rounds of 243 threads), 6 -> 32.9 ms (spills)
-  constexpr int K = IDX ? FC_PK_IDX_K : 3;
+  constexpr int K = IDX ? FC_PK_IDX_K : FC_PK_K;
   for (int e0 = threadIdx.x; e0 < n; e0 += K * blockDim.x) {
     double u[K][C], po[K][C], xo[K][C], am[K][NSYM];
     // indexed: the labels first, so their latency hides behind the field loads and

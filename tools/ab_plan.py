@@ -34,6 +34,6 @@ for var in variants:
     ctx.solve_cg(wl.loads, bench.TOL, bench.MAX_ITER, want_x=False)
     ctx.set_profiling(False)
     prof = ctx.profile()
-    ks = " ".join(f"{k}={v[1] / max(v[0], 1):.3f}" for k, v in prof.items() if not k.endswith("_rhs"))
+    ks = " ".join(f"{k}={v[1] / max(v[0], 1):.3f}" for k, v in prof.items() if not k.endswith("_rhs") or k == "row_fwd_rhs")
     print(f"{name} [{var or 'default'}] phases {ctx.n_phases} iterations {its} {ms / its:.4f} ms/iter | {ks}", flush=True)
     del ctx
