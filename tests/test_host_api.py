@@ -139,3 +139,32 @@ def test_pairwise_sum_runs_matches_numpy(rng):
     for counts in ([1], [7, 3], [128, 129], [1000, 1, 5000], [8191, 8193, 3]):
         vals = rng.standard_normal(len(counts))
         assert pairwise_sum_runs(vals, counts) == np.sum(np.repeat(vals, counts))
+
+
+def test_from_phases_is_the_gathered_field(rng):
+    """CoefficientField.from_phases: host-side the field is exactly what from_matrices
+    builds from the gathered tensors (material.py:135-145); the phase form rides along
+    for the device upload (uint16 labels + (nsym, n_phases) table)."""
+    spec = GridSpec((1.0, 2.0, 0.5), (5, 7, 3))
+    q = rng.standard_normal((4, 3, 3))
+    tensors = q @ np.swapaxes(q, 1, 2) + 0.5 * np.eye(3)
+    labels = rng.integers(0, 4, size=spec.shape)
+    a = CoefficientField.from_phases(spec, labels, tensors)
+    b = CoefficientField.from_matrices(spec, np.moveaxis(tensors[labels], (-2, -1), (0, 1)))
+    assert np.array_equal(a.components, b.components)
+    assert (a.c_A, a.C_A) == (b.c_A, b.C_A)
+    lab16, table = a.phases
+    assert lab16.dtype == np.uint16 and lab16.shape == spec.shape and table.shape == (6, 4)
+    assert np.array_equal(table[:, lab16], a.components)
+    assert b.phases is None
+    # isotropic phases stay on the scalar path; d = 1 has no packed kernels
+    iso = CoefficientField.from_phases(spec, labels, np.array([k + 1.0 for k in range(4)])[:, None, None] * np.eye(3))
+    assert iso.phases is None and iso.isotropic_values is not None
+    with pytest.raises(MaterialDataError):
+        CoefficientField.from_phases(spec, labels, tensors[:3])  # label 3 out of range
+    with pytest.raises(MaterialDataError):
+        CoefficientField.from_phases(spec, labels[:-1], tensors)
+    bad = tensors.copy()
+    bad[0, 0, 1] += 1.0
+    with pytest.raises(MaterialDataError):
+        CoefficientField.from_phases(spec, labels, bad)
