@@ -87,7 +87,7 @@ int32_t fc_device_count(int32_t* count);
  *   two_field (1)    d = 3, one slab: the outer sweep stores F0^-1 q once, the inverse middle
  *                    sweep rebuilds components 1 and 2 from it (0: three fields; same bits)
  *   fold_fwd (-1)    with two_field: the forward middle sweep stores xi1 v1 + xi2 v2 as one
- *                    field for the outer sweep (-1: for middle pencils >= 405; same bits)
+ *                    field for the outer sweep (-1: for middle pencils >= 243; same bits)
  *   defer_x (1)  CG x update deferred into the next first sweep
  *   fused_exchange (1)  in-process slabs store straight into the peers' buffers
  *   sync_debug (0)  synchronize after every launch

@@ -158,7 +158,7 @@ struct PlanOpts {
   int mid_tma_fwd = 1;     // forward middle sweep through TMA boxes (0: per-thread transposed stores)
   int aniso_fused = 1;     // packed coefficients: fused first sweep (0: pointwise kernel + row FFT)
   int two_field = 1;       // d = 3, one slab: two spectrum fields from the outer to the inverse middle sweep
-  int fold_fwd = -1;       // ... and from the forward middle sweep to the outer sweep (needs two_field; -1: middle pencils >= 405)
+  int fold_fwd = -1;       // ... and from the forward middle sweep to the outer sweep (needs two_field; -1: middle pencils >= 243)
   int inv_qpre = 1;        // last sweep: epilogue input staged by a bulk copy issued with the spectrum loads
   int fin_split = -1;      // reductions finalized by a separate launch (-1: from 1024 partial slots on)
   int defer_x = 1;         // CG x update deferred into the next first sweep
@@ -756,9 +756,9 @@ int make_row_tmap(fc_ctx* c) {
     }
   }
   c->two_field = c->dim == 3 && c->P == 1 && c->opt.two_field && c->mgi.tma && c->outer_qb && c->outer_seq && c->og.tma;
-  // (pencils of 405 and more: at 243, with 256-thread CTAs, the folding sweep loses more than the outer sweep gains)
+  // (middle pencils of 243 and more, measured; shorter ones keep three fields)
   c->fold_fwd = c->two_field && c->mg.tma && c->opt.mid_tma_fwd && c->mg.B * (c->n[1] / 9) <= fold_threads(c->n[1]) &&
-                (c->opt.fold_fwd >= 0 ? c->opt.fold_fwd != 0 : c->n[1] / 9 >= 45);
+                (c->opt.fold_fwd >= 0 ? c->opt.fold_fwd != 0 : c->n[1] / 9 >= 27);
   return FC_OK;
 }
 
